@@ -1,0 +1,115 @@
+/* sgb200 — C ABI of the B200 hot path for the ssagrad reference
+ * (arXiv 1811.01457 "Flux" reproduction, /root/reference/pkg/src/ssagrad).
+ *
+ * Every entry point takes plain pointers and sizes; no torch types cross
+ * this boundary.  Device pointers are CUDA device addresses, `stream` is a
+ * cudaStream_t (CUstream) or NULL for the legacy default stream.  The
+ * caller owns and allocates every input and output buffer; the library
+ * never frees caller memory (reference DenseTensor values are immutable
+ * and every op returns a fresh tensor, SPEC.md:195 / tensor.py:29-47).
+ *
+ * Status codes (mirroring the reference's Python exceptions):
+ *   SG_OK            0
+ *   SG_EDOMAIN       1  DomainError / EvalError   (tensor.py:25-26, interp.py:26-35)
+ *   SG_EINVAL        2  ValueError (shapes, arguments)    (tensor.py:118-119, 358-359)
+ *   SG_ECUDA         3  CUDA / NVRTC failure
+ *   SG_ENCCL         4  collective failure (reserved; DP uses torch.distributed/NCCL)
+ * sg_last_error() returns the message of the last failing call on this thread.
+ */
+#ifndef SGB200_H
+#define SGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SG_API __attribute__((visibility("default")))
+#else
+#define SG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_EDOMAIN 1
+#define SG_EINVAL 2
+#define SG_ECUDA 3
+#define SG_ENCCL 4
+
+/* element types */
+#define SG_F32 0
+#define SG_F64 1
+#define SG_BF16 2
+
+#define SG_MAX_DIMS 8
+
+/* A C-contiguous row-major tensor, or (ndim == 0) an f64 scalar by value.
+ * Replaces the reference runtime value `DenseTensor | float`
+ * (tensor.py:29-47; scalars are plain Python floats, interp.py:3-13). */
+typedef struct sg_tensor {
+  void* ptr;
+  int32_t dtype;
+  int32_t ndim;
+  int64_t shape[SG_MAX_DIMS];
+  double scalar;
+} sg_tensor;
+
+typedef struct sg_ctx sg_ctx;
+typedef struct sg_kernel sg_kernel;
+
+/* ---------------------------------------------------------------- context */
+SG_API int sg_version(void);
+SG_API int sg_create(int device, sg_ctx** out);
+SG_API int sg_destroy(sg_ctx* ctx);
+/* Copies the last error message of the calling thread into buf (NUL-terminated). */
+SG_API int sg_last_error(char* buf, size_t n);
+
+/* ------------------------------------------------------- fused broadcast
+ * Replaces the per-element interpreter of `fused_map` / `fused_pack`
+ * (interp.py:322-352, Machine.dispatch "fused_map"/"fused_pack" at
+ * interp.py:264-267) and the public API `fused_map_with_partials` /
+ * `fused_map_pullback` (forward_ad.py:194-235).
+ *
+ * sg_ew_compile registers the CUDA C++ lowering of one scalar IR function
+ * (device functions `sg_entry_p` / `sg_entry_d` produced by the host-side
+ * codegen) under `key`; variants for each broadcast pattern are JIT
+ * compiled with NVRTC for sm_100a on first use and cached.  k = number of
+ * sub-function arguments (<= 16), dtype = SG_F32 or SG_F64. */
+SG_API int sg_ew_compile(sg_ctx* ctx, const char* user_src, const char* key, int k, int dtype,
+                  sg_kernel** out);
+/* y = f.(args...) with trailing-aligned broadcasting (tensor.py:108-121). */
+SG_API int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_tensor* y,
+                  void* stream);
+/* argbars[i] = reduce_like(ybar .* d f/d arg_i, type(arg_i))  — the fused
+ * adjoint (rules.py:177-185 + tensor.py:327-345).  y may be NULL (no primal
+ * output) or receive the primal.  For an f64-scalar arg (ndim 0) the
+ * cotangent is written as one element of argbars[i].ptr (dtype of y).  */
+SG_API int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const sg_tensor* ybar,
+               sg_tensor* y, sg_tensor* argbars, void* stream);
+/* pack = [primal, d f/d arg_0, ...], shape (1+k, *out_shape): `fused_pack`. */
+SG_API int sg_ew_pack(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_tensor* pack,
+               void* stream);
+/* Synchronises `stream`, reads and clears the context's device error word.
+ * Returns SG_EDOMAIN and fills (*element, *site) when an element failed
+ * (lowest flat element index wins); SG_OK otherwise. */
+SG_API int sg_ew_check(sg_ctx* ctx, void* stream, int64_t* element, int32_t* site);
+/* Per-element step budget for sub-functions with loops (interp.py:23,113-122). */
+SG_API int sg_ew_set_step_limit(sg_ctx* ctx, int64_t limit);
+/* NVRTC-compiles one variant without touching a GPU (build checks on CPU
+ * hosts): kinds[i] in {0 full, 1 row, 2 col, 3 one-element, 4 by-value}. */
+SG_API int sg_ew_compile_only(const char* user_src, int k, int dtype, const int* kinds, int vec, int bdx,
+                              int bdy, size_t* cubin_bytes);
+/* Number of NVRTC variants compiled so far (introspection / tests). */
+SG_API int sg_ew_variant_count(sg_kernel* kern);
+
+/* out = reduce_to(a .* b, out_shape); b may be NULL.  The contraction of
+ * `fused_map_pullback` (forward_ad.py:232-235) and `reduce_to`
+ * (tensor.py:327-345) on the device; fp64 accumulation, fixed order. */
+SG_API int sg_reduce_to(sg_ctx* ctx, const sg_tensor* a, const sg_tensor* b, sg_tensor* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGB200_H */

@@ -1,0 +1,59 @@
+// Shared host-side helpers of the sgb200 runtime.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/sgb200.h"
+
+namespace sg {
+
+// Last error message of the calling thread (sg_last_error).
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+// Driver API entry points, resolved through cudart (no link-time libcuda
+// dependency, so the library also loads on hosts without a GPU driver).
+struct Driver {
+  CUresult (*moduleLoadData)(CUmodule*, const void*);
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*);
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, CUstream, void**, void**);
+  CUresult (*getErrorString)(CUresult, const char**);
+  CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+};
+// Returns nullptr (and sets the error) if the driver cannot be reached.
+const Driver* driver();
+
+inline int cu_fail(CUresult r, const char* what) {
+  const char* s = nullptr;
+  if (const Driver* d = driver()) d->getErrorString(r, &s);
+  return fail(SG_ECUDA, std::string(what) + ": " + (s ? s : "unknown driver error"));
+}
+
+inline size_t dtype_size(int dt) { return dt == SG_F64 ? 8 : (dt == SG_F32 ? 4 : 2); }
+
+inline long long numel(const sg_tensor& t) {
+  long long n = 1;
+  for (int i = 0; i < t.ndim; ++i) n *= t.shape[i];
+  return n;
+}
+
+}  // namespace sg
+
+#define SG_CUDA_TRY(expr)                                          \
+  do {                                                             \
+    cudaError_t e_ = (expr);                                       \
+    if (e_ != cudaSuccess) return ::sg::cuda_fail(e_, #expr);      \
+  } while (0)
+
+#define SG_CU_TRY(expr)                                            \
+  do {                                                             \
+    CUresult r_ = (expr);                                          \
+    if (r_ != CUDA_SUCCESS) return ::sg::cu_fail(r_, #expr);       \
+  } while (0)

@@ -1,0 +1,300 @@
+// Fused elementwise kernel skeleton (K1 forward, K2 gradient, pack).
+//
+// Compiled at run time by NVRTC together with the code generated from the
+// user's scalar IR function (codegen.py).  The host prepends:
+//   typedef float|double T;  #define SG_K <k>  #define SG_KT max(k,1)
+//   #define SG_VEC <1|2|4>   #define SG_KINDS {kind0, kind1, ...}
+//   #define SG_BDX/SG_BDY    (block shape, threads along C / along R)
+// and this file's kernels are instantiated for that combination.
+//
+// Layout: canonical 2-D grid out[R][C]; thread (tx, ty) of block (bx, by)
+// owns SG_VEC consecutive columns c = (bx*SG_BDX + tx)*SG_VEC and walks rows
+// r = by*rows_per_block + ty, ... with stride SG_BDY.  A thread therefore
+// keeps the same columns for its whole life, which is what lets the
+// gradient kernel accumulate broadcast-axis sums (ROW operands, e.g. the
+// bias vector) in fp64 registers and write one deterministic partial per
+// (row-thread, column); COL operands (shape (R,1)) are reduced across the
+// columns of a row with warp shuffles.
+//
+// Reference semantics: element e of the output is f(args[e']) for the
+// trailing-aligned broadcast of interp.py:322-332; the gradient writes
+// reduce_like(ybar * d f/d arg_i, type_i) (forward_ad.py:226-235,
+// rules.py:177-185) without materialising the (1+K)-row pack.
+
+#define SG_UNROLL 4
+
+struct D { T p; T t[SG_KT]; };
+
+#if defined(SG_T_IS_DOUBLE)
+__device__ __forceinline__ T sg_exp(T x) { return exp(x); }
+__device__ __forceinline__ T sg_log(T x) { return log(x); }
+__device__ __forceinline__ T sg_tanh(T x) { return tanh(x); }
+#else
+__device__ __forceinline__ T sg_exp(T x) { return expf(x); }
+__device__ __forceinline__ T sg_log(T x) { return logf(x); }
+__device__ __forceinline__ T sg_tanh(T x) { return tanhf(x); }
+#endif
+
+// ---- vector access helpers (SG_VEC * sizeof(T) is 4, 8 or 16 bytes)
+#if defined(SG_T_IS_DOUBLE)
+#if SG_VEC == 2
+typedef double2 SgRaw;
+#else
+typedef double SgRaw;
+#endif
+#else
+#if SG_VEC == 4
+typedef float4 SgRaw;
+#elif SG_VEC == 2
+typedef float2 SgRaw;
+#else
+typedef float SgRaw;
+#endif
+#endif
+
+struct __align__(sizeof(SgRaw)) VT { T v[SG_VEC]; };
+
+__device__ __forceinline__ VT sg_from_raw(const SgRaw& w) {
+  static_assert(sizeof(SgRaw) == sizeof(VT), "vector width");
+  return *reinterpret_cast<const VT*>(&w);
+}
+__device__ __forceinline__ SgRaw sg_to_raw(const VT& v) { return *reinterpret_cast<const SgRaw*>(&v); }
+// operands read once per element: streaming (evict-first) loads
+__device__ __forceinline__ VT sg_ldv_stream(const T* p) {
+  return sg_from_raw(__ldcs(reinterpret_cast<const SgRaw*>(p)));
+}
+// broadcast vectors (bias-like, re-read by every row): cached loads
+__device__ __forceinline__ VT sg_ldv(const T* p) {
+  return sg_from_raw(__ldg(reinterpret_cast<const SgRaw*>(p)));
+}
+__device__ __forceinline__ void sg_stv(T* p, const VT& v) {
+  __stcs(reinterpret_cast<SgRaw*>(p), sg_to_raw(v));
+}
+
+__device__ __forceinline__ void sg_publish_error(unsigned long long* err, long long elem, int site) {
+  unsigned long long w = ((unsigned long long)elem << 24) | (unsigned long long)(site & 0xffffff);
+  atomicMin(err, w);
+}
+
+static __device__ const int sg_kinds[SG_KT] = SG_KINDS;
+
+// Load operand i for rows r, columns c..c+SG_VEC-1.
+__device__ __forceinline__ void sg_load_operand(const SgEwParams& p, int i, long long r, long long c,
+                                                T (&x)[SG_VEC]) {
+  const int kind = sg_kinds[i];
+  const T* base = reinterpret_cast<const T*>(p.in[i]);
+  if (kind == SG_FULL) {
+    VT v = sg_ldv_stream(base + r * p.C + c);
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) x[j] = v.v[j];
+  } else if (kind == SG_ROW) {
+    VT v = sg_ldv(base + c);
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) x[j] = v.v[j];
+  } else if (kind == SG_COL) {
+    T s = base[r];
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
+  } else if (kind == SG_SPTR) {
+    T s = base[0];
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
+  } else {
+    T s = (T)p.sval[i];
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
+  }
+}
+
+__device__ __forceinline__ long long sg_row_begin(const SgEwParams& p) {
+  return (long long)blockIdx.y * p.rows_per_block;
+}
+__device__ __forceinline__ long long sg_row_end(const SgEwParams& p) {
+  long long e = ((long long)blockIdx.y + 1) * p.rows_per_block;
+  return e < p.R ? e : p.R;
+}
+
+// --------------------------------------------------------------- K1: forward
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+sg_ew_forward(const SgEwParams p) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
+  if (c >= p.C) return;
+  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  T* out = reinterpret_cast<T*>(p.out);
+  for (long long rb = r0 + ty; rb < r1; rb += (long long)SG_BDY * SG_UNROLL) {
+    T xs[SG_UNROLL][SG_KT][SG_VEC];
+#pragma unroll
+    for (int u = 0; u < SG_UNROLL; ++u) {
+      const long long r = rb + (long long)u * SG_BDY;
+      if (r < r1) {
+#pragma unroll
+        for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[u][i]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SG_UNROLL; ++u) {
+      const long long r = rb + (long long)u * SG_BDY;
+      if (r >= r1) break;
+      VT y;
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) {
+        T a[SG_KT];
+#pragma unroll
+        for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? xs[u][i][j] : (T)0;
+        int err = 0;
+        long long steps = p.step_limit;
+        sg_entry_p(a, y.v[j], err, steps);
+        if (err) sg_publish_error(p.err, r * p.C + c + j, err);
+      }
+      sg_stv(out + r * p.C + c, y);
+    }
+  }
+}
+
+// ------------------------------------------------------ K2: fused gradient
+// Recomputes the duals from the inputs, writes xbar for full operands and
+// fp64 partial sums for broadcast operands.  Partial layouts:
+//   SG_ROW:              part[(by*SG_BDY + ty) * C + c]      (G_row = gy*SG_BDY rows)
+//   SG_COL:              part[g * R + r], g = lane-group column id
+//   SG_SPTR / SG_SVAL:   part[by * gx + bx]                  (block partial)
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+sg_ew_grad(const SgEwParams p) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
+  const bool active = c < p.C;
+  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const T* ybar = reinterpret_cast<const T*>(p.ybar);
+  T* out = reinterpret_cast<T*>(p.out);
+
+  double rowacc[SG_KT][SG_VEC];   // ROW operands: per-column sums over my rows
+  double sacc[SG_KT];             // scalar operands: sums over everything I see
+#pragma unroll
+  for (int i = 0; i < SG_KT; ++i) {
+    sacc[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) rowacc[i][j] = 0.0;
+  }
+  // lanes of one warp that share a row (COL reductions): SG_BDX >= 32 -> whole warp
+  constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
+
+  const long long rows_span = r1 > r0 ? (r1 - r0 + SG_BDY - 1) / SG_BDY : 0;
+  for (long long it = 0; it < rows_span; it += SG_UNROLL) {
+    T xs[SG_UNROLL][SG_KT][SG_VEC];
+    T yb[SG_UNROLL][SG_VEC];
+#pragma unroll
+    for (int u = 0; u < SG_UNROLL; ++u) {
+      const long long r = r0 + ty + (it + u) * SG_BDY;
+      if (active && r < r1 && it + u < rows_span) {
+#pragma unroll
+        for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[u][i]);
+        VT v = sg_ldv_stream(ybar + r * p.C + c);
+#pragma unroll
+        for (int j = 0; j < SG_VEC; ++j) yb[u][j] = v.v[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SG_UNROLL; ++u) {
+      if (it + u >= rows_span) break;   // uniform across the block
+      const long long r = r0 + ty + (it + u) * SG_BDY;
+      const bool live = active && r < r1;
+      double colsum[SG_KT];
+#pragma unroll
+      for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
+      if (live) {
+        VT y, g[SG_KT];
+#pragma unroll
+        for (int j = 0; j < SG_VEC; ++j) {
+          T a[SG_KT], d[SG_KT];
+#pragma unroll
+          for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? xs[u][i][j] : (T)0;
+          int err = 0;
+          long long steps = p.step_limit;
+          sg_entry_d(a, y.v[j], d, err, steps);
+          if (err) sg_publish_error(p.err, r * p.C + c + j, err);
+#pragma unroll
+          for (int i = 0; i < SG_K; ++i) {
+            const T contrib = yb[u][j] * d[i];   // ybar ⊙ partial_i (forward_ad.py:233)
+            const int kind = sg_kinds[i];
+            if (kind == SG_FULL) g[i].v[j] = contrib;
+            else if (kind == SG_ROW) rowacc[i][j] += (double)contrib;
+            else if (kind == SG_COL) colsum[i] += (double)contrib;
+            else sacc[i] += (double)contrib;
+          }
+        }
+        if (out) sg_stv(out + r * p.C + c, y);
+#pragma unroll
+        for (int i = 0; i < SG_K; ++i)
+          if (sg_kinds[i] == SG_FULL) sg_stv(reinterpret_cast<T*>(p.xbar[i]) + r * p.C + c, g[i]);
+      }
+      // row reductions for COL operands: lanes with the same ty share row r
+#pragma unroll
+      for (int i = 0; i < SG_K; ++i) {
+        if (sg_kinds[i] != SG_COL) continue;
+        double s = colsum[i];
+#pragma unroll
+        for (int off = kGroup / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, kGroup);
+        if (live && (tx % kGroup) == 0) {
+          const long long g = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
+          p.part[i][g * p.R + r] = s;
+        }
+      }
+    }
+  }
+  // ROW partials: one row of partials per row-thread
+#pragma unroll
+  for (int i = 0; i < SG_K; ++i) {
+    if (sg_kinds[i] != SG_ROW || !active) continue;
+    const long long g = (long long)blockIdx.y * SG_BDY + ty;
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) p.part[i][g * p.C + c + j] = rowacc[i][j];
+  }
+  // scalar partials: block tree reduction in a fixed order
+  __shared__ double red[SG_BDX * SG_BDY];
+  const int tid = ty * SG_BDX + tx;
+#pragma unroll
+  for (int i = 0; i < SG_K; ++i) {
+    if (sg_kinds[i] != SG_SPTR && sg_kinds[i] != SG_SVAL) continue;
+    red[tid] = active ? sacc[i] : 0.0;
+    __syncthreads();
+    for (int s = (SG_BDX * SG_BDY) / 2; s > 0; s >>= 1) {
+      if (tid < s) red[tid] += red[tid + s];
+      __syncthreads();
+    }
+    if (tid == 0) p.part[i][(long long)blockIdx.y * gridDim.x + blockIdx.x] = red[0];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- pack
+// fused_pack layout of interp.py:334-352: pack[0] = primal, pack[1+i] = d f/d arg_i.
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+sg_ew_pack(const SgEwParams p) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
+  if (c >= p.C) return;
+  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const long long plane = p.R * p.C;
+  T* pk = reinterpret_cast<T*>(p.pack);
+  for (long long r = r0 + ty; r < r1; r += SG_BDY) {
+    T xs[SG_KT][SG_VEC];
+#pragma unroll
+    for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[i]);
+    VT y, g[SG_KT];
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) {
+      T a[SG_KT], d[SG_KT];
+#pragma unroll
+      for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? xs[i][j] : (T)0;
+      int err = 0;
+      long long steps = p.step_limit;
+      sg_entry_d(a, y.v[j], d, err, steps);
+      if (err) sg_publish_error(p.err, r * p.C + c + j, err);
+#pragma unroll
+      for (int i = 0; i < SG_KT; ++i) g[i].v[j] = d[i];
+    }
+    sg_stv(pk + r * p.C + c, y);
+#pragma unroll
+    for (int i = 0; i < SG_K; ++i) sg_stv(pk + (long long)(1 + i) * plane + r * p.C + c, g[i]);
+  }
+}

@@ -1,0 +1,184 @@
+// Precompiled reduction / broadcast helpers used around the fused kernels.
+//
+//  * sum of fp64 partials written by the fused gradient kernel, in a fixed
+//    order (deterministic, like the reference's sequential cumsum folds,
+//    tensor.py:287-345 — the order differs, the result is reproducible);
+//  * generic broadcast materialisation for patterns that do not collapse
+//    to the 2-D fast path;
+//  * generic reduce_to(a .* b) for `fused_map_pullback` (forward_ad.py:226-235).
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "reduce_kernels.h"
+
+namespace sg {
+
+namespace {
+
+template <class T>
+__global__ void k_sum_cols(const double* __restrict__ part, long long G, long long N, T* __restrict__ out) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N;
+       j += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (long long g = 0; g < G; ++g) acc += part[g * N + j];
+    out[j] = (T)acc;
+  }
+}
+
+// One block per output column; strided partial sums then a fixed tree.
+template <class T>
+__global__ void __launch_bounds__(256) k_sum_block(const double* __restrict__ part, long long G, long long N,
+                                                   T* __restrict__ out) {
+  __shared__ double red[256];
+  for (long long j = blockIdx.x; j < N; j += gridDim.x) {
+    double acc = 0.0;
+    for (long long g = threadIdx.x; g < G; g += 256) acc += part[g * N + j];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = (T)red[0];
+    __syncthreads();
+  }
+}
+
+template <class T>
+__global__ void k_expand(const T* __restrict__ in, T* __restrict__ out, long long n, DimMap m) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long rem = e, off = 0;
+    for (int d = m.nd - 1; d >= 0; --d) {
+      long long q = rem / m.ext[d];
+      long long cd = rem - q * m.ext[d];
+      rem = q;
+      off += cd * m.stride[d];
+    }
+    out[e] = in[off];
+  }
+}
+
+// out[o] = sum_j a[off(o,j)] * b[off(o,j)], block per output
+template <class T>
+__global__ void __launch_bounds__(256) k_reduce_block(const T* __restrict__ a, const T* __restrict__ b,
+                                                      T* __restrict__ out, long long n_out, long long n_red,
+                                                      DimMap kept, DimMap red_map) {
+  __shared__ double red[256];
+  for (long long o = blockIdx.x; o < n_out; o += gridDim.x) {
+    long long rem = o, base = 0;
+    for (int d = kept.nd - 1; d >= 0; --d) {
+      long long q = rem / kept.ext[d];
+      base += (rem - q * kept.ext[d]) * kept.stride[d];
+      rem = q;
+    }
+    double acc = 0.0;
+    for (long long j = threadIdx.x; j < n_red; j += 256) {
+      long long r2 = j, off = base;
+      for (int d = red_map.nd - 1; d >= 0; --d) {
+        long long q = r2 / red_map.ext[d];
+        off += (r2 - q * red_map.ext[d]) * red_map.stride[d];
+        r2 = q;
+      }
+      double v = (double)a[off];
+      if (b) v *= (double)b[off];
+      acc += v;
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[o] = (T)red[0];
+    __syncthreads();
+  }
+}
+
+// thread per output, sequential ascending fold (small reduction extents)
+template <class T>
+__global__ void k_reduce_thread(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                                long long n_out, long long n_red, DimMap kept, DimMap red_map) {
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n_out;
+       o += (long long)gridDim.x * blockDim.x) {
+    long long rem = o, base = 0;
+    for (int d = kept.nd - 1; d >= 0; --d) {
+      long long q = rem / kept.ext[d];
+      base += (rem - q * kept.ext[d]) * kept.stride[d];
+      rem = q;
+    }
+    double acc = 0.0;
+    for (long long j = 0; j < n_red; ++j) {
+      long long r2 = j, off = base;
+      for (int d = red_map.nd - 1; d >= 0; --d) {
+        long long q = r2 / red_map.ext[d];
+        off += (r2 - q * red_map.ext[d]) * red_map.stride[d];
+        r2 = q;
+      }
+      double v = (double)a[off];
+      if (b) v *= (double)b[off];
+      acc += v;
+    }
+    out[o] = (T)acc;
+  }
+}
+
+inline int grid_for(long long n, int block, int cap) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+
+int launch_sum_partials(const double* part, long long G, long long N, void* out, int dtype,
+                        cudaStream_t s) {
+  const bool blockwise = N < 4096 && G >= 64;
+  if (dtype == SG_F32) {
+    if (blockwise)
+      k_sum_block<float><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (float*)out);
+    else
+      k_sum_cols<float><<<grid_for(N, 256, 4096), 256, 0, s>>>(part, G, N, (float*)out);
+  } else {
+    if (blockwise)
+      k_sum_block<double><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (double*)out);
+    else
+      k_sum_cols<double><<<grid_for(N, 256, 4096), 256, 0, s>>>(part, G, N, (double*)out);
+  }
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int launch_expand(const void* in, void* out, long long n, const DimMap& m, int dtype, cudaStream_t s) {
+  if (dtype == SG_F32)
+    k_expand<float><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>((const float*)in, (float*)out, n, m);
+  else
+    k_expand<double><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>((const double*)in, (double*)out, n, m);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int launch_reduce(const void* a, const void* b, void* out, long long n_out, long long n_red,
+                  const DimMap& kept, const DimMap& red, int dtype, cudaStream_t s) {
+  const bool per_thread = n_red <= 64;
+  if (dtype == SG_F32) {
+    if (per_thread)
+      k_reduce_thread<float><<<grid_for(n_out, 256, 148 * 16), 256, 0, s>>>(
+          (const float*)a, (const float*)b, (float*)out, n_out, n_red, kept, red);
+    else
+      k_reduce_block<float><<<grid_for(n_out, 1, 148 * 16), 256, 0, s>>>(
+          (const float*)a, (const float*)b, (float*)out, n_out, n_red, kept, red);
+  } else {
+    if (per_thread)
+      k_reduce_thread<double><<<grid_for(n_out, 256, 148 * 16), 256, 0, s>>>(
+          (const double*)a, (const double*)b, (double*)out, n_out, n_red, kept, red);
+    else
+      k_reduce_block<double><<<grid_for(n_out, 1, 148 * 16), 256, 0, s>>>(
+          (const double*)a, (const double*)b, (double*)out, n_out, n_red, kept, red);
+  }
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+}  // namespace sg

@@ -1,0 +1,225 @@
+"""Generate golden vectors by running the UNMODIFIED reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference (pure Python + numpy) is importable here but does not travel
+to the GPU box, so its outputs are frozen into the small fixtures next to
+this script.  Everything is seeded; re-running reproduces the files
+bit for bit.  Inputs are float32-representable so the same fixtures serve
+the f32 and f64 device paths.
+
+Reference entry points exercised (all under /root/reference/pkg/src/ssagrad):
+  forward_ad.fused_map_with_partials / fused_map_pullback (forward_ad.py:194-235)
+  interp.Machine fused_map and EvalError sites (interp.py:95-138, 322-332)
+  reverse_ad.grad through fused_map and Dense IR (reverse_ad.py:633-663)
+  tensor.matmul / reduce_to (tensor.py:327-361)
+  nn_train-style Dense chains built with SEmitter (nn_train.py:189-227)
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import random
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from ssagrad import DenseTensor, Machine, Module, grad, parse_ir  # noqa: E402
+from ssagrad import tensor as T  # noqa: E402
+from ssagrad.forward_ad import fused_map_pullback, fused_map_with_partials  # noqa: E402
+from ssagrad.interp import EvalError  # noqa: E402
+from ssagrad.ir import F64, tensor_type  # noqa: E402
+from ssagrad.structure import SEmitter, flatten  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+from fused_src import FUSED_SRC  # noqa: E402
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def dt(shape, rng, lo=-2.0, hi=2.0):
+    return DenseTensor(f32(rng.uniform(lo, hi, size=shape)))
+
+
+def enc(v):
+    if isinstance(v, DenseTensor):
+        return {"shape": list(v.shape), "data": v.flat()}
+    return float(v)
+
+
+# ------------------------------------------------------------------ fused
+def fused_cases():
+    m = parse_ir(FUSED_SRC)
+    rng = np.random.default_rng(11)
+    cases = []
+    plans = [
+        ("two", [(4,), ()]), ("two", [(2, 3), (2, 3)]), ("two", [(2, 1), (3,)]),
+        ("two", [(), ()]), ("sgau", [(3, 3), ()]), ("sgau", [(6,), (6,)]),
+        ("poly", [(5,)]), ("branchy", [(9,)]), ("gauss", [(4,), ()]),
+        ("affsig", [(3,), (5, 3), (3,)]), ("affsig", [(), (4, 6), ()]),
+        ("affsig", [(4, 1), (4, 6), (1, 6)]), ("affsig", [(2, 1, 3), (2, 4, 3), (4, 1)]),
+        ("cubeloop", [(7,)]), ("powloop3", [(2, 5)]), ("relusq", [(8,)]),
+        ("pick", [(6,), (6,)]), ("callin", [(5,)]), ("divy", [(4,), (4,)]),
+        ("mixed", [(3, 4), (4,), ()]), ("logp", [(6,)]),
+    ]
+    for name, shapes in plans:
+        args = []
+        for s in shapes:
+            if s == ():
+                args.append(float(f32(rng.uniform(-2, 2))))
+            else:
+                lo = 0.1 if name == "logp" else -2.0
+                args.append(dt(s, rng, lo=lo))
+        if name == "branchy":  # keep clear of the branch point
+            a = args[0].data.copy()
+            a[np.abs(a) < 0.05] = 0.5
+            args[0] = DenseTensor(a)
+        primal, parts = fused_map_with_partials(m, name, tuple(args))
+        shp = primal.shape if isinstance(primal, DenseTensor) else ()
+        ybar = dt(shp, rng, -1, 1) if shp else None
+        types = [tensor_type(*a.shape) if isinstance(a, DenseTensor) else F64 for a in args]
+        pb = fused_map_pullback(parts, types, ybar) if ybar is not None else None
+        cases.append({
+            "fn": name,
+            "args": [enc(a) for a in args],
+            "primal": enc(primal),
+            "partials": [enc(p) for p in parts],
+            "ybar": enc(ybar) if ybar is not None else None,
+            "pullback": [enc(c) for c in pb] if pb is not None else None,
+        })
+    # reverse mode through fused_map (test_forward_ad.py:164-172 analogue)
+    x = DenseTensor(f32([0.2, -0.9, 1.4, 0.05]))
+    g = grad(m, "mapped", (x, 0.7))
+    mfn = m.get("mapped")
+    grads = {"x": enc(g[mfn.params[0][0]]), "b": enc(g[mfn.params[1][0]])}
+    # domain errors: reference EvalError location of the first failing element
+    errors = []
+    for name, vals in (("logp", [0.5, 2.0, -1.0, 3.0, -2.0]), ("divy", None)):
+        if name == "logp":
+            args = (DenseTensor(f32(vals)),)
+        else:
+            args = (DenseTensor(f32([1.0, 2.0, 3.0])), DenseTensor(f32([1.0, 0.0, 2.0])))
+        try:
+            fused_map_with_partials(m, name, args)
+            raise AssertionError("expected EvalError")
+        except EvalError as e:
+            errors.append({"fn": name, "args": [enc(a) for a in args], "function": e.function,
+                           "block": e.block, "index": e.index, "message": e.message})
+    return {"cases": cases, "grad_mapped": grads, "errors": errors}
+
+
+# ----------------------------------------------------------------- tensor
+def tensor_cases():
+    rng = np.random.default_rng(5)
+    out = {}
+    for i, (m_, k_, n_) in enumerate([(7, 13, 5), (33, 64, 17), (16, 100, 24)]):
+        a = f32(rng.uniform(-1, 1, (m_, k_)))
+        b = f32(rng.uniform(-1, 1, (k_, n_)))
+        out[f"mm{i}_a"], out[f"mm{i}_b"] = a, b
+        out[f"mm{i}_c"] = T.matmul(DenseTensor(a), DenseTensor(b)).data
+    x = f32(rng.uniform(-1, 1, (6, 4, 5)))
+    out["rt_x"] = x
+    out["rt_to_5"] = T.reduce_to(DenseTensor(x), (5,)).data
+    out["rt_to_415"] = T.reduce_to(DenseTensor(x), (4, 1)).data
+    out["rt_to_145"] = T.reduce_to(DenseTensor(x), (1, 4, 5)).data
+    out["rt_to_all"] = np.array([T.reduce_to(DenseTensor(x), ())])
+    return out
+
+
+# ------------------------------------------------------------ dense chains
+def build_chain_loss(module, name, sizes, acts, n, loss):
+    """Emit the loss of a Dense chain exactly as nn_train builds layers."""
+    em = SEmitter(name, (F64,), module)
+    pairs = []
+    for k in range(len(sizes) - 1):
+        w = em.param(f"W{k}", tensor_type(sizes[k + 1], sizes[k]))
+        b = em.param(f"b{k}", tensor_type(sizes[k + 1]))
+        pairs.append((w, b))
+    x = em.param("X", tensor_type(n, sizes[0]))
+    y = em.param("Y", tensor_type(n, sizes[-1]))
+    h = x
+    for (w, b), act in zip(pairs, acts):  # nn_train.py:189-196
+        wt = em.emit("transpose", (w,), None, "wt")
+        z = em.emit("matmul", (h, wt), None, "z")
+        zb = em.emit("add", (z, b), None, "zb")
+        h = zb if act == "identity" else em.emit(act, (zb,), None, "h")
+    if loss == "softmax_xent":  # SURVEY §8(d) c1 loss IR
+        e = em.emit("exp", (h,), None, "e")
+        s = em.emit("reduce_sum", (e,), {"axis": 1}, "s")
+        s2 = em.emit("reshape", (s,), {"shape": (n, 1)}, "s2")
+        p = em.emit("div", (e, s2), None, "p")
+        lp = em.emit("log", (p,), None, "lp")
+        t = em.emit("mul", (y, lp), None, "t")
+        tot = em.emit("reduce_sum", (t,), {"axis": "all"}, "tot")
+        sc = em.const_f64(-1.0 / n, "sc")
+    elif loss == "mse":
+        d = em.emit("sub", (h, y), None, "d")
+        sq = em.emit("mul", (d, d), None, "sq")
+        tot = em.emit("reduce_sum", (sq,), {"axis": "all"}, "tot")
+        sc = em.const_f64(1.0 / n, "sc")
+    else:  # "dot": loss = sum(h * Y), i.e. pull back the seed Y through the chain
+        t = em.emit("mul", (h, y), None, "t")
+        tot = em.emit("reduce_sum", (t,), {"axis": "all"}, "tot")
+        sc = em.const_f64(1.0, "sc")
+    l = em.emit("mul", (tot, sc), None, "loss")
+    module.add(flatten(em.finish((l,))))
+
+
+def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot"):
+    rng = np.random.default_rng(seed)
+    module = Module()
+    build_chain_loss(module, "chain", sizes, acts, n, loss)
+    params = []
+    for k in range(len(sizes) - 1):
+        fi, fo = sizes[k], sizes[k + 1]
+        r = np.sqrt(6.0 / (fi + fo))  # init_params, nn_train.py:130-140
+        W = f32(rng.uniform(-r, r, (fo, fi)))
+        b = f32(rng.uniform(-0.1, 0.1, fo))
+        params.append((W, b))
+    X = f32(rng.uniform(0, 1, (n, sizes[0])))
+    if y_kind == "onehot":
+        Y = np.zeros((n, sizes[-1]))
+        Y[np.arange(n), rng.integers(0, sizes[-1], n)] = 1.0
+    else:
+        Y = f32(rng.uniform(-1, 1, (n, sizes[-1])))
+    args = []
+    for W, b in params:
+        args += [DenseTensor(W), DenseTensor(b)]
+    args += [DenseTensor(X), DenseTensor(Y)]
+    loss_v = Machine(module).call("chain", tuple(args))[0]
+    g = grad(module, "chain", tuple(args))
+    fn = module.get("chain")
+    # inputs are float32-representable: store them as float32 (exact)
+    out = {"X": X.astype(np.float32), "Y": Y.astype(np.float32), "loss": np.array([loss_v]),
+           "sizes": np.array(sizes), "lr": np.array([lr])}
+    for k, (W, b) in enumerate(params):
+        out[f"W{k}"], out[f"b{k}"] = W.astype(np.float32), b.astype(np.float32)
+        gW = g[fn.params[2 * k][0]].data
+        gb = g[fn.params[2 * k + 1][0]].data
+        out[f"dW{k}"], out[f"db{k}"] = gW, gb
+    out["dX"] = g[fn.params[2 * len(params)][0]].data
+    return out
+
+
+def main():
+    with open(os.path.join(HERE, "fused.json"), "w") as f:
+        json.dump(fused_cases(), f, indent=0)
+    np.savez_compressed(os.path.join(HERE, "tensor.npz"), **tensor_cases())
+    np.savez_compressed(os.path.join(HERE, "mlp_c1_b32.npz"),
+                        **chain_case((784, 32, 10), ("sigmoid", "identity"), 32, "softmax_xent", 1))
+    np.savez_compressed(os.path.join(HERE, "mlp_mse.npz"),
+                        **chain_case((24, 24, 24, 24), ("tanh", "tanh", "identity"), 16, "mse", 2,
+                                     y_kind="uniform"))
+    np.savez_compressed(os.path.join(HERE, "dense_sigmoid.npz"),
+                        **chain_case((40, 24), ("sigmoid",), 16, "dot", 3, y_kind="uniform"))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

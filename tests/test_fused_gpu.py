@@ -1,0 +1,188 @@
+"""GPU parity of the fused broadcast kernels against the reference.
+
+Golden vectors come from the unmodified reference (tests/golden); larger
+cases are checked against the pinned oracle.  Tolerances (rel metric of
+the reference suite, pkg/tests/conftest.py:137-144):
+  f64 device path: 1e-13 (only libm ulps differ; + - * / round like Python),
+  f32 device path: 1e-6 (BASELINE.json north star, fp32 elementwise).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import decode, max_rel
+from oracle import scalar as OS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1811_01457_b200 import fused as F  # noqa: E402
+from paper_1811_01457_b200.ir import F64, tensor_type  # noqa: E402
+
+TOL = {torch.float64: 1e-13, torch.float32: 1e-6}
+
+
+def dev_args(case, dtype):
+    out = []
+    for a in case["args"]:
+        v = decode(a)
+        out.append(torch.tensor(v, dtype=dtype, device="cuda") if isinstance(v, np.ndarray) else v)
+    return out
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_partials_match_reference(golden_fused, fused_module, dtype):
+    for case in golden_fused["cases"]:
+        args = dev_args(case, dtype)
+        if not any(isinstance(a, torch.Tensor) for a in args):
+            args = [float(a) for a in args]
+        primal, parts = F.fused_map_with_partials(fused_module, case["fn"], args, dtype=dtype)
+        assert max_rel(primal, decode(case["primal"])) <= TOL[dtype], case["fn"]
+        for p, g in zip(parts, case["partials"]):
+            assert max_rel(p, decode(g)) <= TOL[dtype], case["fn"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_forward_matches_reference(golden_fused, fused_module, dtype):
+    for case in golden_fused["cases"]:
+        args = dev_args(case, dtype)
+        y = F.fused_map(fused_module, case["fn"], args, dtype=dtype)
+        assert max_rel(y, decode(case["primal"])) <= TOL[dtype], case["fn"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fused_grad_matches_reference_pullback(golden_fused, fused_module, dtype):
+    # K2 computes reduce_like(ybar * partial_i) directly from the inputs
+    for case in golden_fused["cases"]:
+        if case["pullback"] is None:
+            continue
+        args = dev_args(case, dtype)
+        ybar = torch.tensor(decode(case["ybar"]), dtype=dtype, device="cuda")
+        y, cots = F.fused_map_grad(fused_module, case["fn"], args, ybar, want_primal=True)
+        assert max_rel(y, decode(case["primal"])) <= TOL[dtype], case["fn"]
+        for c, want, a in zip(cots, case["pullback"], args):
+            w = decode(want)
+            if isinstance(a, float):
+                assert max_rel(float(c.item()), w) <= TOL[dtype], case["fn"]
+            else:
+                assert tuple(c.shape) == tuple(np.shape(w)), case["fn"]
+                assert max_rel(c, w) <= TOL[dtype], case["fn"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_pullback_api_matches_reference(golden_fused, fused_module, dtype):
+    for case in golden_fused["cases"]:
+        if case["pullback"] is None:
+            continue
+        args = dev_args(case, dtype)
+        _, parts = F.fused_map_with_partials(fused_module, case["fn"], args, dtype=dtype)
+        types = [tensor_type(*a.shape) if isinstance(a, torch.Tensor) else F64 for a in args]
+        ybar = torch.tensor(decode(case["ybar"]), dtype=dtype, device="cuda")
+        got = F.fused_map_pullback(parts, types, ybar)
+        for g, want in zip(got, case["pullback"]):
+            assert max_rel(g, decode(want)) <= TOL[dtype], case["fn"]
+
+
+def test_domain_errors_raise_reference_eval_error(golden_fused, fused_module):
+    for err in golden_fused["errors"]:
+        args = dev_args(err, torch.float64)
+        with pytest.raises(F.EvalError) as ei:
+            F.fused_map_with_partials(fused_module, err["fn"], args)
+        e = ei.value
+        assert (e.function, e.block, e.index) == (err["function"], err["block"], err["index"])
+        assert err["message"].startswith(e.message)
+    # the error word is cleared: a clean call afterwards succeeds
+    F.fused_map(fused_module, "logp", [torch.ones(4, dtype=torch.float64, device="cuda")])
+
+
+def test_step_limit_on_runaway_loop():
+    from paper_1811_01457_b200.irtext import parse_ir
+
+    m = parse_ir("""
+func @spin(%x: f64) -> f64 {
+^entry:
+  jmp ^loop(%x)
+^loop(%v: f64):
+  %t = const bool true
+  br %t, ^loop(%v), ^out(%v)
+^out(%r: f64):
+  ret %r
+}
+""")
+    F.set_step_limit(10_000)
+    try:
+        with pytest.raises(F.EvalError) as ei:
+            F.fused_map(m, "spin", [torch.ones(8, device="cuda")])
+        assert ei.value.message == "step limit exhausted"
+    finally:
+        F.set_step_limit(F.DEFAULT_STEP_LIMIT)
+
+
+@pytest.mark.parametrize("R,C", [(1024, 1024), (333, 77), (4096, 12)])
+def test_affsig_rowwise_broadcast_vs_oracle(fused_module, R, C):
+    # c2 pattern sigma(a*x+b), a,b of shape (C,), at sizes the oracle handles
+    rng = np.random.default_rng(R + C)
+    x = rng.uniform(-2, 2, (R, C)).astype(np.float32)
+    a = rng.uniform(-2, 2, C).astype(np.float32)
+    b = rng.uniform(-2, 2, C).astype(np.float32)
+    yb = rng.uniform(-1, 1, (R, C)).astype(np.float32)
+    args = [torch.from_numpy(v).cuda() for v in (a, x, b)]
+    y, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", args, torch.from_numpy(yb).cuda(),
+                                       want_primal=True)
+    p, parts = OS.vec_eval(fused_module, "affsig", [a.astype(np.float64), x.astype(np.float64),
+                                                   b.astype(np.float64)])
+    ybd = yb.astype(np.float64)
+    assert max_rel(y, p) <= 1e-6
+    assert max_rel(dx, ybd * parts[1]) <= 1e-6
+    assert max_rel(da, OS.reduce_to(ybd * parts[0], (C,))) <= 1e-6
+    assert max_rel(db, OS.reduce_to(ybd * parts[2], (C,))) <= 1e-6
+    y2 = F.fused_map(fused_module, "affsig", args)
+    assert torch.equal(y, y2)  # primal of K1 == primal of K2 (no FMA contraction)
+
+
+def test_column_and_scalar_reductions(fused_module):
+    # (R,1) operand -> row sums via warp shuffles; scalar -> block tree
+    rng = np.random.default_rng(3)
+    R, C = 257, 1000
+    x = rng.uniform(-2, 2, (R, C))
+    w = rng.uniform(-2, 2, (R, 1))
+    s = 0.3
+    yb = rng.uniform(-1, 1, (R, C))
+    args = [torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), s]
+    _, (dx, dw, ds) = F.fused_map_grad(fused_module, "mixed", args, torch.from_numpy(yb).cuda())
+    p, parts = OS.vec_eval(fused_module, "mixed", [x, w, s])
+    assert max_rel(dx, yb * parts[0]) <= 1e-13
+    assert max_rel(dw, OS.reduce_to(yb * parts[1], (R, 1))) <= 1e-12
+    assert abs(float(ds.item()) - OS.fused_map_pullback([parts[2]], [None], yb)[0]) <= 1e-10 * R * C
+
+
+def test_deterministic_gradients(fused_module):
+    torch.manual_seed(0)
+    x = torch.rand(2048, 512, device="cuda") * 4 - 2
+    a = torch.rand(512, device="cuda")
+    b = torch.rand(512, device="cuda")
+    yb = torch.rand(2048, 512, device="cuda")
+    _, g1 = F.fused_map_grad(fused_module, "affsig", [a, x, b], yb)
+    _, g2 = F.fused_map_grad(fused_module, "affsig", [a, x, b], yb)
+    for u, v in zip(g1, g2):
+        assert torch.equal(u, v)
+
+
+def test_reference_style_inputs(fused_module):
+    # reference DenseTensor-like objects and numpy arrays are accepted
+    class DT:  # duck-typed reference DenseTensor (tensor.py:29-47)
+        def __init__(self, a):
+            self.data = np.asarray(a, dtype=np.float64)
+
+    primal, parts = F.fused_map_with_partials(fused_module, "two", (DT([0.2, -0.9, 1.4, 0.05]), 0.7))
+    want = [math.tanh(v + 0.7) for v in (0.2, -0.9, 1.4, 0.05)]
+    assert max_rel(primal, np.array(want)) <= 1e-15
+    assert primal.dtype == torch.float64
+    p, q = F.fused_map_with_partials(fused_module, "two", (0.5, 0.25))
+    assert isinstance(p, float) and abs(p - math.tanh(0.75)) < 1e-15
+    assert len(q) == 2 and all(isinstance(v, float) for v in q)
