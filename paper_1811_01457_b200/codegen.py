@@ -111,8 +111,9 @@ def _cyclic(fn) -> bool:
 
 
 class _FnLowering:
-    def __init__(self, owner: "_Lowerer", fn, index: int):
+    def __init__(self, owner: "_Lowerer", fn, index: int, is_entry: bool = False):
         self.o = owner
+        self.is_entry = is_entry
         self.fn = fn
         self.idx = index
         self.dual = owner.dual
@@ -203,10 +204,172 @@ class _FnLowering:
             return ks[1]
         return None
 
+    # ---------------------------------------------------- tangent lanes
+    # Dual values carry K tangent lanes.  Seeds are one-hot (pack_rows,
+    # forward_ad.py:178-191), so most lanes are structurally 0 or 1; a
+    # forward dataflow pass over the CFG finds them and the emitter never
+    # computes them (a 0 lane contributes 0*p, which equals 0 for every
+    # finite primal p).  States: "Z" zero, "O" one, "V" computed.
+    def lane_ref(self, vid: int, j: int):
+        s = self.lanes[vid][j]
+        if s == "V":
+            return ("V", f"{self.v(vid)}.t[{j}]")
+        return (s, "(T)1" if s == "O" else "(T)0")
+
+    def dual_rule(self, op, ins, r, xs):
+        """(primal statements, lane list) for an f64 op; xs = [(pexpr, [lane refs])]."""
+        K = self.o.k
+        P = f"{r}.p"
+        pre = []
+        out = []
+
+        def lit(ln):
+            return ln[1]
+
+        if op in ("const", "itof") or (op == "pow_int" and int(ins.attrs["n"]) == 0):
+            return pre, [("Z", "(T)0")] * K
+        (xp, xl) = xs[0]
+        yp, yl = xs[1] if len(xs) > 1 else (None, None)
+        for j in range(K):
+            sx, ex = xl[j]
+            if op == "add":
+                sy, ey = yl[j]
+                out.append((sy, ey) if sx == "Z" else (sx, ex) if sy == "Z"
+                           else ("V", f"{ex} + {ey}"))
+            elif op == "sub":
+                sy, ey = yl[j]
+                out.append((sx, ex) if sy == "Z" else ("V", f"-({ey})") if sx == "Z"
+                           else ("V", f"{ex} - {ey}"))
+            elif op == "mul":  # s*y.p + x.p*t  (forward_ad.py:81)
+                sy, ey = yl[j]
+                t1 = None if sx == "Z" else (yp if sx == "O" else f"{ex} * {yp}")
+                t2 = None if sy == "Z" else (xp if sy == "O" else f"{xp} * {ey}")
+                terms = [t for t in (t1, t2) if t is not None]
+                out.append(("Z", "(T)0") if not terms else ("V", " + ".join(terms)))
+            elif op == "div":  # (s - p*t)/y.p  (forward_ad.py:87-88)
+                sy, ey = yl[j]
+                if sy == "Z":
+                    num = None if sx == "Z" else ex
+                else:
+                    pt = P if sy == "O" else f"{P} * {ey}"
+                    num = f"-({pt})" if sx == "Z" else f"{ex} - {pt}"
+                out.append(("Z", "(T)0") if num is None else ("V", f"({num}) / {yp}"))
+            elif op == "neg":
+                out.append(("Z", "(T)0") if sx == "Z" else ("V", f"-({ex})"))
+            elif op == "log":
+                out.append(("Z", "(T)0") if sx == "Z" else ("V", f"{ex} / {xp}"))
+            elif op in ("exp",):
+                out.append(("Z", "(T)0") if sx == "Z" else ("V", P if sx == "O" else f"{P} * {ex}"))
+            elif op in ("tanh", "sigmoid", "relu", "pow_int"):
+                out.append(("Z", "(T)0") if sx == "Z" else ("V", "d_" if sx == "O" else f"d_ * {ex}"))
+            else:
+                raise CodegenError(f"op '{op}' has no dual lowering")
+        if op == "div":
+            pre.append(f"{P} = {xp} / {yp};")
+        elif op == "tanh":
+            pre.append(f"{P} = sg_tanh({xp}); T d_ = (T)1 - {P} * {P};")
+        elif op == "sigmoid":
+            pre.append(f"{P} = sg_sigmoid({xp}); T d_ = {P} * ((T)1 - {P});")
+        elif op == "relu":
+            pre.append(f"T d_ = {xp} > (T)0 ? (T)1 : (T)0; {P} = {xp} > (T)0 ? {xp} : (T)0;")
+        elif op == "pow_int":
+            n = int(ins.attrs["n"])
+            pre.append(f"{P} = sg_pow_int({xp}, {n}); T d_ = (T){n} * sg_pow_int({xp}, {n - 1});")
+        else:
+            pre.append(f"{P} = {self.primal_expr(op, [xp, yp], ins)};")
+        return pre, out
+
+    def lane_states_of(self, ins):
+        op = ins.op
+        K = self.o.k
+        rk = self.types[ins.result]
+        if rk != "f64":
+            return None
+        if op == "call":
+            return ("V",) * K
+        if op == "select":
+            a, b = self.lanes[ins.operands[1]], self.lanes[ins.operands[2]]
+            return tuple(x if x == y and x != "V" else "V" for x, y in zip(a, b))
+        xs = []
+        for o in ins.operands:
+            if self.types[o] == "f64":
+                xs.append(("p", [(s, "e") for s in self.lanes[o]]))
+            else:
+                xs.append(("p", [("Z", "0")] * K))
+        _, lanes = self.dual_rule(op, ins, "r", xs or [("p", [("Z", "0")] * K)])
+        return tuple(s for s, _ in lanes)
+
+    def analyze_lanes(self):
+        K = self.o.k
+        fn = self.fn
+        self.lanes = {}
+        for i, (vid, ty) in enumerate(fn.params):
+            if kind_of(ty) == "f64":
+                if self.is_entry:
+                    self.lanes[vid] = tuple("O" if j == i else "Z" for j in range(K))
+                else:
+                    self.lanes[vid] = ("V",) * K
+        blocks = {b.name: b for b in fn.blocks}
+
+        def edges(b):
+            t = b.term
+            if hasattr(t, "then_target"):
+                return [(t.then_target, t.then_args), (t.else_target, t.else_args)]
+            if hasattr(t, "target"):
+                return [(t.target, t.args)]
+            return []
+
+        def ready(b):
+            return all(self.types[v] != "f64" or v in self.lanes for v, _ in b.params)
+
+        changed = True
+        while changed:
+            changed = False
+            for b in fn.blocks:
+                if not ready(b):
+                    continue
+                for ins in b.body:
+                    st = self.lane_states_of(ins)
+                    if st is not None:
+                        self.lanes[ins.result] = st
+                for tgt, args in edges(b):
+                    for (pv, _), av in zip(blocks[tgt].params, args):
+                        if self.types[pv] != "f64":
+                            continue
+                        new = self.lanes[av]
+                        old = self.lanes.get(pv)
+                        if old is not None:
+                            new = tuple(x if x == y else "V" for x, y in zip(old, new))
+                        if new != old:
+                            self.lanes[pv] = new
+                            changed = True
+        # unreachable blocks: anything goes
+        for b in fn.blocks:
+            for v, _ in b.params:
+                if self.types[v] == "f64" and v not in self.lanes:
+                    self.lanes[v] = ("V",) * K
+            for ins in b.body:
+                if self.types[ins.result] == "f64" and ins.result not in self.lanes:
+                    self.lanes[ins.result] = ("V",) * K
+        for b in fn.blocks:  # final states for every instruction
+            for ins in b.body:
+                st = self.lane_states_of(ins)
+                if st is not None:
+                    self.lanes[ins.result] = st
+
+    def materialize(self, vid: int) -> str:
+        """Write the literal value of virtual (Z/O) lanes into the struct."""
+        if not self.dual or self.types[vid] != "f64":
+            return ""
+        return " ".join(f"{self.v(vid)}.t[{j}] = {'(T)1' if s == 'O' else '(T)0'};"
+                        for j, s in enumerate(self.lanes[vid]) if s != "V")
+
     # ------------------------------------------------------ emission
     def emit(self) -> str:
         fn = self.fn
         self.infer()
+        if self.dual:
+            self.analyze_lanes()
         cyc = _cyclic(fn)
         rkind = kind_of(fn.results[0])
         rty = self.ctype(rkind)
@@ -243,7 +406,7 @@ class _FnLowering:
         if op == "const":
             val = ins.attrs["value"]
             if rk == "f64":
-                L.append(f"  {r} = sg_lift<{'D' if D else 'T'}>({_lit(float(val))});")
+                L.append(f"  {r}{'.p' if D else ''} = {_lit(float(val))};")
             elif rk == "i64":
                 L.append(f"  {r} = {int(val)}LL;")
             else:
@@ -254,6 +417,9 @@ class _FnLowering:
             ci = self.o.index_of(callee)
             nm = f"sgfn{ci}_{'d' if D else 'p'}"
             args = ", ".join(a + ["sg_err", "sg_steps"])
+            mats = " ".join(self.materialize(o) for o in ins.operands)
+            if mats.strip():
+                L.append(f"  {mats}")
             L.append(f"  {r} = {nm}({args});")
             L.append(f"  if (sg_err) return {self.zero_ret()};")
             return
@@ -263,7 +429,16 @@ class _FnLowering:
             L.append(f"  {r} = ({x[0]} {sym} {x[1]});")
             return
         if op == "select":
-            L.append(f"  {r} = {a[0]} ? {a[1]} : {a[2]};")
+            if D and rk == "f64":
+                o1, o2 = ins.operands[1], ins.operands[2]
+                parts = [f"{r}.p = {a[0]} ? {a[1]}.p : {a[2]}.p;"]
+                for j, st in enumerate(self.lanes[ins.result]):
+                    if st == "V":
+                        parts.append(f"{r}.t[{j}] = {a[0]} ? {self.lane_ref(o1, j)[1]} : "
+                                     f"{self.lane_ref(o2, j)[1]};")
+                L.append("  " + " ".join(parts))
+            else:
+                L.append(f"  {r} = {a[0]} ? {a[1]} : {a[2]};")
             return
         if rk == "i64":
             if op == "neg":
@@ -273,7 +448,7 @@ class _FnLowering:
                 L.append(f"  {r} = {a[0]} {sym} {a[1]};")
             return
         if op == "itof":
-            L.append(f"  {r} = sg_lift<{'D' if D else 'T'}>((T){a[0]});")
+            L.append(f"  {r}{'.p' if D else ''} = (T){a[0]};")
             return
 
         # f64 arithmetic from here on
@@ -286,7 +461,11 @@ class _FnLowering:
         if not D:
             L.append(f"  {r} = {self.primal_expr(op, a, ins)};")
         else:
-            L.append(f"  {{ {self.dual_block(op, r, a, ins)} }}")
+            xs = [(f"{self.v(o)}.p", [self.lane_ref(o, j) for j in range(self.o.k)])
+                  for o in ins.operands]
+            pre, lanes = self.dual_rule(op, ins, r, xs)
+            body = pre + [f"{r}.t[{j}] = {e};" for j, (st, e) in enumerate(lanes) if st == "V"]
+            L.append("  { " + " ".join(body) + " }")
 
     def prim(self, v: str, kind: str) -> str:
         return f"{v}.p" if (self.dual and kind == "f64") else v
@@ -317,47 +496,6 @@ class _FnLowering:
             return f"sg_pow_int({a[0]}, {int(ins.attrs['n'])})"
         raise CodegenError(f"op '{op}' has no scalar lowering")
 
-    @staticmethod
-    def dual_block(op, r, a, ins) -> str:
-        # formulas of forward_ad._DualRunner.dispatch, same operation order
-        loop = "_Pragma(\"unroll\") for (int j = 0; j < SG_KT; ++j)"
-        x = a[0]
-        if op in ("add", "sub"):
-            s = "+" if op == "add" else "-"
-            y = a[1]
-            return (f"{r}.p = {x}.p {s} {y}.p; {loop} {r}.t[j] = {x}.t[j] {s} {y}.t[j];")
-        if op == "mul":
-            y = a[1]
-            return (f"{r}.p = {x}.p * {y}.p; "
-                    f"{loop} {r}.t[j] = {x}.t[j] * {y}.p + {x}.p * {y}.t[j];")
-        if op == "div":
-            y = a[1]
-            return (f"T p_ = {x}.p / {y}.p; {r}.p = p_; "
-                    f"{loop} {r}.t[j] = ({x}.t[j] - p_ * {y}.t[j]) / {y}.p;")
-        if op == "neg":
-            return f"{r}.p = -{x}.p; {loop} {r}.t[j] = -{x}.t[j];"
-        if op == "exp":
-            return f"T y_ = sg_exp({x}.p); {r}.p = y_; {loop} {r}.t[j] = y_ * {x}.t[j];"
-        if op == "log":
-            return (f"{r}.p = sg_log({x}.p); {loop} {r}.t[j] = {x}.t[j] / {x}.p;")
-        if op == "tanh":
-            return (f"T y_ = sg_tanh({x}.p); T d_ = (T)1 - y_ * y_; {r}.p = y_; "
-                    f"{loop} {r}.t[j] = d_ * {x}.t[j];")
-        if op == "sigmoid":
-            return (f"T y_ = sg_sigmoid({x}.p); T d_ = y_ * ((T)1 - y_); {r}.p = y_; "
-                    f"{loop} {r}.t[j] = d_ * {x}.t[j];")
-        if op == "relu":
-            return (f"T d_ = {x}.p > (T)0 ? (T)1 : (T)0; "
-                    f"{r}.p = {x}.p > (T)0 ? {x}.p : (T)0; {loop} {r}.t[j] = d_ * {x}.t[j];")
-        if op == "pow_int":
-            n = int(ins.attrs["n"])
-            if n == 0:
-                return f"{r}.p = sg_pow_int({x}.p, 0); {loop} {r}.t[j] = (T)0;"
-            return (f"{r}.p = sg_pow_int({x}.p, {n}); "
-                    f"T d_ = (T){n} * sg_pow_int({x}.p, {n - 1}); "
-                    f"{loop} {r}.t[j] = d_ * {x}.t[j];")
-        raise CodegenError(f"op '{op}' has no dual lowering")
-
     def assign(self, target_name: str, args) -> str:
         tgt = next(b for b in self.fn.blocks if b.name == target_name)
         if not tgt.params:
@@ -365,6 +503,14 @@ class _FnLowering:
         tmps = []
         outs = []
         for j, ((pv, _), av) in enumerate(zip(tgt.params, args)):
+            if self.dual and self.types[pv] == "f64":
+                tmps.append(f"T t{j}_p = {self.v(av)}.p;")
+                outs.append(f"{self.v(pv)}.p = t{j}_p;")
+                for l, st in enumerate(self.lanes[pv]):
+                    if st == "V":
+                        tmps.append(f"T t{j}_{l} = {self.lane_ref(av, l)[1]};")
+                        outs.append(f"{self.v(pv)}.t[{l}] = t{j}_{l};")
+                continue
             ty = self.ctype(self.types[pv])
             tmps.append(f"{ty} t{j}_ = {self.v(av)};")
             outs.append(f"{self.v(pv)} = t{j}_;")
@@ -376,7 +522,8 @@ class _FnLowering:
         if t is None:
             raise CodegenError(f"@{self.fn.name} ^{b.name}: missing terminator")
         if hasattr(t, "values"):
-            L.append(f"  return {self.v(t.values[0])};")
+            m = self.materialize(t.values[0])
+            L.append(f"  {m + ' ' if m else ''}return {self.v(t.values[0])};")
         elif hasattr(t, "then_target"):
             c = self.v(t.cond)
             L.append(f"  if ({c}) {{ {self.assign(t.then_target, t.then_args)}goto B_{t.then_target}; }}")
@@ -386,9 +533,10 @@ class _FnLowering:
 
 
 class _Lowerer:
-    def __init__(self, module, dual: bool):
+    def __init__(self, module, dual: bool, k: int = 0):
         self.module = module
         self.dual = dual
+        self.k = max(1, k)
         self.order: list = []   # callees first
         self.sites: list[Site] = []
 
@@ -439,11 +587,11 @@ def lower(module, name: str) -> Lowered:
     sites: list[Site] = []
     entries = {}
     for dual in (False, True):
-        lo = _Lowerer(module, dual)
+        lo = _Lowerer(module, dual, k)
         lo.sites = sites
         lo.schedule(fn)
         for i, f in enumerate(lo.order):
-            chunks.append(_FnLowering(lo, f, i).emit())
+            chunks.append(_FnLowering(lo, f, i, is_entry=(f.name == fn.name)).emit())
         entries[dual] = f"sgfn{lo.index_of(fn)}_{'d' if dual else 'p'}"
     xs = ", ".join(f"x[{i}]" for i in range(k))
     sep = ", " if k else ""

@@ -139,8 +139,12 @@ def test_affsig_rowwise_broadcast_vs_oracle(fused_module, R, C):
     ybd = yb.astype(np.float64)
     assert max_rel(y, p) <= 1e-6
     assert max_rel(dx, ybd * parts[1]) <= 1e-6
-    assert max_rel(da, OS.reduce_to(ybd * parts[0], (C,))) <= 1e-6
-    assert max_rel(db, OS.reduce_to(ybd * parts[2], (C,))) <= 1e-6
+    # broadcast-axis sums: each of the R terms is within 1e-6 (fp32 elementwise)
+    # and they are accumulated in fp64, so |err| <= 1e-6 * sum|terms|
+    for got, part in ((da, parts[0]), (db, parts[2])):
+        terms = ybd * part
+        err = np.abs(got.double().cpu().numpy() - OS.reduce_to(terms, (C,)))
+        assert (err <= 1e-6 * np.maximum(1.0, np.abs(terms).sum(axis=0))).all()
     y2 = F.fused_map(fused_module, "affsig", args)
     assert torch.equal(y, y2)  # primal of K1 == primal of K2 (no FMA contraction)
 
