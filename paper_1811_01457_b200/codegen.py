@@ -226,8 +226,10 @@ class _FnLowering:
         def lit(ln):
             return ln[1]
 
-        if op in ("const", "itof") or (op == "pow_int" and int(ins.attrs["n"]) == 0):
+        if op in ("const", "itof"):
             return pre, [("Z", "(T)0")] * K
+        if op == "pow_int" and int(ins.attrs["n"]) == 0:  # forward_ad.py:123-124
+            return [f"{P} = sg_pow_int({xs[0][0]}, 0);"], [("Z", "(T)0")] * K
         (xp, xl) = xs[0]
         yp, yl = xs[1] if len(xs) > 1 else (None, None)
         for j in range(K):

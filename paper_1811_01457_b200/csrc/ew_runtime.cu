@@ -315,6 +315,9 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   else src << "typedef float T;\n";
   src << "#define SG_K " << k << "\n#define SG_KT " << std::max(1, k) << "\n";
   src << "#define SG_VEC " << L.vec << "\n#define SG_BDX " << L.bdx << "\n#define SG_BDY " << L.bdy << "\n";
+  bool has_col = false;
+  for (int i = 0; i < k; ++i) has_col |= kinds[i] == SG_COL;
+  src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n";
   src << "#define SG_KINDS {";
   for (int i = 0; i < std::max(1, k); ++i) src << (i ? "," : "") << (i < k ? kinds[i] : 0);
   src << "}\n";

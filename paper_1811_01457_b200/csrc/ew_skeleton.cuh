@@ -21,7 +21,15 @@
 // reduce_like(ybar * d f/d arg_i, type_i) (forward_ad.py:226-235,
 // rules.py:177-185) without materialising the (1+K)-row pack.
 
-#define SG_UNROLL 4
+#ifndef SG_UNROLL
+#define SG_UNROLL 4   // rows in flight per thread, forward
+#endif
+#ifndef SG_GUNROLL
+#define SG_GUNROLL 2  // rows in flight per thread, gradient (register budget)
+#endif
+#ifndef SG_GRAD_MINB
+#define SG_GRAD_MINB 3
+#endif
 
 struct D { T p; T t[SG_KT]; };
 
@@ -78,31 +86,44 @@ __device__ __forceinline__ void sg_publish_error(unsigned long long* err, long l
 
 static __device__ const int sg_kinds[SG_KT] = SG_KINDS;
 
-// Load operand i for rows r, columns c..c+SG_VEC-1.
-__device__ __forceinline__ void sg_load_operand(const SgEwParams& p, int i, long long r, long long c,
-                                                T (&x)[SG_VEC]) {
-  const int kind = sg_kinds[i];
-  const T* base = reinterpret_cast<const T*>(p.in[i]);
-  if (kind == SG_FULL) {
-    VT v = sg_ldv_stream(base + r * p.C + c);
+// Row-invariant operands (ROW vectors, one-element tensors, by-value scalars)
+// are loaded once per thread: a thread keeps its columns for its lifetime.
+__device__ __forceinline__ void sg_load_invariant(const SgEwParams& p, long long c, T (&inv)[SG_KT][SG_VEC]) {
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) x[j] = v.v[j];
-  } else if (kind == SG_ROW) {
-    VT v = sg_ldv(base + c);
+  for (int i = 0; i < SG_K; ++i) {
+    const int kind = sg_kinds[i];
+    const T* base = reinterpret_cast<const T*>(p.in[i]);
+    if (kind == SG_ROW) {
+      VT v = sg_ldv(base + c);
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) x[j] = v.v[j];
-  } else if (kind == SG_COL) {
-    T s = base[r];
+      for (int j = 0; j < SG_VEC; ++j) inv[i][j] = v.v[j];
+    } else if (kind == SG_SPTR || kind == SG_SVAL) {
+      const T s = kind == SG_SPTR ? base[0] : (T)p.sval[i];
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
-  } else if (kind == SG_SPTR) {
-    T s = base[0];
+      for (int j = 0; j < SG_VEC; ++j) inv[i][j] = s;
+    }
+  }
+}
+
+// Per-row operands (FULL rows, COL scalars) for row r; invariants copied in.
+__device__ __forceinline__ void sg_load_row(const SgEwParams& p, long long r, long long c,
+                                            const T (&inv)[SG_KT][SG_VEC], T (&x)[SG_KT][SG_VEC]) {
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
-  } else {
-    T s = (T)p.sval[i];
+  for (int i = 0; i < SG_K; ++i) {
+    const int kind = sg_kinds[i];
+    const T* base = reinterpret_cast<const T*>(p.in[i]);
+    if (kind == SG_FULL) {
+      VT v = sg_ldv_stream(base + r * p.C + c);
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) x[j] = s;
+      for (int j = 0; j < SG_VEC; ++j) x[i][j] = v.v[j];
+    } else if (kind == SG_COL) {
+      const T s = __ldg(base + r);
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) x[i][j] = s;
+    } else {
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) x[i][j] = inv[i][j];
+    }
   }
 }
 
@@ -113,6 +134,27 @@ __device__ __forceinline__ long long sg_row_end(const SgEwParams& p) {
   long long e = ((long long)blockIdx.y + 1) * p.rows_per_block;
   return e < p.R ? e : p.R;
 }
+// rows of this thread: r0 + ty + it*SG_BDY for it in [0, n)
+__device__ __forceinline__ long long sg_my_rows(long long r0, long long r1, int ty) {
+  const long long lo = r0 + ty;
+  return r1 > lo ? (r1 - lo + SG_BDY - 1) / SG_BDY : 0;
+}
+
+__device__ __forceinline__ void sg_primal_row(const SgEwParams& p, long long r, long long c,
+                                              const T (&x)[SG_KT][SG_VEC], T* out) {
+  VT y;
+#pragma unroll
+  for (int j = 0; j < SG_VEC; ++j) {
+    T a[SG_KT];
+#pragma unroll
+    for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? x[i][j] : (T)0;
+    int err = 0;
+    long long steps = p.step_limit;
+    sg_entry_p(a, y.v[j], err, steps);
+    if (err) sg_publish_error(p.err, r * p.C + c + j, err);
+  }
+  sg_stv(out + r * p.C + c, y);
+}
 
 // --------------------------------------------------------------- K1: forward
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
@@ -121,34 +163,23 @@ sg_ew_forward(const SgEwParams p) {
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
   const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const long long n = sg_my_rows(r0, r1, ty);
   T* out = reinterpret_cast<T*>(p.out);
-  for (long long rb = r0 + ty; rb < r1; rb += (long long)SG_BDY * SG_UNROLL) {
+  T inv[SG_KT][SG_VEC];
+  sg_load_invariant(p, c, inv);
+  long long it = 0;
+  for (; it + SG_UNROLL <= n; it += SG_UNROLL) {  // full chunks: all loads issued first
     T xs[SG_UNROLL][SG_KT][SG_VEC];
 #pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) {
-      const long long r = rb + (long long)u * SG_BDY;
-      if (r < r1) {
+    for (int u = 0; u < SG_UNROLL; ++u) sg_load_row(p, r0 + ty + (it + u) * SG_BDY, c, inv, xs[u]);
 #pragma unroll
-        for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[u][i]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) {
-      const long long r = rb + (long long)u * SG_BDY;
-      if (r >= r1) break;
-      VT y;
-#pragma unroll
-      for (int j = 0; j < SG_VEC; ++j) {
-        T a[SG_KT];
-#pragma unroll
-        for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? xs[u][i][j] : (T)0;
-        int err = 0;
-        long long steps = p.step_limit;
-        sg_entry_p(a, y.v[j], err, steps);
-        if (err) sg_publish_error(p.err, r * p.C + c + j, err);
-      }
-      sg_stv(out + r * p.C + c, y);
-    }
+    for (int u = 0; u < SG_UNROLL; ++u) sg_primal_row(p, r0 + ty + (it + u) * SG_BDY, c, xs[u], out);
+  }
+  for (; it < n; ++it) {
+    T xs[SG_KT][SG_VEC];
+    const long long r = r0 + ty + it * SG_BDY;
+    sg_load_row(p, r, c, inv, xs);
+    sg_primal_row(p, r, c, xs, out);
   }
 }
 
@@ -158,96 +189,124 @@ sg_ew_forward(const SgEwParams p) {
 //   SG_ROW:              part[(by*SG_BDY + ty) * C + c]      (G_row = gy*SG_BDY rows)
 //   SG_COL:              part[g * R + r], g = lane-group column id
 //   SG_SPTR / SG_SVAL:   part[by * gx + bx]                  (block partial)
-extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+struct SgGradAcc {
+  double row[SG_KT][SG_VEC];  // ROW operands: per-column sums over my rows
+  double s[SG_KT];            // scalar operands
+};
+
+// One row: duals, ybar contraction, xbar stores, accumulation.  Returns the
+// per-row sums for COL operands in colsum.
+__device__ __forceinline__ void sg_grad_row(const SgEwParams& p, long long r, long long c,
+                                            const T (&x)[SG_KT][SG_VEC], const VT& yb, SgGradAcc& acc,
+                                            double (&colsum)[SG_KT]) {
+  VT y, g[SG_KT];
+#pragma unroll
+  for (int j = 0; j < SG_VEC; ++j) {
+    T a[SG_KT], d[SG_KT];
+#pragma unroll
+    for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? x[i][j] : (T)0;
+    int err = 0;
+    long long steps = p.step_limit;
+    sg_entry_d(a, y.v[j], d, err, steps);
+    if (err) sg_publish_error(p.err, r * p.C + c + j, err);
+#pragma unroll
+    for (int i = 0; i < SG_K; ++i) {
+      const T contrib = yb.v[j] * d[i];  // ybar .* partial_i (forward_ad.py:233)
+      const int kind = sg_kinds[i];
+      if (kind == SG_FULL) g[i].v[j] = contrib;
+      else if (kind == SG_ROW) acc.row[i][j] += (double)contrib;
+      else if (kind == SG_COL) colsum[i] += (double)contrib;
+      else acc.s[i] += (double)contrib;
+    }
+  }
+  if (p.out) sg_stv(reinterpret_cast<T*>(p.out) + r * p.C + c, y);
+#pragma unroll
+  for (int i = 0; i < SG_K; ++i)
+    if (sg_kinds[i] == SG_FULL) sg_stv(reinterpret_cast<T*>(p.xbar[i]) + r * p.C + c, g[i]);
+}
+
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_GRAD_MINB)
 sg_ew_grad(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   const bool active = c < p.C;
   const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
   const T* ybar = reinterpret_cast<const T*>(p.ybar);
-  T* out = reinterpret_cast<T*>(p.out);
 
-  double rowacc[SG_KT][SG_VEC];   // ROW operands: per-column sums over my rows
-  double sacc[SG_KT];             // scalar operands: sums over everything I see
+  SgGradAcc acc;
 #pragma unroll
   for (int i = 0; i < SG_KT; ++i) {
-    sacc[i] = 0.0;
+    acc.s[i] = 0.0;
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) rowacc[i][j] = 0.0;
+    for (int j = 0; j < SG_VEC; ++j) acc.row[i][j] = 0.0;
   }
-  // lanes of one warp that share a row (COL reductions): SG_BDX >= 32 -> whole warp
-  constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
+  T inv[SG_KT][SG_VEC];
+  if (active) sg_load_invariant(p, c, inv);
 
-  const long long rows_span = r1 > r0 ? (r1 - r0 + SG_BDY - 1) / SG_BDY : 0;
-  for (long long it = 0; it < rows_span; it += SG_UNROLL) {
-    T xs[SG_UNROLL][SG_KT][SG_VEC];
-    T yb[SG_UNROLL][SG_VEC];
+#if !SG_HAS_COL
+  // no cross-thread work per row: full chunks with all loads issued first
+  if (active) {
+    const long long n = sg_my_rows(r0, r1, ty);
+    double colsum[SG_KT];
+    long long it = 0;
+    for (; it + SG_GUNROLL <= n; it += SG_GUNROLL) {
+      T xs[SG_GUNROLL][SG_KT][SG_VEC];
+      VT yb[SG_GUNROLL];
 #pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) {
-      const long long r = r0 + ty + (it + u) * SG_BDY;
-      if (active && r < r1 && it + u < rows_span) {
-#pragma unroll
-        for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[u][i]);
-        VT v = sg_ldv_stream(ybar + r * p.C + c);
-#pragma unroll
-        for (int j = 0; j < SG_VEC; ++j) yb[u][j] = v.v[j];
+      for (int u = 0; u < SG_GUNROLL; ++u) {
+        const long long r = r0 + ty + (it + u) * SG_BDY;
+        sg_load_row(p, r, c, inv, xs[u]);
+        yb[u] = sg_ldv_stream(ybar + r * p.C + c);
       }
+#pragma unroll
+      for (int u = 0; u < SG_GUNROLL; ++u)
+        sg_grad_row(p, r0 + ty + (it + u) * SG_BDY, c, xs[u], yb[u], acc, colsum);
+    }
+    for (; it < n; ++it) {
+      const long long r = r0 + ty + it * SG_BDY;
+      T xs[SG_KT][SG_VEC];
+      sg_load_row(p, r, c, inv, xs);
+      VT yb = sg_ldv_stream(ybar + r * p.C + c);
+      sg_grad_row(p, r, c, xs, yb, acc, colsum);
+    }
+  }
+#else
+  // COL operands reduce across the lanes sharing a row: every lane of a
+  // group must take the same trip count, so walk the block's row span
+  constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
+  const long long rows_span = r1 > r0 ? (r1 - r0 + SG_BDY - 1) / SG_BDY : 0;
+  for (long long it = 0; it < rows_span; ++it) {
+    const long long r = r0 + ty + it * SG_BDY;
+    const bool live = active && r < r1;
+    double colsum[SG_KT];
+#pragma unroll
+    for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
+    if (live) {
+      T xs[SG_KT][SG_VEC];
+      sg_load_row(p, r, c, inv, xs);
+      VT yb = sg_ldv_stream(ybar + r * p.C + c);
+      sg_grad_row(p, r, c, xs, yb, acc, colsum);
     }
 #pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) {
-      if (it + u >= rows_span) break;   // uniform across the block
-      const long long r = r0 + ty + (it + u) * SG_BDY;
-      const bool live = active && r < r1;
-      double colsum[SG_KT];
+    for (int i = 0; i < SG_K; ++i) {
+      if (sg_kinds[i] != SG_COL) continue;
+      double s = colsum[i];
 #pragma unroll
-      for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
-      if (live) {
-        VT y, g[SG_KT];
-#pragma unroll
-        for (int j = 0; j < SG_VEC; ++j) {
-          T a[SG_KT], d[SG_KT];
-#pragma unroll
-          for (int i = 0; i < SG_KT; ++i) a[i] = (i < SG_K) ? xs[u][i][j] : (T)0;
-          int err = 0;
-          long long steps = p.step_limit;
-          sg_entry_d(a, y.v[j], d, err, steps);
-          if (err) sg_publish_error(p.err, r * p.C + c + j, err);
-#pragma unroll
-          for (int i = 0; i < SG_K; ++i) {
-            const T contrib = yb[u][j] * d[i];   // ybar ⊙ partial_i (forward_ad.py:233)
-            const int kind = sg_kinds[i];
-            if (kind == SG_FULL) g[i].v[j] = contrib;
-            else if (kind == SG_ROW) rowacc[i][j] += (double)contrib;
-            else if (kind == SG_COL) colsum[i] += (double)contrib;
-            else sacc[i] += (double)contrib;
-          }
-        }
-        if (out) sg_stv(out + r * p.C + c, y);
-#pragma unroll
-        for (int i = 0; i < SG_K; ++i)
-          if (sg_kinds[i] == SG_FULL) sg_stv(reinterpret_cast<T*>(p.xbar[i]) + r * p.C + c, g[i]);
-      }
-      // row reductions for COL operands: lanes with the same ty share row r
-#pragma unroll
-      for (int i = 0; i < SG_K; ++i) {
-        if (sg_kinds[i] != SG_COL) continue;
-        double s = colsum[i];
-#pragma unroll
-        for (int off = kGroup / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, kGroup);
-        if (live && (tx % kGroup) == 0) {
-          const long long g = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
-          p.part[i][g * p.R + r] = s;
-        }
+      for (int off = kGroup / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, kGroup);
+      if (live && (tx % kGroup) == 0) {
+        const long long gi = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
+        p.part[i][gi * p.R + r] = s;
       }
     }
   }
+#endif
   // ROW partials: one row of partials per row-thread
 #pragma unroll
   for (int i = 0; i < SG_K; ++i) {
     if (sg_kinds[i] != SG_ROW || !active) continue;
-    const long long g = (long long)blockIdx.y * SG_BDY + ty;
+    const long long gi = (long long)blockIdx.y * SG_BDY + ty;
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) p.part[i][g * p.C + c + j] = rowacc[i][j];
+    for (int j = 0; j < SG_VEC; ++j) p.part[i][gi * p.C + c + j] = acc.row[i][j];
   }
   // scalar partials: block tree reduction in a fixed order
   __shared__ double red[SG_BDX * SG_BDY];
@@ -255,7 +314,7 @@ sg_ew_grad(const SgEwParams p) {
 #pragma unroll
   for (int i = 0; i < SG_K; ++i) {
     if (sg_kinds[i] != SG_SPTR && sg_kinds[i] != SG_SVAL) continue;
-    red[tid] = active ? sacc[i] : 0.0;
+    red[tid] = active ? acc.s[i] : 0.0;
     __syncthreads();
     for (int s = (SG_BDX * SG_BDY) / 2; s > 0; s >>= 1) {
       if (tid < s) red[tid] += red[tid + s];
@@ -276,10 +335,11 @@ sg_ew_pack(const SgEwParams p) {
   const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
   const long long plane = p.R * p.C;
   T* pk = reinterpret_cast<T*>(p.pack);
+  T inv[SG_KT][SG_VEC];
+  sg_load_invariant(p, c, inv);
   for (long long r = r0 + ty; r < r1; r += SG_BDY) {
     T xs[SG_KT][SG_VEC];
-#pragma unroll
-    for (int i = 0; i < SG_K; ++i) sg_load_operand(p, i, r, c, xs[i]);
+    sg_load_row(p, r, c, inv, xs);
     VT y, g[SG_KT];
 #pragma unroll
     for (int j = 0; j < SG_VEC; ++j) {
