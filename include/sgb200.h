@@ -104,6 +104,64 @@ SG_API int sg_ew_compile_only(const char* user_src, int k, int dtype, const int*
 /* Number of NVRTC variants compiled so far (introspection / tests). */
 SG_API int sg_ew_variant_count(sg_kernel* kern);
 
+/* ------------------------------------------------------------ Dense GEMM
+ * D[M,N] = sum_k A[m,k] B[n,k] with a fused epilogue: the Dense layer's
+ * `matmul(h, transpose(W))` + `add` + activation (nn_train.py:189-210,
+ * tensor.py:351-361) and its adjoints (rules.py:45-46, 82-94, 113-115, 123-124).
+ * A is [M][lda] (K-major) or, with a_mn_major, [K][lda] (MN-major); same for
+ * B with N.  So X.W^T, dZ.W and dZ^T.X all run without transposes.
+ *
+ * precision:
+ *   SG_PREC_BF16         A,B bf16 -> tcgen05 tensor cores (TMA + TMEM), fp32
+ *                        accumulate; lda/ldb multiples of 8, 16-byte aligned.
+ *   SG_PREC_STRICT_FP32  A,B f32 -> CUDA cores, ascending-k fold with every
+ *                        product and sum rounded (no FMA): bit-exact with the
+ *                        reference kernel's order restated in fp32.
+ *   SG_PREC_STRICT_FP64  same in f64: bit-exact with the unmodified reference.
+ * epilogue (per output element, v = the dot product):
+ *   SG_EPI_STORE     out = v
+ *   SG_EPI_BIAS_ACT  out_pre = v + bias[n];  out = act(v + bias[n])
+ *   SG_EPI_ACT_GRAD  out = v * act'(aux[m][n])   (act' from the saved output h:
+ *                    sigmoid h(1-h), tanh 1-h^2, relu [h>0]; rules.py:82-94)
+ * Outputs: `out` (f32; f64 for STRICT_FP64), optional `out_lp` bf16 copy
+ * (BF16 precision only), optional `out_pre`.  Null pointers are skipped. */
+#define SG_PREC_BF16 0
+#define SG_PREC_STRICT_FP32 1
+#define SG_PREC_STRICT_FP64 2
+
+#define SG_EPI_STORE 0
+#define SG_EPI_BIAS_ACT 1
+#define SG_EPI_ACT_GRAD 2
+
+#define SG_ACT_IDENTITY 0
+#define SG_ACT_SIGMOID 1
+#define SG_ACT_TANH 2
+#define SG_ACT_RELU 3
+
+typedef struct sg_gemm_desc {
+  int64_t M, N, K;
+  const void* A;
+  int64_t lda;
+  int32_t a_mn_major;
+  const void* B;
+  int64_t ldb;
+  int32_t b_mn_major;
+  int32_t precision;
+  int32_t epilogue;
+  int32_t act;
+  const void* bias;
+  const void* aux;
+  int64_t ld_aux;
+  void* out_pre;
+  int64_t ld_pre;
+  void* out;
+  int64_t ld_out;
+  void* out_lp;
+  int64_t ld_lp;
+} sg_gemm_desc;
+
+SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);
+
 /* out = reduce_to(a .* b, out_shape); b may be NULL.  The contraction of
  * `fused_map_pullback` (forward_ad.py:232-235) and `reduce_to`
  * (tensor.py:327-345) on the device; fp64 accumulation, fixed order. */

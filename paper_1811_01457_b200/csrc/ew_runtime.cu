@@ -148,6 +148,15 @@ int ensure_context(sg_ctx* ctx) {
   return SG_OK;
 }
 
+}  // namespace
+
+namespace sg {
+int ctx_num_sms(sg_ctx* ctx) { return ctx->num_sms; }
+int ctx_activate(sg_ctx* ctx) { return ensure_context(ctx); }
+}  // namespace sg
+
+namespace {
+
 // Output shape of the broadcast (tensor.py:108-121): trailing alignment.
 int broadcast_shape(int k, const sg_tensor* args, std::vector<long long>& out) {
   out.clear();

@@ -1,0 +1,111 @@
+// Dense-layer GEMM interfaces shared by the tensor-core and strict kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/sgb200.h"
+
+namespace sg {
+
+// Epilogue of one GEMM tile row (see include/sgb200.h for the modes).
+struct GemmEpilogue {
+  int mode;                    // SG_EPI_STORE / SG_EPI_BIAS_ACT / SG_EPI_ACT_GRAD
+  int act;                     // SG_ACT_*
+  const float* bias;           // [N]                                (BIAS_ACT)
+  const __nv_bfloat16* aux;    // saved activation h [M][ld_aux]     (ACT_GRAD)
+  long long ld_aux;
+  float* out_pre;              // optional fp32 z+b before activation (BIAS_ACT)
+  long long ld_pre;
+  float* out_f32;              // optional fp32 result
+  long long ld_f32;
+  __nv_bfloat16* out_bf16;     // optional bf16 result
+  long long ld_bf16;
+};
+
+struct GemmArgs {
+  int M, N, K;
+  const __nv_bfloat16* A;
+  long long lda;
+  bool a_mn;  // A stored [K][M] (MN-major) instead of [M][K]
+  const __nv_bfloat16* B;
+  long long ldb;
+  bool b_mn;  // B stored [K][N] instead of [N][K]
+  GemmEpilogue epi;
+};
+
+int launch_gemm_bf16(const GemmArgs& g, int num_sms, cudaStream_t st);
+
+namespace strict {
+struct StrictArgs {
+  int M, N, K;
+  const void* A;
+  long long lda;
+  bool a_mn;
+  const void* B;
+  long long ldb;
+  bool b_mn;
+  int mode, act;
+  const void* bias;
+  const void* aux;
+  long long ld_aux;
+  void* out_pre;
+  long long ld_pre;
+  void* out;
+  long long ld_out;
+};
+}  // namespace strict
+int launch_gemm_strict(const strict::StrictArgs& g, bool f64, cudaStream_t st);
+
+// ----------------------------------------------------- epilogue row helpers
+// One thread owns one output row segment of up to 32 consecutive columns.
+__device__ __forceinline__ void store_row_f32(float* dst, const float (&v)[32], int n) {
+  if (n == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < n) dst[i] = v[i];
+  }
+}
+
+__device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const float (&v)[32], int n) {
+  if (n == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 4)
+      *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < n) dst[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+__device__ __forceinline__ void load_row_bf16(const __nv_bfloat16* src, float (&v)[32], int n) {
+  if (n == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint4 w = __ldg(reinterpret_cast<const uint4*>(src + i));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        v[i + 2 * j] = f.x;
+        v[i + 2 * j + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i < n ? __bfloat162float(src[i]) : 0.0f;
+  }
+}
+
+}  // namespace sg

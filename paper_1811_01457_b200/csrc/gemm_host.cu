@@ -1,0 +1,59 @@
+// C ABI of the Dense GEMMs (include/sgb200.h: sg_gemm).
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "gemm.h"
+
+namespace sg {
+int ctx_num_sms(sg_ctx* ctx);
+int ctx_activate(sg_ctx* ctx);
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
+  if (!ctx || !d) return fail(SG_EINVAL, "null argument");
+  if (d->M < 0 || d->N < 0 || d->K < 0 || d->M > (1ll << 31) - 1 || d->N > (1ll << 31) - 1 ||
+      d->K > (1ll << 31) - 1)
+    return fail(SG_EINVAL, "gemm: bad extents");
+  if (d->M == 0 || d->N == 0) return SG_OK;
+  if (d->epilogue < SG_EPI_STORE || d->epilogue > SG_EPI_ACT_GRAD) return fail(SG_EINVAL, "gemm: bad epilogue");
+  if (d->act < SG_ACT_IDENTITY || d->act > SG_ACT_RELU) return fail(SG_EINVAL, "gemm: bad activation");
+  if (d->epilogue == SG_EPI_ACT_GRAD && !d->aux) return fail(SG_EINVAL, "gemm: ACT_GRAD needs aux");
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->precision == SG_PREC_BF16) {
+    if (d->K == 0) return fail(SG_EINVAL, "gemm: K must be positive");
+    GemmArgs g{};
+    g.M = (int)d->M;
+    g.N = (int)d->N;
+    g.K = (int)d->K;
+    g.A = (const __nv_bfloat16*)d->A;
+    g.lda = d->lda;
+    g.a_mn = d->a_mn_major != 0;
+    g.B = (const __nv_bfloat16*)d->B;
+    g.ldb = d->ldb;
+    g.b_mn = d->b_mn_major != 0;
+    g.epi.mode = d->epilogue;
+    g.epi.act = d->act;
+    g.epi.bias = (const float*)d->bias;
+    g.epi.aux = (const __nv_bfloat16*)d->aux;
+    g.epi.ld_aux = d->ld_aux;
+    g.epi.out_pre = (float*)d->out_pre;
+    g.epi.ld_pre = d->ld_pre;
+    g.epi.out_f32 = (float*)d->out;
+    g.epi.ld_f32 = d->ld_out;
+    g.epi.out_bf16 = (__nv_bfloat16*)d->out_lp;
+    g.epi.ld_bf16 = d->ld_lp;
+    return launch_gemm_bf16(g, ctx_num_sms(ctx), st);
+  }
+  if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
+    if (d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
+    strict::StrictArgs g{(int)d->M, (int)d->N, (int)d->K, d->A, d->lda, d->a_mn_major != 0,
+                         d->B, d->ldb, d->b_mn_major != 0, d->epilogue, d->act, d->bias, d->aux,
+                         d->ld_aux, d->out_pre, d->ld_pre, d->out, d->ld_out};
+    return launch_gemm_strict(g, d->precision == SG_PREC_STRICT_FP64, st);
+  }
+  return fail(SG_EINVAL, "gemm: unknown precision");
+}

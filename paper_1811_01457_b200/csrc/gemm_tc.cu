@@ -1,0 +1,439 @@
+// K3/K4/K5: Dense-layer GEMMs on the 5th-generation tensor cores (sm_100a).
+//
+//   D[M,N] = sum_k A[m,k] * B[n,k]      (bf16 inputs, fp32 accumulation in TMEM)
+//
+// Reference: the Dense layer's forward `matmul(h, transpose(W))`
+// (nn_train.py:192-193, tensor.py:351-361) and its adjoints
+// `matmul(ybar, transpose(v))`, `matmul(transpose(a), ybar)` (rules.py:113-115).
+// Each operand is either K-major (row-major [rows][K]) or MN-major
+// (row-major [K][rows]), so all three products of a Dense layer run without
+// materialised transposes:
+//   forward  Z  = X  . W^T : A = X  [B][in]  K-major,  B = W [out][in] K-major
+//   backward dX = dZ . W   : A = dZ [B][out] K-major,  B = W [out][in] MN-major
+//   backward dW = dZ^T . X : A = dZ [B][out] MN-major, B = X [B][in]   MN-major
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: 128B-swizzled A/B tiles -> smem ring (STAGES deep)
+//   warp 1      MMA issuer:   one elected lane issues tcgen05.mma (M=128, N=BN,
+//                             K=16) into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue:     tcgen05.ld -> registers -> fused bias/activation/
+//                             activation-derivative -> global stores, while the
+//                             MMA warp already works on the next tile
+// Synchronisation is mbarrier-only: full/empty per smem stage (TMA tx-count and
+// tcgen05.commit), full/empty per accumulator buffer.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "common.h"
+#include "gemm.h"
+
+namespace sg {
+namespace tc {
+
+constexpr int BM = 128;           // UMMA M (cta_group::1)
+constexpr int BK = 64;            // 64 bf16 = one 128-byte swizzle row
+constexpr int UMMA_K = 16;
+constexpr int NUM_THREADS = 256;  // 8 warps
+constexpr int EPI_WARP0 = 4;
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread t of warp q gets lane 32q+t
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, 128B swizzle (layout type 2), sm_100 version bit.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, M x N, operand majors.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------- epilogue
+__device__ __forceinline__ float act_fwd(float z, int act) {
+  switch (act) {
+    case SG_ACT_SIGMOID: return 1.0f / (1.0f + __expf(-z));  // tensor.py:214-215
+    case SG_ACT_TANH: return tanhf(z);
+    case SG_ACT_RELU: return z > 0.0f ? z : 0.0f;
+    default: return z;
+  }
+}
+// d act / d z expressed through the saved output h (rules.py:82-94)
+__device__ __forceinline__ float act_grad_from_out(float h, int act) {
+  switch (act) {
+    case SG_ACT_SIGMOID: return h * (1.0f - h);
+    case SG_ACT_TANH: return 1.0f - h * h;
+    case SG_ACT_RELU: return h > 0.0f ? 1.0f : 0.0f;
+    default: return 1.0f;
+  }
+}
+
+struct TileCoord {
+  int m0, n0;
+};
+__device__ __forceinline__ TileCoord tile_of(int t, int m_tiles, int n_tiles, int bn) {
+  // grouped raster: 8 M-tiles per group so consecutive CTAs share B tiles in L2
+  constexpr int G = 8;
+  const int per_group = G * n_tiles;
+  const int group = t / per_group;
+  const int first_m = group * G;
+  const int gsize = min(m_tiles - first_m, G);
+  const int in_group = t - group * per_group;
+  TileCoord c;
+  c.m0 = (first_m + in_group % gsize) * BM;
+  c.n0 = (in_group / gsize) * bn;
+  return c;
+}
+
+struct KParams {
+  int M, N, K;
+  GemmEpilogue epi;
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const KParams p) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+  static_assert(TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation");
+  constexpr uint32_t IDESC = idesc_bf16(BM, BN, A_MN, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* acc_full = empty_bar + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m_tiles = (p.M + BM - 1) / BM;
+  const int n_tiles = (p.N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);  // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const TileCoord tc = tile_of(t, m_tiles, n_tiles, BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 64 * BK * 2, &tma_a, &full_bar[stage], tc.m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sa, &tma_a, &full_bar[stage], k0, tc.m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 64 * BK * 2, &tma_b, &full_bar[stage], tc.n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sb, &tma_b, &full_bar[stage], k0, tc.n0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            // K-major: next 16 K-elements are +32 B inside the swizzle row;
+            // MN-major: next 16 K-rows are +16*128 B (two 8-row core groups)
+            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 64 * BK * 2, 1024) : sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 64 * BK * 2, 1024) : sdesc(sb + k * 32, 16, 1024);
+            tc_mma(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty_bar[stage]);  // smem stage free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&acc_full[acc]);  // accumulator complete
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue =====================
+    const int q = warp - EPI_WARP0;  // TMEM lanes 32q..32q+31 (warp % 4 == q)
+    const GemmEpilogue& e = p.epi;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const TileCoord tc = tile_of(t, m_tiles, n_tiles, BN);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int m = tc.m0 + q * 32 + lane;
+      const bool row_ok = m < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int n0 = tc.n0 + c * 32;
+        float v[32];
+        tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
+        if (n0 >= p.N || !row_ok) continue;
+        const bool full = n0 + 32 <= p.N;
+        if (e.mode == SG_EPI_BIAS_ACT) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float b = (e.bias && (full || n0 + i < p.N)) ? __ldg(e.bias + n0 + i) : 0.0f;
+            v[i] += b;
+          }
+          if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, full ? 32 : p.N - n0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = act_fwd(v[i], e.act);
+        } else if (e.mode == SG_EPI_ACT_GRAD) {
+          float h[32];
+          load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, full ? 32 : p.N - n0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(h[i], e.act);
+        }
+        if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, full ? 32 : p.N - n0);
+        if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, full ? 32 : p.N - n0);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+}  // namespace tc
+}  // namespace sg
+
+// ================================================================ host side
+namespace sg {
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer][ld] buffer, box {64, box_outer}, 128B swizzle.
+int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld, int box_outer) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return fail(SG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
+  return SG_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  constexpr int STAGE = tc::BM * tc::BK * 2 + BN * tc::BK * 2;
+  constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
+  CUtensorMap ma, mb;
+  int rc;
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, tc::BM);
+  if (rc) return rc;
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN);
+  if (rc) return rc;
+  auto kern = tc::gemm_bf16_kernel<BN, STAGES, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  tc::KParams p{g.M, g.N, g.K, g.epi};
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, p);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+template <int BN>
+int run_bn(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  if (!g.a_mn && !g.b_mn) return run<BN, false, false>(g, num_sms, st);
+  if (!g.a_mn && g.b_mn) return run<BN, false, true>(g, num_sms, st);
+  if (g.a_mn && g.b_mn) return run<BN, true, true>(g, num_sms, st);
+  return run<BN, true, false>(g, num_sms, st);
+}
+
+}  // namespace
+
+int launch_gemm_bf16(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return fail(SG_EINVAL, "gemm: empty problem");
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!aligned(g.A) || !aligned(g.B)) return fail(SG_EINVAL, "gemm: A and B must be 16-byte aligned");
+  if (g.lda % 8 || g.ldb % 8) return fail(SG_EINVAL, "gemm: lda/ldb must be multiples of 8 elements");
+  if (g.lda < (g.a_mn ? g.M : g.K) || g.ldb < (g.b_mn ? g.N : g.K))
+    return fail(SG_EINVAL, "gemm: leading dimension smaller than the row");
+  if (g.N <= 64) return run_bn<64>(g, num_sms, st);
+  if (g.N <= 128) return run_bn<128>(g, num_sms, st);
+  return run_bn<256>(g, num_sms, st);
+}
+
+}  // namespace sg

@@ -1,0 +1,90 @@
+"""Python binding of ``sg_gemm`` (include/sgb200.h): Dense-layer GEMMs.
+
+``gemm(A, B)`` computes ``D[m, n] = sum_k A[m, k] B[n, k]`` with a fused
+epilogue, where each operand is passed in its storage layout:
+
+* ``a_mn=False``: ``A`` is ``[M, K]``; ``a_mn=True``: ``A`` is ``[K, M]``;
+* ``b_mn=False``: ``B`` is ``[N, K]``; ``b_mn=True``: ``B`` is ``[K, N]``.
+
+This is the reference's ``matmul`` (tensor.py:351-361) specialised to the
+three products of a Dense layer (nn_train.py:192-193, rules.py:113-115).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import runtime as rt
+
+PREC = {"bf16": 0, "strict_fp32": 1, "strict_fp64": 2}
+EPI = {"store": 0, "bias_act": 1, "act_grad": 2}
+ACT = {"identity": 0, "sigmoid": 1, "tanh": 2, "relu": 3}
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [
+        ("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64),
+        ("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("a_mn_major", ctypes.c_int32),
+        ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("b_mn_major", ctypes.c_int32),
+        ("precision", ctypes.c_int32), ("epilogue", ctypes.c_int32), ("act", ctypes.c_int32),
+        ("bias", ctypes.c_void_p),
+        ("aux", ctypes.c_void_p), ("ld_aux", ctypes.c_int64),
+        ("out_pre", ctypes.c_void_p), ("ld_pre", ctypes.c_int64),
+        ("out", ctypes.c_void_p), ("ld_out", ctypes.c_int64),
+        ("out_lp", ctypes.c_void_p), ("ld_lp", ctypes.c_int64),
+    ]
+
+
+_bound = False
+
+
+def _lib():
+    global _bound
+    lib = rt.load_library()
+    if not _bound:
+        lib.sg_gemm.argtypes = [ctypes.c_void_p, ctypes.POINTER(GemmDesc), ctypes.c_void_p]
+        lib.sg_gemm.restype = ctypes.c_int
+        _bound = True
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _ld(t):
+    if t is None:
+        return 0
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("gemm operands must be 2-D with unit column stride")
+    return t.stride(0)
+
+
+def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
+         epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
+         out_pre=None, stream=None):
+    """Launch one GEMM; outputs are written in place into the given tensors."""
+    if a_mn:
+        Ka, Ma = A.shape
+    else:
+        Ma, Ka = A.shape
+    if b_mn:
+        Kb, Nb = B.shape
+    else:
+        Nb, Kb = B.shape
+    M = Ma if M is None else M
+    N = Nb if N is None else N
+    K = min(Ka, Kb) if K is None else K
+    d = GemmDesc()
+    d.M, d.N, d.K = int(M), int(N), int(K)
+    d.A, d.lda, d.a_mn_major = _ptr(A), _ld(A), int(a_mn)
+    d.B, d.ldb, d.b_mn_major = _ptr(B), _ld(B), int(b_mn)
+    d.precision = PREC[precision]
+    d.epilogue = EPI[epilogue]
+    d.act = ACT[act]
+    d.bias = _ptr(bias)
+    d.aux, d.ld_aux = _ptr(aux), _ld(aux)
+    d.out_pre, d.ld_pre = _ptr(out_pre), _ld(out_pre)
+    d.out, d.ld_out = _ptr(out), _ld(out)
+    d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
+    rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")

@@ -1,0 +1,120 @@
+"""GPU parity of the Dense GEMMs (tcgen05 bf16 and strict CUDA-core modes).
+
+* BF16 tensor-core path: vs the fp64 product of the bf16-rounded inputs
+  (the only difference is fp32 accumulation order): rel <= 1e-5 of
+  sum|a*b| per output;
+* STRICT_FP32: bit-exact vs the fp32 restatement of tensor.py:351-361
+  (oracle/csrc/strict_gemm.c);
+* STRICT_FP64: bit-exact vs the unmodified reference (golden tensor.npz).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_npz
+from oracle import dense as OD
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1811_01457_b200.gemm import gemm  # noqa: E402
+
+
+def bf16_round(a):
+    return torch.from_numpy(a).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+def check_close(got, a, b, tol=1e-5):
+    want = a @ b
+    scale = np.abs(a) @ np.abs(b)
+    err = np.abs(got - want)
+    assert (err <= tol * np.maximum(scale, 1e-30) + 1e-30).all(), float((err / np.maximum(scale, 1e-30)).max())
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 200, 104), (1000, 520, 776), (7, 10, 32),
+                                   (256, 64, 4096), (129, 257, 136)])
+@pytest.mark.parametrize("layout", ["kk", "k_mn", "mn_mn"])
+def test_bf16_tensor_core_gemm(M, N, K, layout):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)).astype(np.float32))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)).astype(np.float32))
+    a_mn = layout == "mn_mn"
+    b_mn = layout != "kk"
+
+    def pad_ld(x):  # leading dimension multiple of 8 elements
+        rows, cols = x.shape
+        ld = (cols + 7) // 8 * 8
+        buf = torch.zeros((rows, ld), dtype=torch.bfloat16, device="cuda")
+        buf[:, :cols] = torch.from_numpy(x).to(torch.bfloat16)
+        return buf[:, :cols]
+
+    A = pad_ld(a.T.copy() if a_mn else a)
+    B = pad_ld(b.T.copy() if b_mn else b)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    gemm(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, out=out)
+    torch.cuda.synchronize()
+    check_close(out.double().cpu().numpy(), a, b.T)
+
+
+def test_bf16_epilogues():
+    rng = np.random.default_rng(1)
+    M, N, K = 256, 384, 192
+    a = bf16_round(rng.uniform(-1, 1, (M, K)).astype(np.float32))
+    w = bf16_round(rng.uniform(-1, 1, (N, K)).astype(np.float32))
+    bias = rng.uniform(-0.5, 0.5, N).astype(np.float32)
+    A = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    W = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(bias).cuda()
+    z = a @ w.T + bias
+    for act, f in (("sigmoid", lambda v: 1 / (1 + np.exp(-v))), ("tanh", np.tanh),
+                   ("relu", lambda v: np.maximum(v, 0)), ("identity", lambda v: v)):
+        out = torch.empty((M, N), device="cuda")
+        lp = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        pre = torch.empty((M, N), device="cuda")
+        gemm(A, W, epilogue="bias_act", act=act, bias=bt, out=out, out_lp=lp, out_pre=pre)
+        torch.cuda.synchronize()
+        assert np.abs(pre.double().cpu().numpy() - z).max() <= 1e-4
+        assert np.abs(out.double().cpu().numpy() - f(z)).max() <= 2e-4
+        assert np.abs(lp.double().cpu().numpy() - f(z)).max() <= 2e-2 * max(1, np.abs(f(z)).max())
+    # activation-derivative epilogue: dz = (dY . W) * act'(h)
+    h = rng.uniform(0.05, 0.95, (M, K)).astype(np.float32)
+    H = torch.from_numpy(h).to(torch.bfloat16).cuda()
+    hq = H.double().cpu().numpy()
+    dy = bf16_round(rng.uniform(-1, 1, (M, N)).astype(np.float32))
+    DY = torch.from_numpy(dy).to(torch.bfloat16).cuda()
+    out = torch.empty((M, K), device="cuda")
+    gemm(DY, W, b_mn=True, epilogue="act_grad", act="sigmoid", aux=H, out=out)
+    torch.cuda.synchronize()
+    want = (dy @ w) * hq * (1 - hq)
+    assert np.abs(out.double().cpu().numpy() - want).max() <= 1e-4
+
+
+@pytest.mark.parametrize("layout", ["kk", "k_mn", "mn_mn"])
+def test_strict_fp32_bit_exact(layout):
+    rng = np.random.default_rng(2)
+    M, N, K = 70, 45, 133
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (K, N)).astype(np.float32)  # want a @ b
+    want = OD.matmul_exact(a, b)
+    a_mn = layout == "mn_mn"
+    b_mn = layout != "kk"
+    A = torch.from_numpy(a.T.copy() if a_mn else a).cuda()
+    B = torch.from_numpy(b if b_mn else b.T.copy()).cuda()
+    out = torch.empty((M, N), device="cuda")
+    gemm(A, B, a_mn=a_mn, b_mn=b_mn, precision="strict_fp32", out=out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_strict_fp64_matches_reference_bit_for_bit():
+    z = load_npz("tensor.npz")
+    for i in range(3):
+        a, b, c = z[f"mm{i}_a"], z[f"mm{i}_b"], z[f"mm{i}_c"]
+        A = torch.from_numpy(a).cuda()
+        B = torch.from_numpy(b).cuda()  # [K][N] -> MN-major B
+        out = torch.empty(c.shape, dtype=torch.float64, device="cuda")
+        gemm(A, B, b_mn=True, precision="strict_fp64", out=out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), c)
