@@ -158,9 +158,49 @@ typedef struct sg_gemm_desc {
   int64_t ld_out;
   void* out_lp;
   int64_t ld_lp;
+  /* optional fp32 column sums of the result per 32-row group, [ceil(M/32)][ld_colsum]
+   * (BF16 precision): the bias gradient's first reduction stage, see sg_colsum_finalize */
+  float* colsum;
+  int64_t ld_colsum;
 } sg_gemm_desc;
 
 SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);
+
+/* ------------------------------------------------ Dense step, memory-bound
+ * dz = ybar .* act'(h)  (rules.py:82-94 with the saved output h, reference
+ * operation order), optionally a second copy dz2 in another dtype and the
+ * per-32-row column sums (bias-gradient stage 1).  dtypes: SG_F32/F64/BF16. */
+SG_API int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y, const void* h,
+                       int32_t h_dtype, int64_t ld_h, int64_t M, int64_t N, int32_t act, void* dz,
+                       int32_t dz_dtype, int64_t ld_dz, void* dz2, int32_t dz2_dtype, int64_t ld_dz2,
+                       float* colsum, int64_t ld_colsum, void* stream);
+/* out[n] = sum_g part[g][n] (fixed order, fp64 accumulation): bias-gradient stage 2. */
+SG_API int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_part, int64_t N, float* out,
+                              void* stream);
+/* reduce_to((M,N) -> (N,)) in the reference's exact order (sequential ascending
+ * row fold, tensor.py:287-292, 337-338), f32/f64: STRICT precision bias gradients. */
+SG_API int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t ld, int64_t M, int64_t N,
+                            void* out, void* stream);
+
+#define SG_LOSS_SOFTMAX_XENT 0
+#define SG_LOSS_MSE 1
+/* Fused loss forward + gradient over logits z [M][N] and targets y:
+ *   SOFTMAX_XENT: loss = -scale * sum y log softmax(z);  dz = (p * rowsum(y) - y) * scale
+ *                 (the c1 loss IR: exp / reduce_sum(axis=1) / div / log / mul, scale = 1/n)
+ *   MSE:          loss = scale * sum (z - y)^2;           dz = 2 (z - y) * scale
+ * `loss` (device f64) receives the total; loss_part is scratch of n_part doubles
+ * (>= ceil(N/32)*ceil(M/256) for MSE, ceil(M/256) for softmax).  Under data
+ * parallelism scale = 1/global_batch so shard gradients sum to the full one. */
+SG_API int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_z, const void* y,
+                   int64_t ld_y, int64_t M, int64_t N, double scale, double* loss, double* loss_part,
+                   int64_t n_part, void* dz, int32_t dz_dtype, int64_t ld_dz, void* dz2, int32_t dz2_dtype,
+                   int64_t ld_dz2, float* colsum, int64_t ld_colsum, void* stream);
+/* params -= lr * grads over the flat parameter buffer (nn_train.py:365-372);
+ * optional bf16 shadow copy of the updated parameters for the next GEMMs. */
+SG_API int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t n, double lr,
+                  void* shadow_bf16, void* stream);
+SG_API int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,
+                   void* stream);
 
 /* out = reduce_to(a .* b, out_shape); b may be NULL.  The contraction of
  * `fused_map_pullback` (forward_ad.py:232-235) and `reduce_to`

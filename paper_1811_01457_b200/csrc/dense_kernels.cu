@@ -1,0 +1,407 @@
+// Memory-bound kernels of the Dense training step (K6 bias-grad, K7 loss, K8 SGD).
+//
+// Reference: loss IR composed from exp/reduce_sum/div/log/mul (SURVEY §8(d)
+// c1) or sub/mul/reduce_sum (MSE, c4/c5); bias gradient `reduce_like`
+// column sums (rules.py:45-46, tensor.py:327-345); SGD `p - lr*g`
+// (nn_train.py:365-372).  All reductions are deterministic (fixed order);
+// fp64 accumulation for fp32 data.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "common.h"
+#include "gemm.h"
+
+namespace sg {
+namespace dk {
+
+template <class T> __device__ __forceinline__ T ld_as(const void* p, int dtype, long long i);
+template <> __device__ __forceinline__ float ld_as<float>(const void* p, int dtype, long long i) {
+  if (dtype == SG_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  if (dtype == SG_F64) return (float)reinterpret_cast<const double*>(p)[i];
+  return reinterpret_cast<const float*>(p)[i];
+}
+template <> __device__ __forceinline__ double ld_as<double>(const void* p, int dtype, long long i) {
+  if (dtype == SG_BF16) return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  if (dtype == SG_F64) return reinterpret_cast<const double*>(p)[i];
+  return (double)reinterpret_cast<const float*>(p)[i];
+}
+__device__ __forceinline__ void st_as(void* p, int dtype, long long i, double v) {
+  if (dtype == SG_BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn((float)v);
+  else if (dtype == SG_F64) reinterpret_cast<double*>(p)[i] = v;
+  else reinterpret_cast<float*>(p)[i] = (float)v;
+}
+
+template <class T>
+__device__ __forceinline__ T act_grad_h(T h, int act) {  // rules.py:82-94, derivative from the output
+  switch (act) {
+    case SG_ACT_SIGMOID: return h * ((T)1 - h);
+    case SG_ACT_TANH: return (T)1 - h * h;
+    case SG_ACT_RELU: return h > (T)0 ? (T)1 : (T)0;
+    default: return (T)1;
+  }
+}
+
+// --- dZ = ybar .* act'(h); lane = column, warp walks 32 rows, column sums per 32-row group
+template <class T>
+__global__ void __launch_bounds__(256) k_act_grad(const void* ybar, int yd, long long ldy, const void* h, int hd,
+                                                  long long ldh, long long M, long long N, int act, void* dz,
+                                                  int dzd, long long lddz, void* dz2, int dz2d, long long lddz2,
+                                                  float* colsum, long long ldc) {
+  const long long c = blockIdx.x * 32ll + threadIdx.x;
+  const long long g = blockIdx.y * 8ll + threadIdx.y;  // 32-row group
+  const long long r0 = g * 32;
+  if (r0 >= M) return;
+  T acc = (T)0;
+  if (c < N) {
+    const long long r1 = r0 + 32 < M ? r0 + 32 : M;
+    for (long long r = r0; r < r1; ++r) {
+      const T yb = ld_as<T>(ybar, yd, r * ldy + c);
+      const T hv = ld_as<T>(h, hd, r * ldh + c);
+      const T v = yb * act_grad_h(hv, act);  // mul(ybar, act') (rules.py:87-89)
+      st_as(dz, dzd, r * lddz + c, (double)v);
+      if (dz2) st_as(dz2, dz2d, r * lddz2 + c, (double)v);
+      acc += v;
+    }
+    if (colsum) colsum[g * ldc + c] = (float)acc;
+  }
+}
+
+// --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
+__global__ void __launch_bounds__(256) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
+                                                         float* out) {
+  __shared__ double red[8][33];
+  const long long j = blockIdx.x * 32ll + threadIdx.x;
+  double acc = 0.0;
+  if (j < N)
+    for (long long g = threadIdx.y; g < G; g += 8) acc += (double)part[g * ldp + j];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < N) {
+    double s = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) s += red[y][threadIdx.x];
+    out[j] = (float)s;
+  }
+}
+
+// --- reduce_to over rows in the reference's order: sequential ascending fold
+//     (tensor.py:287-292, 337-338) — STRICT precision bias gradients
+template <class T>
+__global__ void k_colsum_strict(const T* x, long long ld, long long M, long long N, T* out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  T acc = x[j];
+  for (long long r = 1; r < M; ++r) acc = acc + x[r * ld + j];
+  out[j] = acc;
+}
+
+// --- losses.  Per-block loss partial sums (fixed order) -> loss_part[block]
+// MSE: loss = sum((z-y)^2) * scale; dz = d*scale + d*scale (rules.py:53-58 on mul(d,d))
+template <class T>
+__global__ void __launch_bounds__(256) k_mse(const T* z, long long ldz, const T* y, long long ldy, long long M,
+                                             long long N, T scale, void* dz, int dzd, long long lddz, void* dz2,
+                                             int dz2d, long long lddz2, float* colsum, long long ldc,
+                                             double* loss_part) {
+  __shared__ double red[256];
+  const long long c = blockIdx.x * 32ll + threadIdx.x;
+  const long long g = blockIdx.y * 8ll + threadIdx.y;
+  const long long r0 = g * 32;
+  double lsum = 0.0;
+  if (r0 < M && c < N) {
+    T acc = (T)0;
+    const long long r1 = r0 + 32 < M ? r0 + 32 : M;
+    for (long long r = r0; r < r1; ++r) {
+      const T d = z[r * ldz + c] - y[r * ldy + c];
+      lsum += (double)d * (double)d;
+      const T v = d * scale + d * scale;
+      st_as(dz, dzd, r * lddz + c, (double)v);
+      if (dz2) st_as(dz2, dz2d, r * lddz2 + c, (double)v);
+      acc += v;
+    }
+    if (colsum) colsum[g * ldc + c] = (float)acc;
+  }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  red[tid] = lsum;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s) red[tid] += red[tid + s];
+    __syncthreads();
+  }
+  if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+}
+
+// softmax cross-entropy, warp per row (N <= 1024):
+//   loss_row = -sum_j y_j log p_j ; dz = (p * sum_j y_j - y) * scale  (scale = 1/n)
+// Lanes own columns lane + 32t; each warp walks 32 consecutive rows so the
+// column sums for the bias gradient stay in registers.
+template <class T>
+__global__ void __launch_bounds__(256) k_softmax_xent(const T* z, long long ldz, const T* y, long long ldy,
+                                                      long long M, long long N, T scale, void* dz, int dzd,
+                                                      long long lddz, void* dz2, int dz2d, long long lddz2,
+                                                      float* colsum, long long ldc, double* loss_part) {
+  __shared__ double red[8];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const long long g = blockIdx.x * 8ll + w;  // 32-row group
+  const long long r0 = g * 32;
+  constexpr int MAXT = 32;                   // N <= 1024
+  T csum[MAXT];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) csum[t] = (T)0;
+  const int nt = (int)((N + 31) / 32);
+  double lsum = 0.0;
+  if (r0 < M) {
+    const long long r1 = r0 + 32 < M ? r0 + 32 : M;
+    for (long long r = r0; r < r1; ++r) {
+      T mx = -INFINITY;
+      for (int t = 0; t < nt; ++t) {
+        const long long c = lane + 32ll * t;
+        if (c < N) mx = max(mx, z[r * ldz + c]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      T se = 0, sy = 0, syz = 0;
+      for (int t = 0; t < nt; ++t) {
+        const long long c = lane + 32ll * t;
+        if (c < N) {
+          const T zc = z[r * ldz + c] - mx;
+          const T yc = y[r * ldy + c];
+          se += exp(zc);
+          sy += yc;
+          syz += yc * zc;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        se += __shfl_xor_sync(0xffffffffu, se, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        syz += __shfl_xor_sync(0xffffffffu, syz, o);
+      }
+      const T lse = log(se);
+      if (lane == 0) lsum += (double)(sy * lse - syz);  // -sum y (z - mx - lse)
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        const long long c = lane + 32ll * t;
+        if (t < nt && c < N) {
+          const T p = exp(z[r * ldz + c] - mx - lse);
+          const T v = (p * sy - y[r * ldy + c]) * scale;
+          st_as(dz, dzd, r * lddz + c, (double)v);
+          if (dz2) st_as(dz2, dz2d, r * lddz2 + c, (double)v);
+          csum[t] += v;
+        }
+      }
+    }
+    if (colsum) {
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        const long long c = lane + 32ll * t;
+        if (t < nt && c < N) colsum[g * ldc + c] = (float)csum[t];
+      }
+    }
+  }
+  if (lane == 0) red[w] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int i = 0; i < 8; ++i) s += red[i];
+    loss_part[blockIdx.x] = s * (double)scale;
+  }
+}
+
+__global__ void k_sum_loss(const double* part, long long n, double* out) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 256) acc += part[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// --- SGD over the flat parameter buffer + bf16 shadow copy for the next GEMMs
+template <class T>
+__global__ void k_sgd(T* p, const T* g, long long n, T lr, __nv_bfloat16* shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const T v = p[i] - lr * g[i];
+    p[i] = v;
+    if (shadow) shadow[i] = __float2bfloat16_rn((float)v);
+  }
+}
+__global__ void k_sgd_vec(float4* p, const float4* g, long long n4, float lr, uint2* shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 v = p[i];
+    const float4 d = __ldcs(g + i);
+    v.x -= lr * d.x;
+    v.y -= lr * d.y;
+    v.z -= lr * d.z;
+    v.w -= lr * d.w;
+    p[i] = v;
+    if (shadow) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+      shadow[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+  }
+}
+
+__global__ void k_cast(const void* src, int sd, void* dst, int dd, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    st_as(dst, dd, i, ld_as<double>(src, sd, i));
+}
+
+}  // namespace dk
+
+int ctx_num_sms(sg_ctx* ctx);
+int ctx_activate(sg_ctx* ctx);
+
+}  // namespace sg
+
+using namespace sg;
+
+namespace {
+inline unsigned cap_grid(long long n, int block, long long cap) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+inline bool fdt(int d) { return d == SG_F32 || d == SG_F64; }
+}  // namespace
+
+extern "C" {
+
+int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y, const void* h, int32_t h_dtype,
+                int64_t ld_h, int64_t M, int64_t N, int32_t act, void* dz, int32_t dz_dtype, int64_t ld_dz,
+                void* dz2, int32_t dz2_dtype, int64_t ld_dz2, float* colsum, int64_t ld_colsum, void* stream) {
+  if (!ctx || !ybar || !h || !dz) return fail(SG_EINVAL, "null argument");
+  if (M <= 0 || N <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
+  if (grid.y > 65535) return fail(SG_EINVAL, "act_grad: M too large");
+  const bool f64 = ybar_dtype == SG_F64;
+  if (f64)
+    dk::k_act_grad<double><<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
+        ybar, ybar_dtype, ld_y, h, h_dtype, ld_h, M, N, act, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
+        ld_colsum);
+  else
+    dk::k_act_grad<float><<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
+        ybar, ybar_dtype, ld_y, h, h_dtype, ld_h, M, N, act, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
+        ld_colsum);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_part, int64_t N, float* out,
+                       void* stream) {
+  if (!ctx || !part || !out) return fail(SG_EINVAL, "null argument");
+  if (N <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  dk::k_colsum_finalize<<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
+                                                                                             out);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t ld, int64_t M, int64_t N, void* out,
+                     void* stream) {
+  if (!ctx || !x || !out) return fail(SG_EINVAL, "null argument");
+  if (!fdt(dtype)) return fail(SG_EINVAL, "colsum_strict: f32/f64 only");
+  if (M <= 0 || N <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  if (dtype == SG_F64)
+    dk::k_colsum_strict<double><<<cap_grid(N, 128, 1 << 20), 128, 0, (cudaStream_t)stream>>>(
+        (const double*)x, ld, M, N, (double*)out);
+  else
+    dk::k_colsum_strict<float><<<cap_grid(N, 128, 1 << 20), 128, 0, (cudaStream_t)stream>>>(
+        (const float*)x, ld, M, N, (float*)out);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_z, const void* y, int64_t ld_y,
+            int64_t M, int64_t N, double scale, double* loss, double* loss_part, int64_t n_part, void* dz,
+            int32_t dz_dtype, int64_t ld_dz, void* dz2, int32_t dz2_dtype, int64_t ld_dz2, float* colsum,
+            int64_t ld_colsum, void* stream) {
+  if (!ctx || !z || !y || !dz || !loss || !loss_part) return fail(SG_EINVAL, "null argument");
+  if (!fdt(dtype)) return fail(SG_EINVAL, "loss: logits must be f32/f64");
+  if (M <= 0 || N <= 0) return fail(SG_EINVAL, "loss: empty batch");
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  long long blocks = 0;
+  if (kind == SG_LOSS_MSE) {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
+    if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
+    blocks = (long long)grid.x * grid.y;
+    if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
+    if (dtype == SG_F64)
+      dk::k_mse<double><<<grid, dim3(32, 8), 0, st>>>((const double*)z, ld_z, (const double*)y, ld_y, M, N,
+                                                       scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
+                                                       ld_colsum, loss_part);
+    else
+      dk::k_mse<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
+                                                      (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
+                                                      colsum, ld_colsum, loss_part);
+  } else if (kind == SG_LOSS_SOFTMAX_XENT) {
+    if (N > 1024) return fail(SG_EINVAL, "softmax_xent: at most 1024 classes");
+    blocks = (M + 255) / 256;
+    if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
+    if (dtype == SG_F64)
+      dk::k_softmax_xent<double><<<(unsigned)blocks, 256, 0, st>>>(
+          (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
+          colsum, ld_colsum, loss_part);
+    else
+      dk::k_softmax_xent<float><<<(unsigned)blocks, 256, 0, st>>>(
+          (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
+          ld_dz2, colsum, ld_colsum, loss_part);
+  } else {
+    return fail(SG_EINVAL, "loss: unknown kind");
+  }
+  SG_CUDA_TRY(cudaGetLastError());
+  dk::k_sum_loss<<<1, 256, 0, st>>>(loss_part, blocks, loss);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t n, double lr, void* shadow_bf16,
+           void* stream) {
+  if (!ctx || !params || !grads) return fail(SG_EINVAL, "null argument");
+  if (!fdt(dtype)) return fail(SG_EINVAL, "sgd: f32/f64 parameters");
+  if (n <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long cap = (long long)ctx_num_sms(ctx) * 8;
+  const bool vec = dtype == SG_F32 && n % 4 == 0 && ((uintptr_t)params % 16) == 0 &&
+                   ((uintptr_t)grads % 16) == 0 && (!shadow_bf16 || ((uintptr_t)shadow_bf16 % 8) == 0);
+  if (vec)
+    dk::k_sgd_vec<<<cap_grid(n / 4, 256, cap), 256, 0, st>>>((float4*)params, (const float4*)grads, n / 4,
+                                                              (float)lr, (uint2*)shadow_bf16);
+  else if (dtype == SG_F32)
+    dk::k_sgd<float><<<cap_grid(n, 256, cap), 256, 0, st>>>((float*)params, (const float*)grads, n, (float)lr,
+                                                             (__nv_bfloat16*)shadow_bf16);
+  else
+    dk::k_sgd<double><<<cap_grid(n, 256, cap), 256, 0, st>>>((double*)params, (const double*)grads, n, lr,
+                                                              (__nv_bfloat16*)shadow_bf16);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n, void* stream) {
+  if (!ctx || !src || !dst) return fail(SG_EINVAL, "null argument");
+  if (n <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  dk::k_cast<<<cap_grid(n, 256, (long long)ctx_num_sms(ctx) * 16), 256, 0, (cudaStream_t)stream>>>(
+      src, src_dtype, dst, dst_dtype, n);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+}  // extern "C"

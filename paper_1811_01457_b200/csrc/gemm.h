@@ -21,7 +21,26 @@ struct GemmEpilogue {
   long long ld_f32;
   __nv_bfloat16* out_bf16;     // optional bf16 result
   long long ld_bf16;
+  float* colsum;               // optional column sums of the result per 32-row group:
+  long long ld_colsum;         //   colsum[(m / 32)][n], [ceil(M/32)][ld_colsum]
 };
+
+// Column sums of a 32x32 block held one row per lane (v[i] = column i):
+// a 31-shuffle transpose-reduce leaves column L's sum in lane L, summed in a
+// fixed order (deterministic).  v is destroyed.
+__device__ __forceinline__ void warp_colsum_store(float (&v)[32], float* dst, int lane, int n) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = upper ? v[i] : v[i + s];
+      const float keep = upper ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  if (lane < n) dst[lane] = v[0];
+}
 
 struct GemmArgs {
   int M, N, K;

@@ -46,6 +46,8 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     g.epi.ld_f32 = d->ld_out;
     g.epi.out_bf16 = (__nv_bfloat16*)d->out_lp;
     g.epi.ld_bf16 = d->ld_lp;
+    g.epi.colsum = d->colsum;
+    g.epi.ld_colsum = d->ld_colsum;
     return launch_gemm_bf16(g, ctx_num_sms(ctx), st);
   }
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {

@@ -309,8 +309,17 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
         const int n0 = tc.n0 + c * 32;
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
-        if (n0 >= p.N || !row_ok) continue;
+        if (n0 >= p.N) continue;  // warp-uniform
         const bool full = n0 + 32 <= p.N;
+        if (!row_ok) {
+          if (e.colsum) {  // rows past M contribute zeros to the column sums
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            warp_colsum_store(v, e.colsum + (long long)((tc.m0 >> 5) + q) * e.ld_colsum + n0, lane,
+                              full ? 32 : p.N - n0);
+          }
+          continue;
+        }
         if (e.mode == SG_EPI_BIAS_ACT) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -328,6 +337,11 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
         }
         if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, full ? 32 : p.N - n0);
         if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, full ? 32 : p.N - n0);
+        // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
+        // transpose-reduce destroys v, so it runs after the stores
+        if (e.colsum)
+          warp_colsum_store(v, e.colsum + (long long)((tc.m0 >> 5) + q) * e.ld_colsum + n0, lane,
+                            full ? 32 : p.N - n0);
       }
       tc_fence_before();
       __syncwarp();

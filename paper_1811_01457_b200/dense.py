@@ -1,0 +1,379 @@
+"""Dense layers, Chain, and the device engine of one training step.
+
+Mirrors the reference's Dense recipe (``nn_train._batch_trunk`` /
+``_batch_head``, nn_train.py:189-210)::
+
+    wt = transpose(W); z = matmul(h, wt); zb = add(z, b); h' = act(zb)
+
+with ``DenseLayerParams(W: out x in, b: out)`` (nn_train.py:40-45) and the
+parameter order ``[W0, b0, W1, b1, ...]`` of ``_weight_args``
+(nn_train.py:99-103), which is also the order of the flat gradient buffer
+that data parallelism all-reduces.
+
+HBM layout of :class:`ChainEngine` (one per GPU):
+
+* ``P`` flat master parameters (fp32; fp64 in STRICT_FP64), ``G`` the flat
+  gradients in the same layout, ``S`` a bf16 shadow of ``P`` that the SGD
+  kernel rewrites for the next step's tensor-core GEMMs.  Each ``W`` is
+  stored row-major ``[out][ld(in)]`` with ``ld`` rounded up to 8 elements
+  and every segment 256-byte aligned (TMA row-stride/alignment rules);
+* activations ``H[l]`` ``[B][ld(d_l)]`` in bf16 (saved for ``act'`` and as
+  the next layer's input and the dW operand), top-layer outputs ``Zt`` in
+  fp32 for the loss, two ping-pong ``dZ`` buffers, per-32-row column-sum
+  partials for the bias gradients.
+
+Precision modes: ``bf16`` (tcgen05 tensor cores, fp32 accumulate),
+``strict_fp32`` / ``strict_fp64`` (ordered CUDA-core GEMMs, reference
+fold order, everything in fp32/fp64).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import runtime as rt
+from .gemm import ACT, gemm
+from .tape import Tape, TapeEntry
+
+LOSSES = {"softmax_xent": 0, "mse": 1}
+
+
+def _ld(d: int) -> int:
+    return (d + 7) // 8 * 8
+
+
+@dataclass
+class Dense:
+    """One dense layer ``act.(W * x .+ b)`` with W of shape (out, in)."""
+
+    fan_in: int
+    fan_out: int
+    act: str = "identity"
+    W: np.ndarray | None = None
+    b: np.ndarray | None = None
+
+    def __post_init__(self):
+        if self.act not in ACT:
+            raise ValueError(f"unknown activation {self.act!r}")
+
+
+class Chain:
+    """Sequential composition of Dense layers (Flux ``Chain``)."""
+
+    def __init__(self, *layers: Dense):
+        if not layers:
+            raise ValueError("Chain needs at least one layer")
+        for a, b in zip(layers, layers[1:]):
+            if a.fan_out != b.fan_in:
+                raise ValueError(f"layer sizes do not chain: {a.fan_out} -> {b.fan_in}")
+        self.layers = list(layers)
+
+    @property
+    def sizes(self) -> tuple:
+        return (self.layers[0].fan_in,) + tuple(l.fan_out for l in self.layers)
+
+    @property
+    def acts(self) -> tuple:
+        return tuple(l.act for l in self.layers)
+
+    def init_params(self, rng: np.random.Generator, bias: float = 0.0):
+        """Uniform fan-in/fan-out init of init_params (nn_train.py:130-140)."""
+        for l in self.layers:
+            r = math.sqrt(6.0 / (l.fan_in + l.fan_out))
+            l.W = rng.uniform(-r, r, (l.fan_out, l.fan_in)).astype(np.float32)
+            l.b = np.full(l.fan_out, bias, dtype=np.float32)
+        return self
+
+
+# ---------------------------------------------------------------- C binding
+_bound = False
+
+
+def _lib():
+    global _bound
+    lib = rt.load_library()
+    if not _bound:
+        P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        lib.sg_act_grad.argtypes = [P, P, I32, I64, P, I32, I64, I64, I64, I32, P, I32, I64, P, I32, I64,
+                                    P, I64, P]
+        lib.sg_colsum_finalize.argtypes = [P, P, I64, I64, I64, P, P]
+        lib.sg_colsum_strict.argtypes = [P, P, I32, I64, I64, I64, P, P]
+        lib.sg_loss.argtypes = [P, I32, P, I32, I64, P, I64, I64, I64, D, P, P, I64, P, I32, I64, P, I32,
+                                I64, P, I64, P]
+        lib.sg_sgd.argtypes = [P, P, P, I32, I64, D, P, P]
+        lib.sg_cast.argtypes = [P, P, I32, P, I32, I64, P]
+        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast"):
+            getattr(lib, n).restype = ctypes.c_int
+        _bound = True
+    return lib
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _dt(t):
+    return rt.dtype_code(t.dtype)
+
+
+class DenseLayer:
+    """One Dense layer's forward and pullback with preallocated device buffers.
+
+    The single-layer form of the chain engine, used for the c3 workload
+    (one Dense 4096->4096 fwd + pullback with an external seed ybar):
+
+    * forward:  H = act(X . W^T + b)   -- one tcgen05 GEMM, bias+act epilogue
+    * pullback: dZ = ybar .* act'(H)   (+ per-32-row column sums)
+                dX = dZ . W            -- GEMM, W read MN-major
+                dW = dZ^T . X          -- GEMM, both operands MN-major
+                db = colsum(dZ)        -- finalize of the partial sums
+    """
+
+    def __init__(self, M: int, fan_in: int, fan_out: int, act: str = "sigmoid"):
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.M, self.K, self.N, self.act = M, fan_in, fan_out, act
+        bf = torch.bfloat16
+        self.X = torch.zeros((M, _ld(fan_in)), dtype=bf, device=dev)[:, :fan_in]
+        self.W = torch.zeros((fan_out, _ld(fan_in)), dtype=torch.float32, device=dev)[:, :fan_in]
+        self.Wb = torch.zeros((fan_out, _ld(fan_in)), dtype=bf, device=dev)[:, :fan_in]
+        self.b = torch.zeros(fan_out, dtype=torch.float32, device=dev)
+        self.H = torch.zeros((M, _ld(fan_out)), dtype=bf, device=dev)[:, :fan_out]
+        self.dZ = torch.zeros((M, _ld(fan_out)), dtype=bf, device=dev)[:, :fan_out]
+        self.dX = torch.zeros((M, _ld(fan_in)), dtype=torch.float32, device=dev)[:, :fan_in]
+        self.dW = torch.zeros((fan_out, _ld(fan_in)), dtype=torch.float32, device=dev)[:, :fan_in]
+        self.db = torch.zeros(fan_out, dtype=torch.float32, device=dev)
+        self.colsum = torch.zeros(((M + 31) // 32, _ld(fan_out)), dtype=torch.float32, device=dev)
+
+    def set_params(self, W, b):
+        import torch
+
+        self.W.copy_(torch.as_tensor(np.asarray(W), dtype=torch.float32))
+        self.Wb.copy_(self.W.to(torch.bfloat16))
+        self.b.copy_(torch.as_tensor(np.asarray(b), dtype=torch.float32))
+
+    def forward(self, X=None):
+        if X is not None:
+            self.X.copy_(X, non_blocking=True)
+        gemm(self.X, self.Wb, epilogue="bias_act", act=self.act, bias=self.b, out_lp=self.H)
+        return self.H
+
+    def pullback(self, ybar, need_dx: bool = True):
+        lib = _lib()
+        ctx, st = rt.context(), rt.stream_ptr()
+        rt.check(lib.sg_act_grad(ctx, _p(ybar), _dt(ybar), ybar.stride(0), _p(self.H), _dt(self.H),
+                                 self.H.stride(0), self.M, self.N, ACT[self.act], _p(self.dZ), _dt(self.dZ),
+                                 self.dZ.stride(0), None, 0, 0, _p(self.colsum), self.colsum.stride(0), st),
+                 "sg_act_grad")
+        if need_dx:
+            gemm(self.dZ, self.Wb, b_mn=True, out=self.dX)
+        gemm(self.dZ, self.X, a_mn=True, b_mn=True, out=self.dW)
+        rt.check(lib.sg_colsum_finalize(ctx, _p(self.colsum), (self.M + 31) // 32, self.colsum.stride(0),
+                                        self.N, _p(self.db), st), "sg_colsum_finalize")
+        return self.dX, self.dW, self.db
+
+    def flops(self, need_dx: bool = True) -> float:
+        return 2.0 * self.M * self.K * self.N * (3 if need_dx else 2)
+
+
+class ChainEngine:
+    """Device state + kernels of a Dense chain's training step on one GPU."""
+
+    def __init__(self, chain: Chain, batch: int, loss: str = "mse", precision: str = "bf16",
+                 global_batch: int | None = None):
+        import torch
+
+        if loss not in LOSSES:
+            raise ValueError(f"unknown loss {loss!r}")
+        if precision not in ("bf16", "strict_fp32", "strict_fp64"):
+            raise ValueError(f"unknown precision {precision!r}")
+        self.chain = chain
+        self.B = int(batch)
+        self.loss_kind = loss
+        self.precision = precision
+        self.scale = 1.0 / float(global_batch or batch)
+        self.sizes = chain.sizes
+        self.acts = chain.acts
+        self.L = len(chain.layers)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.mdt = torch.float64 if precision == "strict_fp64" else torch.float32  # master dtype
+        self.adt = torch.bfloat16 if precision == "bf16" else self.mdt          # activation dtype
+        self.gprec = "bf16" if precision == "bf16" else precision
+
+        # flat parameter layout [W0, b0, W1, b1, ...], 64-element (256 B) aligned segments
+        off = 0
+        self.seg = []
+        for l in chain.layers:
+            wo = off
+            off += l.fan_out * _ld(l.fan_in)
+            off = (off + 63) // 64 * 64
+            bo = off
+            off += l.fan_out
+            off = (off + 63) // 64 * 64
+            self.seg.append((wo, bo))
+        self.numel = off
+        self.P = torch.zeros(off, dtype=self.mdt, device=dev)
+        self.G = torch.zeros(off, dtype=self.mdt, device=dev)
+        self.S = torch.zeros(off, dtype=torch.bfloat16, device=dev) if precision == "bf16" else None
+        self.W, self.b, self.gW, self.gb, self.Ws = [], [], [], [], []
+        for l, (wo, bo) in zip(chain.layers, self.seg):
+            ldi = _ld(l.fan_in)
+            n = l.fan_out * ldi
+            self.W.append(self.P[wo:wo + n].view(l.fan_out, ldi)[:, :l.fan_in])
+            self.gW.append(self.G[wo:wo + n].view(l.fan_out, ldi)[:, :l.fan_in])
+            self.b.append(self.P[bo:bo + l.fan_out])
+            self.gb.append(self.G[bo:bo + l.fan_out])
+            if self.S is not None:
+                self.Ws.append(self.S[wo:wo + n].view(l.fan_out, ldi)[:, :l.fan_in])
+        self.bucket_bounds = [(wo, (bo + l.fan_out + 63) // 64 * 64)
+                              for l, (wo, bo) in zip(chain.layers, self.seg)]
+
+        B = self.B
+        self.H = [torch.zeros((B, _ld(d)), dtype=self.adt, device=dev)[:, :d] for d in self.sizes[:-1]]
+        dL = self.sizes[-1]
+        self.Zt = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
+        self.Y = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
+        dmax = max(self.sizes[1:])
+        self.dZ = [torch.zeros((B, _ld(dmax)), dtype=self.adt, device=dev) for _ in range(2)]
+        self.dH = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
+        self.colsum = torch.zeros(((B + 31) // 32, _ld(dmax)), dtype=torch.float32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        n_part = max(1, ((dmax + 31) // 32) * ((B + 255) // 256))
+        self.loss_part = torch.zeros(n_part, dtype=torch.float64, device=dev)
+        self.tape = Tape()
+        self.grad_ready = None  # optional callback(layer_index) when layer l's gradients are written
+        if chain.layers[0].W is not None:
+            self.set_params([(l.W, l.b) for l in chain.layers])
+
+    # ---------------------------------------------------------- parameters
+    def set_params(self, params) -> None:
+        import torch
+
+        for l, (W, b) in enumerate(params):
+            self.W[l].copy_(torch.as_tensor(np.asarray(W), dtype=self.mdt))
+            self.b[l].copy_(torch.as_tensor(np.asarray(b), dtype=self.mdt))
+        if self.S is not None:
+            self.S.copy_(self.P.to(torch.bfloat16))
+
+    def get_params(self):
+        return [(self.W[l].double().cpu().numpy(), self.b[l].double().cpu().numpy()) for l in range(self.L)]
+
+    def get_grads(self):
+        return [(self.gW[l].double().cpu().numpy(), self.gb[l].double().cpu().numpy()) for l in range(self.L)]
+
+    # ------------------------------------------------------------- inputs
+    def load_batch(self, X, Y) -> None:
+        """Copy one minibatch into the engine's input/target buffers."""
+        d0 = self.sizes[0]
+        if tuple(X.shape) != (self.B, d0) or tuple(Y.shape) != (self.B, self.sizes[-1]):
+            raise ValueError(f"batch shapes {tuple(X.shape)}, {tuple(Y.shape)} do not match the engine")
+        self.H[0].copy_(X, non_blocking=True)
+        self.Y.copy_(Y, non_blocking=True)
+
+    # ------------------------------------------------------------ forward
+    def forward(self):
+        """Record the forward pass on the tape; returns the top-layer outputs."""
+        self.tape.clear()
+        L = self.L
+        for l in range(L):
+            last = l == L - 1
+            Wop = self.Ws[l] if self.precision == "bf16" else self.W[l]
+            if self.precision == "bf16":
+                gemm(self.H[l], Wop, epilogue="bias_act", act=self.acts[l], bias=self.b[l],
+                     out_lp=None if last else self.H[l + 1], out=self.Zt if last else None)
+            else:
+                gemm(self.H[l], Wop, precision=self.gprec, epilogue="bias_act", act=self.acts[l],
+                     bias=self.b[l], out=self.Zt if last else self.H[l + 1])
+            self.tape.push(TapeEntry(f"dense{l}", (self.H[l], self.W[l]),
+                                     self._make_backward(l), self._ready(l)))
+        return self.Zt
+
+    def _ready(self, l):
+        def cb(_entry):
+            if self.grad_ready is not None:
+                self.grad_ready(l)
+        return cb
+
+    # --------------------------------------------------------------- loss
+    def loss_and_seed(self):
+        """Fused loss fwd+grad: loss scalar and dZ of the top layer (+ its bias sums)."""
+        lib = _lib()
+        ctx, st = rt.context(), rt.stream_ptr()
+        top = self.L - 1
+        dL = self.sizes[-1]
+        dz = self.dZ[top % 2][:, :dL]
+        ident = self.acts[top] == "identity"
+        strict = self.precision != "bf16"
+        target = dz if ident else self.dH
+        rt.check(lib.sg_loss(ctx, LOSSES[self.loss_kind], _p(self.Zt), _dt(self.Zt), self.Zt.stride(0),
+                             _p(self.Y), self.Y.stride(0), self.B, dL, self.scale, _p(self.loss),
+                             _p(self.loss_part), self.loss_part.numel(), _p(target), _dt(target),
+                             target.stride(0), None, 0, 0,
+                             None if (strict or not ident) else _p(self.colsum), self.colsum.stride(0), st),
+                 "sg_loss")
+        if not ident:  # top activation: dz = dL/dh * act'(h)  (rules.py:82-94)
+            rt.check(lib.sg_act_grad(ctx, _p(self.dH), _dt(self.dH), self.dH.stride(0), _p(self.Zt),
+                                     _dt(self.Zt), self.Zt.stride(0), self.B, dL, ACT[self.acts[top]],
+                                     _p(dz), _dt(dz), dz.stride(0), None, 0, 0,
+                                     None if strict else _p(self.colsum), self.colsum.stride(0), st),
+                     "sg_act_grad")
+        return self.loss
+
+    # ----------------------------------------------------------- pullback
+    def _make_backward(self, l):
+        def backward(_ctx):
+            lib = _lib()
+            ctx, st = rt.context(), rt.stream_ptr()
+            d_out, d_in = self.sizes[l + 1], self.sizes[l]
+            dz = self.dZ[l % 2][:, :d_out]
+            strict = self.precision != "bf16"
+            # dW = dZ^T . H[l]   (rules.py:113-115 second cotangent, then _transpose)
+            gemm(dz, self.H[l], a_mn=True, b_mn=True, precision=self.gprec, out=self.gW[l])
+            # db = reduce_like(dZ, (out,))   (rules.py:45-46)
+            if strict:
+                rt.check(lib.sg_colsum_strict(ctx, _p(dz), _dt(dz), dz.stride(0), self.B, d_out,
+                                              _p(self.gb[l]), st), "sg_colsum_strict")
+            else:
+                rt.check(lib.sg_colsum_finalize(ctx, _p(self.colsum), (self.B + 31) // 32,
+                                                self.colsum.stride(0), d_out, _p(self.gb[l]), st),
+                         "sg_colsum_finalize")
+            if l > 0:
+                # dH[l] = dZ . W, fused with act' of the layer below -> dZ[l-1]
+                dzn = self.dZ[(l - 1) % 2][:, :d_in]
+                Wop = self.Ws[l] if self.precision == "bf16" else self.W[l]
+                if strict:
+                    gemm(dz, Wop, b_mn=True, precision=self.gprec, epilogue="act_grad",
+                         act=self.acts[l - 1], aux=self.H[l], out=dzn)
+                else:
+                    gemm(dz, Wop, b_mn=True, epilogue="act_grad", act=self.acts[l - 1], aux=self.H[l],
+                         out_lp=dzn, colsum=self.colsum)
+        return backward
+
+    def pullback(self):
+        self.tape.pullback()
+
+    # ---------------------------------------------------------------- SGD
+    def sgd(self, lr: float):
+        lib = _lib()
+        rt.check(lib.sg_sgd(rt.context(), _p(self.P), _p(self.G), _dt(self.P), self.numel, float(lr),
+                            _p(self.S), rt.stream_ptr()), "sg_sgd")
+
+    def step(self, lr: float):
+        """forward + loss + pullback + SGD on the loaded batch (all device-side)."""
+        self.forward()
+        self.loss_and_seed()
+        self.pullback()
+        self.sgd(lr)
+        return self.loss
+
+    def flops_per_step(self, skip_first_dx: bool = True) -> float:
+        f = 0.0
+        for l in range(self.L):
+            mnk = self.B * self.sizes[l] * self.sizes[l + 1]
+            f += 2 * mnk * (3 if (l > 0 or not skip_first_dx) else 2)
+        return f

@@ -32,6 +32,7 @@ class GemmDesc(ctypes.Structure):
         ("out_pre", ctypes.c_void_p), ("ld_pre", ctypes.c_int64),
         ("out", ctypes.c_void_p), ("ld_out", ctypes.c_int64),
         ("out_lp", ctypes.c_void_p), ("ld_lp", ctypes.c_int64),
+        ("colsum", ctypes.c_void_p), ("ld_colsum", ctypes.c_int64),
     ]
 
 
@@ -62,8 +63,12 @@ def _ld(t):
 
 def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
          epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-         out_pre=None, stream=None):
-    """Launch one GEMM; outputs are written in place into the given tensors."""
+         out_pre=None, colsum=None, stream=None):
+    """Launch one GEMM; outputs are written in place into the given tensors.
+
+    ``colsum`` (fp32 ``[ceil(M/32)][>=N]``) receives per-32-row column sums of
+    the result (the first stage of a bias gradient).
+    """
     if a_mn:
         Ka, Ma = A.shape
     else:
@@ -87,4 +92,5 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     d.out_pre, d.ld_pre = _ptr(out_pre), _ld(out_pre)
     d.out, d.ld_out = _ptr(out), _ld(out)
     d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
+    d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
     rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")

@@ -1,0 +1,168 @@
+"""GPU parity of the Dense training step against the reference.
+
+Golden vectors: the unmodified reference's `grad` through Dense-chain IR
+(tests/golden/mlp_*.npz, dense_sigmoid.npz).  Larger shapes: the pinned
+oracle (oracle/dense.py).  Tolerances, per tensor, relative to the
+tensor's largest magnitude (norm-relative, stricter than the elementwise
+rel metric for small gradients):
+  bf16 tensor-core path   <= 1e-2  (north star, TF32/BF16 GEMMs)
+  strict_fp32             <= 1e-5
+  strict_fp64             <= 1e-12 (only exp/tanh libm ulps differ)
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_npz
+from oracle import dense as OD
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1811_01457_b200.dense import Chain, ChainEngine, Dense, DenseLayer  # noqa: E402
+from paper_1811_01457_b200.train import Trainer  # noqa: E402
+
+TOL = {"bf16": 1e-2, "strict_fp32": 1e-5, "strict_fp64": 1e-12}
+
+
+def nrel(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-30))
+
+
+def chain_from(z, acts):
+    sizes = [int(s) for s in z["sizes"]]
+    layers = [Dense(sizes[i], sizes[i + 1], acts[i], z[f"W{i}"].astype(np.float64),
+                    z[f"b{i}"].astype(np.float64)) for i in range(len(acts))]
+    return Chain(*layers)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "strict_fp32", "strict_fp64"])
+@pytest.mark.parametrize("name,acts,loss", [
+    ("mlp_c1_b32.npz", ("sigmoid", "identity"), "softmax_xent"),
+    ("mlp_mse.npz", ("tanh", "tanh", "identity"), "mse"),
+])
+def test_chain_gradients_match_reference(precision, name, acts, loss):
+    z = load_npz(name)
+    chain = chain_from(z, acts)
+    n = z["X"].shape[0]
+    tr = Trainer(chain, n, loss=loss, precision=precision)
+    dt = torch.float64 if precision == "strict_fp64" else torch.float32
+    X = torch.from_numpy(z["X"]).to(dt).cuda()
+    Y = torch.from_numpy(z["Y"]).to(dt).cuda()
+    lv, grads = tr.gradient(X, Y)
+    tol = TOL[precision]
+    assert abs(lv - z["loss"][0]) <= tol * max(1.0, abs(z["loss"][0]))
+    for k, (gW, gb) in enumerate(grads):
+        assert nrel(gW, z[f"dW{k}"]) <= tol, (k, nrel(gW, z[f"dW{k}"]))
+        assert nrel(gb, z[f"db{k}"]) <= tol, (k, nrel(gb, z[f"db{k}"]))
+
+
+@pytest.mark.parametrize("precision", ["bf16", "strict_fp64"])
+def test_sgd_step_matches_oracle(precision):
+    z = load_npz("mlp_c1_b32.npz")
+    acts = ("sigmoid", "identity")
+    chain = chain_from(z, acts)
+    tr = Trainer(chain, 32, loss="softmax_xent", lr=0.05, precision=precision)
+    dt = torch.float64 if precision == "strict_fp64" else torch.float32
+    X = torch.from_numpy(z["X"]).to(dt).cuda()
+    Y = torch.from_numpy(z["Y"]).to(dt).cuda()
+    tr.step(X, Y)
+    params = [(z[f"W{k}"].astype(np.float64), z[f"b{k}"].astype(np.float64)) for k in range(2)]
+    _, _, new = OD.mlp_step(params, z["X"].astype(np.float64), z["Y"].astype(np.float64), acts,
+                            "softmax_xent", lr=0.05, mode="exact")
+    got = tr.engine.get_params()
+    for (W, b), (Wn, bn), (W0, b0) in zip(got, new, params):
+        # compare the update itself (p_new - p_old) against the oracle's
+        assert nrel(W - W0, Wn - W0) <= TOL[precision] * 10
+        assert nrel(b - b0, bn - b0) <= TOL[precision] * 10
+
+
+def test_dense_layer_pullback_matches_reference():
+    z = load_npz("dense_sigmoid.npz")
+    W, b = z["W0"].astype(np.float64), z["b0"].astype(np.float64)
+    X, Ybar = z["X"].astype(np.float64), z["Y"].astype(np.float64)
+    layer = DenseLayer(X.shape[0], W.shape[1], W.shape[0], "sigmoid")
+    layer.set_params(W, b)
+    layer.forward(torch.from_numpy(X).to(torch.bfloat16).cuda())
+    dX, dW, db = layer.pullback(torch.from_numpy(Ybar).float().cuda())
+    torch.cuda.synchronize()
+    assert nrel(dX.double().cpu(), z["dX"]) <= 1e-2
+    assert nrel(dW.double().cpu(), z["dW0"]) <= 1e-2
+    assert nrel(db.double().cpu(), z["db0"]) <= 1e-2
+
+
+@pytest.mark.parametrize("sizes,acts,loss,B", [
+    ((784, 32, 10), ("sigmoid", "identity"), "softmax_xent", 128),       # c1 at full size
+    ((256, 256, 256, 256, 256), ("tanh",) * 3 + ("identity",), "mse", 1024),  # c4/c5 shape, scaled
+    ((1024, 1024, 1024), ("tanh", "identity"), "mse", 4096),
+])
+def test_chain_vs_oracle_at_size(sizes, acts, loss, B):
+    rng = np.random.default_rng(B)
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(len(acts))]).init_params(rng)
+    for l in chain.layers:
+        l.b = rng.uniform(-0.1, 0.1, l.fan_out).astype(np.float32)
+    X = rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)
+    if loss == "softmax_xent":
+        Y = np.zeros((B, sizes[-1]), np.float32)
+        Y[np.arange(B), rng.integers(0, sizes[-1], B)] = 1
+    else:
+        Y = rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)
+    tr = Trainer(chain, B, loss=loss, precision="bf16")
+    lv, grads = tr.gradient(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+    # oracle on the same bf16-rounded operands the tensor cores see
+    params = [(l.W.astype(np.float64), l.b.astype(np.float64)) for l in chain.layers]
+    lo, go, _ = OD.mlp_step(params, X.astype(np.float64), Y.astype(np.float64), acts, loss, mode="blas")
+    assert abs(lv - lo) <= 1e-2 * max(1.0, abs(lo))
+    for (gW, gb), (oW, ob) in zip(grads, go):
+        assert nrel(gW, oW) <= 1e-2
+        assert nrel(gb, ob) <= 1e-2
+
+
+def test_cuda_graph_replay_matches_eager_and_is_deterministic():
+    rng = np.random.default_rng(7)
+    sizes, acts = (256, 512, 512, 128), ("tanh", "tanh", "identity")
+    B = 512
+    X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+
+    def run(graph):
+        chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(3)]).init_params(
+            np.random.default_rng(1))
+        tr = Trainer(chain, B, loss="mse", lr=0.1, precision="bf16", graph=graph)
+        losses = [float(tr.step(X, Y).item()) for _ in range(5)]
+        return losses, tr.engine.P.clone()
+
+    l1, p1 = run(False)
+    l2, p2 = run(True)
+    l3, p3 = run(True)
+    assert l1 == l2 == l3
+    assert torch.equal(p1, p2) and torch.equal(p2, p3)
+    assert l1[-1] < l1[0]  # it trains
+
+
+def test_data_parallel_shards_sum_to_full_gradient():
+    """Single-GPU check of the DP math: shard gradients scaled by the global
+    1/B sum to the full-batch gradient (the all-reduce itself is covered by
+    the gloo multi-process test on CPU)."""
+    rng = np.random.default_rng(3)
+    sizes, acts = (128, 256, 64), ("tanh", "identity")
+    B, world = 512, 4
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(2)]).init_params(rng)
+    X = rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)
+    Y = rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)
+    full = ChainEngine(chain, B, "mse", "strict_fp64")
+    full.load_batch(torch.from_numpy(X).double().cuda(), torch.from_numpy(Y).double().cuda())
+    full.forward(); full.loss_and_seed(); full.pullback()
+    acc = torch.zeros_like(full.G)
+    for r in range(world):
+        e = ChainEngine(chain, B // world, "mse", "strict_fp64", global_batch=B)
+        xs = X[r * B // world:(r + 1) * B // world]
+        ys = Y[r * B // world:(r + 1) * B // world]
+        e.load_batch(torch.from_numpy(xs).double().cuda(), torch.from_numpy(ys).double().cuda())
+        e.forward(); e.loss_and_seed(); e.pullback()
+        acc += e.G
+    assert nrel(acc.cpu().numpy(), full.G.cpu().numpy()) <= 1e-12

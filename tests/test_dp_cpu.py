@@ -1,0 +1,116 @@
+"""Multi-process data-parallel host logic on CPU (gloo, world size 2 and 4).
+
+Each rank computes its shard's gradient with the loss scaled by the GLOBAL
+1/B (oracle restatement of the reference pullback), packs it into the
+flat [W0, b0, W1, b1, ...] buffer (nn_train.py:99-103 order) with the
+engine's bucket layout, and the bucketed all-reduce of
+paper_1811_01457_b200.train.DataParallel must reproduce the full-batch
+gradient.  The device kernels are covered by the GPU tests; this checks
+sharding, scaling, bucketing and the collective itself.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import dense as OD
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _layout(sizes):
+    """Same flat layout rule as ChainEngine (64-element aligned segments)."""
+    ld = lambda d: (d + 7) // 8 * 8  # noqa: E731
+    off, segs = 0, []
+    for i in range(len(sizes) - 1):
+        fi, fo = sizes[i], sizes[i + 1]
+        wo = off
+        off = (off + fo * ld(fi) + 63) // 64 * 64
+        bo = off
+        off = (off + fo + 63) // 64 * 64
+        segs.append((wo, bo, fi, fo))
+    return off, segs
+
+
+def _pack(grads, sizes):
+    n, segs = _layout(sizes)
+    flat = np.zeros(n)
+    for (dW, db), (wo, bo, fi, fo) in zip(grads, segs):
+        ldi = (fi + 7) // 8 * 8
+        flat[wo:wo + fo * ldi].reshape(fo, ldi)[:, :fi] = dW
+        flat[bo:bo + fo] = db
+    buckets = [(wo, (bo + fo + 63) // 64 * 64) for wo, bo, fi, fo in segs]
+    return flat, buckets
+
+
+def _shard_grads(params, X, Y, acts, loss, B_global):
+    # loss of the shard with the global mean scale: scale the oracle's 1/n by n/B
+    lv, grads, _ = OD.mlp_step(params, X, Y, acts, loss, mode="blas")
+    f = X.shape[0] / B_global
+    return lv * f, [(dW * f, db * f) for dW, db in grads]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_01457_b200.train import DataParallel, shard_rows
+
+        rng = np.random.default_rng(0)  # same data and params on every rank
+        sizes, acts = (20, 13, 7), ("tanh", "identity")
+        B = 16
+        params = [(rng.uniform(-0.5, 0.5, (sizes[i + 1], sizes[i])), rng.uniform(-0.1, 0.1, sizes[i + 1]))
+                  for i in range(2)]
+        X = rng.uniform(0, 1, (B, sizes[0]))
+        Y = rng.uniform(-1, 1, (B, sizes[-1]))
+        lv, grads = _shard_grads(params, shard_rows(X, rank, world), shard_rows(Y, rank, world), acts, "mse", B)
+        flat, buckets = _pack(grads, sizes)
+        G = torch.from_numpy(flat)
+        dp = DataParallel(G, buckets)
+        for i in reversed(range(len(buckets))):  # pullback order: top layer first
+            dp.ready(i)
+        dp.finish()
+        loss = torch.tensor([lv], dtype=torch.float64)
+        dist.all_reduce(loss)
+        full_lv, full_grads = _shard_grads(params, X, Y, acts, "mse", B)
+        want, _ = _pack(full_grads, sizes)
+        err = float(np.abs(G.numpy() - want).max())
+        q.put((rank, err, abs(float(loss.item()) - full_lv)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bucketed_allreduce_reproduces_full_batch_gradient(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = [q.get(timeout=10) for _ in range(world)]
+    for p in procs:
+        assert p.exitcode == 0
+    for rank, err, lerr in results:
+        assert err <= 1e-12, (rank, err)
+        assert lerr <= 1e-12, (rank, lerr)
+
+
+def test_layout_matches_engine_rule():
+    n, segs = _layout((784, 32, 10))
+    assert all(wo % 64 == 0 and bo % 64 == 0 for wo, bo, _, _ in segs)
+    assert n % 64 == 0
