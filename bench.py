@@ -318,6 +318,148 @@ def cpu_baseline_broadcast(rows=64):
     }
 
 
+# ------------------------------------------------------- dense workloads
+def _timed(fn, steps, warmup, dist, stream, per_step_events=None):
+    """CUDA-event time of `steps` calls (max over ranks), after `warmup` calls."""
+    import torch
+
+    for _ in range(warmup):
+        fn(None)
+    barrier(dist)
+    s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = []
+    s.record(stream)
+    for i in range(steps):
+        ev = None
+        if per_step_events:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(per_step_events)]
+            evs.append(ev)
+        fn(ev)
+    t.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    return max_over_ranks(dist, s.elapsed_time(t)) / steps, evs
+
+
+def dense_c3_bench(args, dist, peaks):
+    """c3: one Dense 4096->4096 (sigmoid) fwd + pullback, batch 8192, bf16 tensor cores."""
+    import torch
+
+    from paper_1811_01457_b200 import runtime as rt
+    from paper_1811_01457_b200.dense import ACT, DenseLayer, _dt, _lib, _p
+    from paper_1811_01457_b200.gemm import gemm
+
+    M, D = 8192, 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    layer = DenseLayer(M, D, D, "sigmoid")
+    r = (6.0 / (2 * D)) ** 0.5
+    layer.W.copy_((torch.rand((D, D), generator=g, device="cuda") * 2 - 1) * r)
+    layer.Wb.copy_(layer.W.to(torch.bfloat16))
+    layer.b.copy_((torch.rand(D, generator=g, device="cuda") * 2 - 1) * 0.01)
+    layer.X.copy_((torch.rand((M, D), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    ybar = torch.rand((M, D), generator=g, device="cuda") * 2 - 1
+    stream = torch.cuda.current_stream()
+    lib, ctx = _lib(), rt.context()
+
+    def step(ev):
+        if ev: ev[0].record(stream)
+        gemm(layer.X, layer.Wb, epilogue="bias_act", act="sigmoid", bias=layer.b, out_lp=layer.H)
+        if ev: ev[1].record(stream)
+        rt.check(lib.sg_act_grad(ctx, _p(ybar), _dt(ybar), ybar.stride(0), _p(layer.H), _dt(layer.H),
+                                 layer.H.stride(0), M, D, ACT["sigmoid"], _p(layer.dZ), _dt(layer.dZ),
+                                 layer.dZ.stride(0), None, 0, 0, _p(layer.colsum), layer.colsum.stride(0),
+                                 rt.stream_ptr()))
+        if ev: ev[2].record(stream)
+        gemm(layer.dZ, layer.Wb, b_mn=True, out=layer.dX)
+        if ev: ev[3].record(stream)
+        gemm(layer.dZ, layer.X, a_mn=True, b_mn=True, out=layer.dW)
+        if ev: ev[4].record(stream)
+        rt.check(lib.sg_colsum_finalize(ctx, _p(layer.colsum), (M + 31) // 32, layer.colsum.stride(0), D,
+                                        _p(layer.db), rt.stream_ptr()))
+        if ev: ev[5].record(stream)
+
+    ms, evs = _timed(step, max(5, args.dense_steps), args.warmup, dist, stream, per_step_events=6)
+    names = ["fwd_gemm", "act_grad", "dX_gemm", "dW_gemm", "db_finalize"]
+    kms = {n: statistics.mean(e[i].elapsed_time(e[i + 1]) for e in evs) for i, n in enumerate(names)}
+    gf = 2.0 * M * D * D
+    gemm_ms = kms["fwd_gemm"] + kms["dX_gemm"] + kms["dW_gemm"]
+    achieved = 3 * gf / (gemm_ms * 1e-3) / 1e12
+    return {
+        "workload": "c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, bf16 tcgen05",
+        "value": round(3 * gf / (ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
+        "flops_per_step": 3 * gf,
+        "kernels_ms": {k: round(v, 4) for k, v in kms.items()},
+        "gemm_TFLOPs": {k: round(gf / (kms[k] * 1e-3) / 1e12, 1) for k in ("fwd_gemm", "dX_gemm", "dW_gemm")},
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (fwd, dX, dW aggregated)",
+                     "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": round(achieved / peaks["bf16_tflops"], 4), "peak_kind": "burst",
+                     "traffic": None},
+        "gpu_launches_per_step": 5,
+        "l2": "working set ~544 MB per step > 126 MB L2",
+    }
+
+
+def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, graph, lr=1e-4):
+    """Dense-chain training step (fwd + loss + pullback + [allreduce] + SGD)."""
+    import torch
+
+    from paper_1811_01457_b200.dense import Chain, Dense
+    from paper_1811_01457_b200.train import Trainer
+
+    rng = np.random.default_rng(11)
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(len(acts))]).init_params(rng)
+    tr = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=graph)
+    lb = tr.local_batch
+    g = torch.Generator(device="cuda").manual_seed(100 + rank)
+    X = torch.rand((lb, sizes[0]), generator=g, device="cuda")
+    if loss == "softmax_xent":
+        Y = torch.zeros((lb, sizes[-1]), device="cuda")
+        Y[torch.arange(lb, device="cuda"), torch.randint(0, sizes[-1], (lb,), generator=g, device="cuda")] = 1
+    else:
+        Y = torch.rand((lb, sizes[-1]), generator=g, device="cuda") * 2 - 1
+    stream = torch.cuda.current_stream()
+    steps = args.mlp_steps if name != "c1" else max(args.mlp_steps, 50)
+    ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
+    loss_v = float(tr.engine.loss.item())
+    flops = tr.engine.flops_per_step() * world
+    tflops = flops / (ms * 1e-3) / 1e12
+    rec = {
+        "workload": f"{name} MLP {'-'.join(map(str, sizes))} ({'/'.join(acts)}, {loss}) train step, "
+                    f"global batch {batch}, bf16 tcgen05" + (f", DP x{world} NCCL" if world > 1 else ""),
+        "value": round(batch / (ms * 1e-3), 1), "unit": "samples/s", "ms_per_step": round(ms, 4),
+        "flops_per_step": flops, "TFLOPs": round(tflops, 1),
+        "roofline": {"bound": "tensor", "kernel": "whole step (GEMM-dominated)", "achieved": round(tflops / world, 1),
+                     "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": round(tflops / world / peaks["bf16_tflops_sustained"], 4),
+                     "peak_kind": "sustained", "traffic": None},
+        "cuda_graph": bool(tr.use_graph), "loss_last": loss_v, "n_gpus": world,
+        "scaling": "strong (global batch fixed)",
+    }
+    return rec
+
+
+def secondary_benches(args, world, rank, dist):
+    peaks = load_peaks()
+    out = []
+    todo = [w.strip() for w in args.secondary.split(",") if w.strip()]
+    for w in todo:
+        try:
+            if w == "c3" and world == 1:
+                out.append(dense_c3_bench(args, dist, peaks))
+            elif w == "c4":
+                out.append(mlp_bench(args, world, rank, dist, peaks, "c4", (4096,) * 5,
+                                     ("tanh",) * 3 + ("identity",), 65536, "mse", graph=False))
+            elif w == "c5":
+                out.append(mlp_bench(args, world, rank, dist, peaks, "c5", (1024,) * 17,
+                                     ("tanh",) * 15 + ("identity",), 32768, "mse", graph=True))
+            elif w == "c1":
+                out.append(mlp_bench(args, world, rank, dist, peaks, "c1", (784, 32, 10),
+                                     ("sigmoid", "identity"), 128, "softmax_xent", graph=True, lr=0.05))
+        except Exception as e:  # report, do not lose the headline line
+            out.append({"workload": w, "error": f"{type(e).__name__}: {e}"[:500]})
+    return out
+
+
 def reference_arm(args, world, rank):
     if rank != 0:
         return None
@@ -357,6 +499,10 @@ def main():
     ap.add_argument("--rows", type=int, default=R_ROWS)
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default="c1,c3,c4,c5",
+                    help="comma list of extra workloads measured in the same run (c1,c3,c4,c5)")
+    ap.add_argument("--dense-steps", type=int, default=20)
+    ap.add_argument("--mlp-steps", type=int, default=10)
     args = ap.parse_args()
     world, rank, local = dist_env()
 
@@ -368,6 +514,8 @@ def main():
 
     dist = init_dist(world, local)
     rec = broadcast_bench(args, world, rank, local, dist)
+    if args.secondary:
+        rec["secondary"] = secondary_benches(args, world, rank, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             rec["cpu_baseline"] = cpu_baseline_broadcast(rows=args.ref_rows)

@@ -68,6 +68,102 @@ __global__ void __launch_bounds__(256) k_act_grad(const void* ybar, int yd, long
   }
 }
 
+// --- vectorised fast paths (fp32 seed/logits, bf16 activations and dZ):
+// thread = 8 consecutive columns, block = 2048 columns x one 32-row group;
+// all global traffic is 16-byte loads/stores, column sums stay in registers.
+struct V8 {
+  float v[8];
+};
+__device__ __forceinline__ V8 ld8_f32(const float* p) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  return V8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+}
+__device__ __forceinline__ V8 ld8_bf16(const __nv_bfloat16* p) {
+  const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+  V8 r;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h[j]);
+    r.v[2 * j] = f.x;
+    r.v[2 * j + 1] = f.y;
+  }
+  return r;
+}
+__device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const V8& x) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(x.v[2 * j], x.v[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ void st8_f32(float* p, const V8& x) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(x.v[4], x.v[5], x.v[6], x.v[7]);
+}
+
+__global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long long ldy, const __nv_bfloat16* h,
+                                                     long long ldh, long long M, long long N, int act,
+                                                     __nv_bfloat16* dz, long long lddz, float* colsum,
+                                                     long long ldc) {
+  const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
+  if (c >= N) return;
+  const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+  for (long long r = r0; r < r1; ++r) {
+    const V8 yb = ld8_f32(ybar + r * ldy + c);
+    const V8 hv = ld8_bf16(h + r * ldh + c);
+    V8 o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      o.v[j] = yb.v[j] * act_grad_h(hv.v[j], act);
+      acc[j] += o.v[j];
+    }
+    st8_bf16(dz + r * lddz + c, o);
+  }
+  if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
+}
+
+__global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, const float* y, long long ldy,
+                                                long long M, long long N, float scale, __nv_bfloat16* dz,
+                                                long long lddz, float* colsum, long long ldc, double* loss_part) {
+  __shared__ double red[256];
+  const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
+  const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
+  double lsum = 0.0;
+  if (c < N) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+    for (long long r = r0; r < r1; ++r) {
+      const V8 zv = ld8_f32(z + r * ldz + c);
+      const V8 yv = ld8_f32(y + r * ldy + c);
+      V8 o;
+      float l = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = zv.v[j] - yv.v[j];
+        l += d * d;
+        o.v[j] = d * scale + d * scale;
+        acc[j] += o.v[j];
+      }
+      lsum += (double)l;
+      st8_bf16(dz + r * lddz + c, o);
+    }
+    if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
+  }
+  red[threadIdx.x] = lsum;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+}
+
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
 __global__ void __launch_bounds__(256) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
                                                          float* out) {
@@ -280,6 +376,17 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
   if (M <= 0 || N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (ybar_dtype == SG_F32 && h_dtype == SG_BF16 && dz_dtype == SG_BF16 && !dz2 && N % 8 == 0 &&
+      ld_y % 8 == 0 && ld_h % 8 == 0 && ld_dz % 8 == 0 && a16(ybar) && a16(h) && a16(dz) &&
+      (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
+    dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
+    dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
+                                                            ld_h, M, N, act, (__nv_bfloat16*)dz, ld_dz, colsum,
+                                                            ld_colsum);
+    SG_CUDA_TRY(cudaGetLastError());
+    return SG_OK;
+  }
   dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
   if (grid.y > 65535) return fail(SG_EINVAL, "act_grad: M too large");
   const bool f64 = ybar_dtype == SG_F64;
@@ -335,7 +442,16 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   long long blocks = 0;
-  if (kind == SG_LOSS_MSE) {
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (kind == SG_LOSS_MSE && dtype == SG_F32 && dz_dtype == SG_BF16 && !dz2 && N % 8 == 0 && ld_z % 8 == 0 &&
+      ld_y % 8 == 0 && ld_dz % 8 == 0 && a16(z) && a16(y) && a16(dz) &&
+      (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
+    dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
+    blocks = (long long)g8.x * g8.y;
+    if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
+    dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                     (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part);
+  } else if (kind == SG_LOSS_MSE) {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
     if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
     blocks = (long long)grid.x * grid.y;

@@ -142,9 +142,12 @@ struct Shape2D {
   bool expand[SG_MAXK];  // operand must be materialised at full shape first
 };
 
+// Capture-safe (no synchronising calls): the primary context was
+// initialised once in sg_create, cudaSetDevice makes it current again.
 int ensure_context(sg_ctx* ctx) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == ctx->device) return SG_OK;
   SG_CUDA_TRY(cudaSetDevice(ctx->device));
-  SG_CUDA_TRY(cudaFree(nullptr));  // make the primary context current for the driver API
   return SG_OK;
 }
 
@@ -484,10 +487,9 @@ int sg_create(int device, sg_ctx** out) {
   if (!out) return fail(SG_EINVAL, "null output");
   auto* ctx = new sg_ctx();
   ctx->device = device;
-  int rc = ensure_context(ctx);
-  if (rc) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) {
     delete ctx;
-    return rc;
+    return fail(SG_ECUDA, "cannot initialise the CUDA primary context");
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (cudaMalloc(&ctx->d_err, sizeof(unsigned long long)) != cudaSuccess) {

@@ -39,8 +39,9 @@ namespace tc {
 constexpr int BM = 128;           // UMMA M (cta_group::1)
 constexpr int BK = 64;            // 64 bf16 = one 128-byte swizzle row
 constexpr int UMMA_K = 16;
-constexpr int NUM_THREADS = 256;  // 8 warps
+constexpr int NUM_THREADS = 384;  // 12 warps: TMA, MMA, TMEM, idle, 8 epilogue
 constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;      // two per TMEM lane quadrant, each takes half the columns
 
 // ------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -131,10 +132,18 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 }
 
 // ------------------------------------------------------------- epilogue
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Epilogue math runs per output element on 8 warps while the tensor cores
+// work on the next tile, so it uses the SFU approximations (rel. error
+// ~2^-11, below the bf16 rounding of the stored activations).
 __device__ __forceinline__ float act_fwd(float z, int act) {
   switch (act) {
-    case SG_ACT_SIGMOID: return 1.0f / (1.0f + __expf(-z));  // tensor.py:214-215
-    case SG_ACT_TANH: return tanhf(z);
+    case SG_ACT_SIGMOID: return __fdividef(1.0f, 1.0f + __expf(-z));  // tensor.py:214-215
+    case SG_ACT_TANH: return tanh_fast(z);
     case SG_ACT_RELU: return z > 0.0f ? z : 0.0f;
     default: return z;
   }
@@ -169,6 +178,10 @@ __device__ __forceinline__ TileCoord tile_of(int t, int m_tiles, int n_tiles, in
 struct KParams {
   int M, N, K;
   GemmEpilogue epi;
+  int splits;         // split-K factor (>= 1); splits > 1 writes raw fp32 partials
+  int kb_per_split;   // k-blocks per split
+  float* part;        // [splits][M][ld_part] when splits > 1
+  long long ld_part;
 };
 
 template <int BN, int STAGES, bool A_MN, bool B_MN>
@@ -194,8 +207,15 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
   const int lane = threadIdx.x % 32;
   const int m_tiles = (p.M + BM - 1) / BM;
   const int n_tiles = (p.N + BN - 1) / BN;
-  const int tiles = m_tiles * n_tiles;
-  const int num_kb = (p.K + BK - 1) / BK;
+  const int out_tiles = m_tiles * n_tiles;
+  const int tiles = out_tiles * p.splits;  // work items: (split, output tile)
+  const int num_kb_total = (p.K + BK - 1) / BK;
+  // k-block range of work item t
+  auto kb_range = [&](int t, int& kb0, int& kb1) {
+    const int s = t / out_tiles;
+    kb0 = s * p.kb_per_split;
+    kb1 = min(num_kb_total, kb0 + p.kb_per_split);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma_a);
@@ -208,7 +228,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&acc_empty[a], EPI_WARPS);  // one arrival per epilogue warp
     }
     fence_barrier_init();
   }
@@ -229,8 +249,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const TileCoord tc = tile_of(t, m_tiles, n_tiles, BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const TileCoord tc = tile_of(t % out_tiles, m_tiles, n_tiles, BN);
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -266,7 +288,9 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
@@ -277,7 +301,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
             // MN-major: next 16 K-rows are +16*128 B (two 8-row core groups)
             const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 64 * BK * 2, 1024) : sdesc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 64 * BK * 2, 1024) : sdesc(sb + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            tc_mma(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc_commit(&empty_bar[stage]);  // smem stage free once these MMAs retire
           if (++stage == STAGES) {
@@ -294,23 +318,33 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
     }
   } else if (warp >= EPI_WARP0) {
     // ===================== epilogue =====================
-    const int q = warp - EPI_WARP0;  // TMEM lanes 32q..32q+31 (warp % 4 == q)
+    const int ew = warp - EPI_WARP0;
+    const int q = ew % 4;   // TMEM lanes 32q..32q+31 (a warp may only touch lanes 32*(warp%4)..)
+    const int half = ew / 4;  // which half of the tile's columns
+    constexpr int CHUNKS = BN / 32;
+    constexpr int CH_PER = CHUNKS / 2;
     const GemmEpilogue& e = p.epi;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const TileCoord tc = tile_of(t, m_tiles, n_tiles, BN);
+      const TileCoord tc = tile_of(t % out_tiles, m_tiles, n_tiles, BN);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int m = tc.m0 + q * 32 + lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * CH_PER; c < (half + 1) * CH_PER; ++c) {
         const int n0 = tc.n0 + c * 32;
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
         const bool full = n0 + 32 <= p.N;
+        if (p.splits > 1) {  // split-K: raw fp32 partial of this K range
+          if (row_ok)
+            store_row_f32(p.part + ((long long)(t / out_tiles) * p.M + m) * p.ld_part + n0, v,
+                          full ? 32 : p.N - n0);
+          continue;
+        }
         if (!row_ok) {
           if (e.colsum) {  // rows past M contribute zeros to the column sums
 #pragma unroll
@@ -321,10 +355,20 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
           continue;
         }
         if (e.mode == SG_EPI_BIAS_ACT) {
+          if (e.bias) {
+            float bv[32];
+            if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float b = (e.bias && (full || n0 + i < p.N)) ? __ldg(e.bias + n0 + i) : 0.0f;
-            v[i] += b;
+              for (int i = 0; i < 32; i += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + i));
+                bv[i] = b4.x, bv[i + 1] = b4.y, bv[i + 2] = b4.z, bv[i + 3] = b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += bv[i];
           }
           if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, full ? 32 : p.N - n0);
 #pragma unroll
@@ -400,6 +444,20 @@ int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer
   return SG_OK;
 }
 
+// split-K finalize: out = sum_s part[s] in ascending s (deterministic)
+__global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
+                                long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
+  const long long total = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long m = e / N, n = e - m * N;
+    float acc = part[m * ldp + n];
+    for (int s = 1; s < S; ++s) acc += part[((long long)s * M + m) * ldp + n];
+    if (out) out[m * ld_out + n] = acc;
+    if (out_lp) out_lp[m * ld_lp + n] = __float2bfloat16_rn(acc);
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN>
 int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   constexpr int STAGE = tc::BM * tc::BK * 2 + BN * tc::BK * 2;
@@ -421,10 +479,39 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
     attr_set = true;
   }
   const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  tc::KParams p{g.M, g.N, g.K, g.epi};
+  const int num_kb = (g.K + tc::BK - 1) / tc::BK;
+  // split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
+  // layer: M = N = 1024, K = batch): plain-store epilogues only
+  int splits = 1, kb_per = num_kb;
+  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && tiles * 2 <= num_sms && num_kb >= 8) {
+    int s = num_sms / tiles;
+    if (s > num_kb / 4) s = num_kb / 4;
+    if (s > 16) s = 16;
+    if (s >= 2) {
+      kb_per = (num_kb + s - 1) / s;
+      splits = (num_kb + kb_per - 1) / kb_per;
+    }
+  }
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0};
+  float* part = nullptr;
+  if (splits > 1) {
+    p.ld_part = (g.N + 3) / 4 * 4;
+    SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
+    p.part = part;
+  }
+  const int work = tiles * splits;
+  const int grid = work < num_sms ? work : num_sms;
   kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, p);
   SG_CUDA_TRY(cudaGetLastError());
+  if (splits > 1) {
+    const long long total = (long long)g.M * g.N;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
+    k_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(part, splits, g.M, g.N, p.ld_part, g.epi.out_f32,
+                                                      g.epi.ld_f32, g.epi.out_bf16, g.epi.ld_bf16);
+    SG_CUDA_TRY(cudaGetLastError());
+    SG_CUDA_TRY(cudaFreeAsync(part, st));
+  }
   return SG_OK;
 }
 

@@ -243,7 +243,7 @@ class ChainEngine:
         self.dH = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
         self.colsum = torch.zeros(((B + 31) // 32, _ld(dmax)), dtype=torch.float32, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
-        n_part = max(1, ((dmax + 31) // 32) * ((B + 255) // 256))
+        n_part = max(1, ((dmax + 31) // 32) * ((B + 31) // 32))
         self.loss_part = torch.zeros(n_part, dtype=torch.float64, device=dev)
         self.tape = Tape()
         self.grad_ready = None  # optional callback(layer_index) when layer l's gradients are written

@@ -132,7 +132,7 @@ def test_cuda_graph_replay_matches_eager_and_is_deterministic():
     def run(graph):
         chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(3)]).init_params(
             np.random.default_rng(1))
-        tr = Trainer(chain, B, loss="mse", lr=0.1, precision="bf16", graph=graph)
+        tr = Trainer(chain, B, loss="mse", lr=0.002, precision="bf16", graph=graph)
         losses = [float(tr.step(X, Y).item()) for _ in range(5)]
         return losses, tr.engine.P.clone()
 
