@@ -43,6 +43,16 @@ BYTES_PER_ELEM = 20                    # fwd 8 + grad 12
 METRIC = "fused-broadcast GB/s vs HBM peak"
 
 
+def traffic_of(kernel: str, applicable: bool):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not applicable or not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(kernel, {}).get("bytes")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -262,7 +272,8 @@ def broadcast_bench(args, world, rank, local, dist):
                        "grad_GBps": round(achieved, 1)},
         "roofline": {"bound": "hbm", "kernel": "sg_ew_grad (K2, incl. 2 partial-sum finalizers)",
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                     "frac": round(achieved / peaks["hbm_gbs"], 4),
+                     "traffic": traffic_of("sg_ew_grad", R * C == R_ROWS * C_COLS),
                      "peak_source": peaks["source"],
                      "step_frac": round(value / world / peaks["hbm_gbs"], 4)},
         "e2e": {"value": round(world * n * BYTES_PER_ELEM / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -393,7 +404,8 @@ def dense_c3_bench(args, dist, peaks):
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (fwd, dX, dW aggregated)",
                      "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": round(achieved / peaks["bf16_tflops"], 4), "peak_kind": "burst",
-                     "traffic": None},
+                     "traffic": traffic_of("gemm_bf16_fwd_c3", True),
+                     "traffic_algorithmic_bytes": 2 * (M * D + D * D) + 2 * M * D},
         "gpu_launches_per_step": 5,
         "l2": "working set ~544 MB per step > 126 MB L2",
     }
