@@ -165,19 +165,24 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
 }
 
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
+// 8 columns (one 32-byte sector) x 32 row groups per block: many blocks even
+// for narrow layers, each thread folds g = ty, ty+32, ... then a fixed fold over ty.
 __global__ void __launch_bounds__(256) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
                                                          float* out) {
-  __shared__ double red[8][33];
-  const long long j = blockIdx.x * 32ll + threadIdx.x;
+  __shared__ double red[32][9];
+  const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
+  const long long j = blockIdx.x * 8ll + tx;
   double acc = 0.0;
-  if (j < N)
-    for (long long g = threadIdx.y; g < G; g += 8) acc += (double)part[g * ldp + j];
-  red[threadIdx.y][threadIdx.x] = acc;
+  if (j < N) {
+#pragma unroll 4
+    for (long long g = ty; g < G; g += 32) acc += (double)part[g * ldp + j];
+  }
+  red[ty][tx] = acc;
   __syncthreads();
-  if (threadIdx.y == 0 && j < N) {
-    double s = red[0][threadIdx.x];
+  if (ty == 0 && j < N) {
+    double s = red[0][tx];
 #pragma unroll
-    for (int y = 1; y < 8; ++y) s += red[y][threadIdx.x];
+    for (int y = 1; y < 32; ++y) s += red[y][tx];
     out[j] = (float)s;
   }
 }
@@ -408,7 +413,7 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
   if (N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
-  dk::k_colsum_finalize<<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
+  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 256, 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
                                                                                              out);
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;

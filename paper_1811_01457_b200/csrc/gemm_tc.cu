@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -184,6 +185,60 @@ struct KParams {
   long long ld_part;
 };
 
+// One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
+// fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
+// `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
+__device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
+                                          bool grp_ok, int n0, int lane, int split) {
+  const GemmEpilogue& e = p.epi;
+  const bool full = n0 + 32 <= p.N;
+  const int nn = full ? 32 : p.N - n0;
+  if (p.splits > 1) {  // split-K: raw fp32 partial of this K range
+    if (row_ok) store_row_f32(p.part + ((long long)split * p.M + m) * p.ld_part + n0, v, nn);
+    return;
+  }
+  if (!row_ok) {
+    // rows past M contribute zeros to their group's column sums; groups
+    // entirely past M do not exist in the [ceil(M/32)][N] partial buffer
+    if (e.colsum && grp_ok) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+      warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
+    }
+    return;
+  }
+  if (e.mode == SG_EPI_BIAS_ACT) {
+    if (e.bias) {
+      float bv[32];
+      if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + i));
+          bv[i] = b4.x, bv[i + 1] = b4.y, bv[i + 2] = b4.z, bv[i + 3] = b4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += bv[i];
+    }
+    if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = act_fwd(v[i], e.act);
+  } else if (e.mode == SG_EPI_ACT_GRAD) {
+    float h[32];
+    load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(h[i], e.act);
+  }
+  if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, nn);
+  if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, nn);
+  // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
+  // transpose-reduce destroys v, so it runs after the stores
+  if (e.colsum) warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
+}
+
 template <int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -338,54 +393,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
-        const bool full = n0 + 32 <= p.N;
-        if (p.splits > 1) {  // split-K: raw fp32 partial of this K range
-          if (row_ok)
-            store_row_f32(p.part + ((long long)(t / out_tiles) * p.M + m) * p.ld_part + n0, v,
-                          full ? 32 : p.N - n0);
-          continue;
-        }
-        if (!row_ok) {
-          if (e.colsum) {  // rows past M contribute zeros to the column sums
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-            warp_colsum_store(v, e.colsum + (long long)((tc.m0 >> 5) + q) * e.ld_colsum + n0, lane,
-                              full ? 32 : p.N - n0);
-          }
-          continue;
-        }
-        if (e.mode == SG_EPI_BIAS_ACT) {
-          if (e.bias) {
-            float bv[32];
-            if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + i));
-                bv[i] = b4.x, bv[i + 1] = b4.y, bv[i + 2] = b4.z, bv[i + 3] = b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += bv[i];
-          }
-          if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, full ? 32 : p.N - n0);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = act_fwd(v[i], e.act);
-        } else if (e.mode == SG_EPI_ACT_GRAD) {
-          float h[32];
-          load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, full ? 32 : p.N - n0);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(h[i], e.act);
-        }
-        if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, full ? 32 : p.N - n0);
-        if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, full ? 32 : p.N - n0);
-        // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
-        // transpose-reduce destroys v, so it runs after the stores
-        if (e.colsum)
-          warp_colsum_store(v, e.colsum + (long long)((tc.m0 >> 5) + q) * e.ld_colsum + n0, lane,
-                            full ? 32 : p.N - n0);
+        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles);
       }
       tc_fence_before();
       __syncwarp();
@@ -401,6 +409,246 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ===================================================== 2-SM (CTA pair) variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile.
+// Each CTA stages 128 rows of A and 128 rows (half the N extent) of B per
+// k-block (32 KB, 6-deep ring); the leader CTA issues tcgen05.mma with
+// M = 256 and the tensor cores read both CTAs' shared memory; each CTA's
+// TMEM holds its 128 rows of the fp32 accumulator.  Half the smem operand
+// traffic per SM and 2/3 of the L2->SM bytes per FLOP of the 1-SM kernel.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on the barrier in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int STAGES, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                      const KParams p) {
+  constexpr int PM = 256, BN = 256, HALF = 128;
+  constexpr int A_BYTES = HALF * BK * 2;
+  constexpr int B_BYTES = HALF * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t IDESC = idesc_bf16(PM, BN, A_MN, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* acc_full = empty_bar + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m_tiles = (p.M + PM - 1) / PM;
+  const int n_tiles = (p.N + BN - 1) / BN;
+  const int out_tiles = m_tiles * n_tiles;
+  const int tiles = out_tiles * p.splits;
+  const int num_kb_total = (p.K + BK - 1) / BK;
+  const int pair = blockIdx.x / 2, pairs = gridDim.x / 2;
+  auto kb_range = [&](int t, int& kb0, int& kb1) {
+    const int s = t / out_tiles;
+    kb0 = s * p.kb_per_split;
+    kb1 = min(num_kb_total, kb0 + p.kb_per_split);
+  };
+  auto coord = [&](int t) {
+    constexpr int G = 8;  // grouped raster over 256-row pair tiles
+    const int u = t % out_tiles;
+    const int per_group = G * n_tiles;
+    const int group = u / per_group;
+    const int first_m = group * G;
+    const int gsize = min(m_tiles - first_m, G);
+    const int in_group = u - group * per_group;
+    TileCoord c;
+    c.m0 = (first_m + in_group % gsize) * PM;
+    c.n0 = (in_group / gsize) * BN;
+    return c;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 2 * EPI_WARPS);  // every epilogue warp of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote traffic
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += pairs) {
+        const TileCoord tc = coord(t);
+        const int am = tc.m0 + (int)rank * HALF, bn = tc.n0 + (int)rank * HALF;
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);  // leader's full barrier
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2d_pair(sa + j * 64 * BK * 2, &tma_a, fb, am + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(sa, &tma_a, fb, k0, am);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2d_pair(sb + j * 64 * BK * 2, &tma_b, fb, bn + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(sb, &tma_b, fb, k0, bn);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader only) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < tiles; t += pairs) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 64 * BK * 2, 1024) : sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 64 * BK * 2, 1024) : sdesc(sb + k * 32, 16, 1024);
+            tc_mma_pair(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
+          tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&acc_full[acc]);  // both CTAs' accumulator halves complete
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue (both CTAs, own 128 rows) =====================
+    const int ew = warp - EPI_WARP0;
+    const int q = ew % 4;
+    const int half = ew / 4;
+    constexpr int CH_PER = (BN / 32) / 2;
+    const uint32_t acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < tiles; t += pairs) {
+      const TileCoord tc = coord(t);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = tc.m0 + (int)rank * HALF + q * 32;
+      const int m = row0 + lane;
+      const bool row_ok = m < p.M;
+#pragma unroll 1
+      for (int c = half * CH_PER; c < (half + 1) * CH_PER; ++c) {
+        const int n0 = tc.n0 + c * 32;
+        float v[32];
+        tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
+        if (n0 >= p.N) continue;
+        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer may still be reading our smem / signalling our barriers
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                  : "memory");
   }
 }
@@ -515,6 +763,62 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   return SG_OK;
 }
 
+template <bool A_MN, bool B_MN>
+int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  constexpr int STAGES = 6;
+  constexpr int STAGE = 128 * tc::BK * 2 * 2;
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
+  CUtensorMap ma, mb;
+  int rc;
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, 128);
+  if (rc) return rc;
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128);
+  if (rc) return rc;
+  auto kern = tc::gemm_bf16_pair_kernel<STAGES, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_set = true;
+  }
+  const int pairs_avail = num_sms / 2;
+  const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const int num_kb = (g.K + tc::BK - 1) / tc::BK;
+  int splits = 1, kb_per = num_kb;
+  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && tiles * 2 <= pairs_avail && num_kb >= 8) {
+    int s = pairs_avail / tiles;
+    if (s > num_kb / 4) s = num_kb / 4;
+    if (s > 16) s = 16;
+    if (s >= 2) {
+      kb_per = (num_kb + s - 1) / s;
+      splits = (num_kb + kb_per - 1) / kb_per;
+    }
+  }
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0};
+  float* part = nullptr;
+  if (splits > 1) {
+    p.ld_part = (g.N + 3) / 4 * 4;
+    SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
+    p.part = part;
+  }
+  const int work = tiles * splits;
+  const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, p);
+  SG_CUDA_TRY(cudaGetLastError());
+  if (splits > 1) {
+    const long long total = (long long)g.M * g.N;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
+    k_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(part, splits, g.M, g.N, p.ld_part, g.epi.out_f32,
+                                                      g.epi.ld_f32, g.epi.out_bf16, g.epi.ld_bf16);
+    SG_CUDA_TRY(cudaGetLastError());
+    SG_CUDA_TRY(cudaFreeAsync(part, st));
+  }
+  return SG_OK;
+}
+
 template <int BN>
 int run_bn(const GemmArgs& g, int num_sms, cudaStream_t st) {
   if (!g.a_mn && !g.b_mn) return run<BN, false, false>(g, num_sms, st);
@@ -534,6 +838,16 @@ int launch_gemm_bf16(const GemmArgs& g, int num_sms, cudaStream_t st) {
     return fail(SG_EINVAL, "gemm: leading dimension smaller than the row");
   if (g.N <= 64) return run_bn<64>(g, num_sms, st);
   if (g.N <= 128) return run_bn<128>(g, num_sms, st);
+  static const bool pair_ok = [] {
+    const char* e = std::getenv("SGB200_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (pair_ok && g.M >= 256 && num_sms >= 2) {
+    if (!g.a_mn && !g.b_mn) return run_pair<false, false>(g, num_sms, st);
+    if (!g.a_mn && g.b_mn) return run_pair<false, true>(g, num_sms, st);
+    if (g.a_mn && g.b_mn) return run_pair<true, true>(g, num_sms, st);
+    return run_pair<true, false>(g, num_sms, st);
+  }
   return run_bn<256>(g, num_sms, st);
 }
 
