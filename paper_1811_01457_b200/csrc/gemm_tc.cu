@@ -164,6 +164,33 @@ __device__ __forceinline__ float act_grad_from_out(float h, int act) {
   }
 }
 
+// The activation is uniform per launch: branch once per 32-element chunk,
+// not per element (a per-element switch compiles to an indirect branch).
+__device__ __forceinline__ void act_fwd_chunk(float (&v)[32], int act) {
+  if (act == SG_ACT_SIGMOID) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __fdividef(1.0f, 1.0f + __expf(-v[i]));
+  } else if (act == SG_ACT_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+  } else if (act == SG_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
+  }
+}
+__device__ __forceinline__ void act_grad_chunk(float (&v)[32], const float (&h)[32], int act) {
+  if (act == SG_ACT_SIGMOID) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= h[i] * (1.0f - h[i]);
+  } else if (act == SG_ACT_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= 1.0f - h[i] * h[i];
+  } else if (act == SG_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = h[i] > 0.0f ? v[i] : 0.0f * v[i];
+  }
+}
+
 struct TileCoord {
   int m0, n0;
 };
@@ -229,13 +256,11 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       for (int i = 0; i < 32; ++i) v[i] += bv[i];
     }
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = act_fwd(v[i], e.act);
+    act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
     float h[32];
     load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(h[i], e.act);
+    act_grad_chunk(v, h, e.act);
   }
   if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, nn);
   if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, nn);
