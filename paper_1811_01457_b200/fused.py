@@ -186,7 +186,9 @@ def _raise_eval(lo: Lowered, ctx: int, stream: int) -> None:
     if st != rt.SG_EDOMAIN:
         rt.check(st, "sg_ew_check")
     s = lo.sites[site.value - 1]
-    raise EvalError(s.function, s.block, s.index, s.message)
+    err = EvalError(s.function, s.block, s.index, s.message)
+    err.element = int(elem.value)  # flat index of the first failing element
+    raise err
 
 
 def check_errors(module, name: str, stream=None) -> None:

@@ -152,7 +152,9 @@ class _Reader:
 
     def operands(self) -> list[str]:
         ops = []
-        while self.peek()[1] == "%":
+        # `%x` followed by `=` starts the next instruction (zero-operand ops
+        # like tape_new are followed directly by the next result name)
+        while self.peek()[1] == "%" and self.peek(2)[1] != "=":
             ops.append(self.name("%"))
             if not self.maybe(","):
                 break

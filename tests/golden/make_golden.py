@@ -37,6 +37,7 @@ from ssagrad.structure import SEmitter, flatten  # noqa: E402
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 from fused_src import FUSED_SRC  # noqa: E402
+sys.path.insert(0, HERE)
 
 
 def f32(x):
@@ -207,9 +208,82 @@ def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot"):
     return out
 
 
+# ----------------------------------------------- augmented IR (GpuMachine)
+def machine_cases():
+    """Augmented forward/pullback pairs printed by the reference, with inputs
+    and the reference's own cotangents, so the GPU machine can run the same
+    IR on a box without the reference."""
+    from ssagrad import augment, print_ir, generate_suite
+    from ssagrad.nn_train import (DANConfig, _batch_tensors, _weight_args, build_loss_ir,
+                                  dan_step, init_params, make_synthetic)
+    from conftest_ref import ANALYTIC_SRC
+
+    out = {}
+    # analytic: tensor matmul/tanh/reduce (@net) and fused_map through a pack (@mapped)
+    m = parse_ir(ANALYTIC_SRC)
+    for name in ("net", "mapped", "cube", "absval", "callin"):
+        augment(m, name)
+    w = DenseTensor(f32([[0.3, -0.5, 0.8], [1.1, 0.2, -0.4]]))
+    v = DenseTensor(f32([[0.5], [-1.2], [0.9]]))
+    x = DenseTensor(f32([0.2, -0.9, 1.4, 0.05]))
+    cases = {"net": (w, v), "mapped": (x, 0.7), "cube": (1.3,), "absval": (-2.5,), "callin": (1.3,)}
+    analytic = {"ir": print_ir(m), "cases": []}
+    for name, args in cases.items():
+        fn = m.get(name)
+        g = grad(m, name, args)
+        analytic["cases"].append({"fn": name, "args": [enc(a) for a in args],
+                                  "grads": [enc(g[pv]) for pv, ty in fn.params if ty.is_differentiable]})
+    out["analytic"] = analytic
+
+    # generated programs with branches/loops over tensors (test corpus seed)
+    gm = Module()
+    suite = generate_suite(gm, random.Random(20260822), 40, inputs_per=2)
+    picked = []
+    for name, inputs in suite:
+        fn = gm.get(name)
+        if any(ty.is_tensor for _, ty in fn.params) and len(picked) < 8:
+            picked.append((name, inputs))
+    corpus = {"cases": []}
+    for name, inputs in picked:
+        augment(gm, name)
+        fn = gm.get(name)
+        for args in inputs:
+            g = grad(gm, name, args)
+            corpus["cases"].append({"fn": name, "args": [enc(a) if not isinstance(a, int) else {"i64": a}
+                                                         for a in args],
+                                    "grads": [enc(g[pv]) for pv, ty in fn.params if ty.is_differentiable]})
+    corpus["ir"] = print_ir(gm)
+    out["corpus"] = corpus
+
+    # the DAN two-head step (nn_train.py:337-375) at the test-suite SMALL config
+    cfg = DANConfig(dim=6, trunk_sizes=(6, 4), head_sizes=(4, 1), n_samples=48, batch_size=8, epochs=2)
+    sizes = (cfg.trunk_sizes, cfg.head_sizes, cfg.head_sizes)
+    dm = Module()
+    loss_fn = build_loss_ir(dm, sizes, cfg.batch_size)
+    augment(dm, loss_fn.name)
+    params = init_params(sizes, random.Random(2))
+    batch = make_synthetic(cfg)[:cfg.batch_size]
+    X, Yc, Yd = _batch_tensors(batch)
+    args = _weight_args(params) + (X, Yc, Yd, cfg.lam)
+    g_c = grad(dm, loss_fn.name, args, (1.0, 0.0))
+    g_d = grad(dm, loss_fn.name, args, (0.0, 1.0))
+    new, losses = dan_step(dm, params, batch, cfg)
+    out["dan"] = {
+        "ir": print_ir(dm), "fn": loss_fn.name, "lr": cfg.lr, "lam": cfg.lam,
+        "args": [enc(a) for a in args],
+        "g_c": [enc(g_c[pv]) for pv, ty in loss_fn.params if ty.is_differentiable],
+        "g_d": [enc(g_d[pv]) for pv, ty in loss_fn.params if ty.is_differentiable],
+        "new_params": [enc(t) for l in new.layers() for t in (l.W, l.b)],
+        "losses": [losses["c_loss"], losses["d_loss"]],
+    }
+    return out
+
+
 def main():
     with open(os.path.join(HERE, "fused.json"), "w") as f:
         json.dump(fused_cases(), f, indent=0)
+    with open(os.path.join(HERE, "machine.json"), "w") as f:
+        json.dump(machine_cases(), f, indent=0)
     np.savez_compressed(os.path.join(HERE, "tensor.npz"), **tensor_cases())
     np.savez_compressed(os.path.join(HERE, "mlp_c1_b32.npz"),
                         **chain_case((784, 32, 10), ("sigmoid", "identity"), 32, "softmax_xent", 1))
