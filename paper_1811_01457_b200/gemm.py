@@ -56,6 +56,8 @@ def _ptr(t):
 def _ld(t):
     if t is None:
         return 0
+    if t.dim() == 2 and t.is_contiguous():  # also covers size-1 dims with arbitrary strides
+        return t.shape[1]
     if t.dim() != 2 or t.stride(1) != 1:
         raise ValueError("gemm operands must be 2-D with unit column stride")
     return t.stride(0)
