@@ -472,6 +472,45 @@ def secondary_benches(args, world, rank, dist):
     return out
 
 
+def cpu_baseline_mlp(name, sizes, acts, batch, loss, mode, rows=None):
+    """Oracle port of the reference's Dense step (fwd + loss + pullback + SGD) on the host.
+
+    mode "exact": the reference's own matmul order (ascending-k, C restatement,
+    1 core); mode "blas": numpy/OpenBLAS fp64 restatement (all cores), on a
+    row slice of `rows` samples when the full batch would take too long.
+    """
+    import math as _m
+
+    from oracle import dense as OD
+
+    rng = np.random.default_rng(0)
+    n = rows or batch
+    params = []
+    for i in range(len(acts)):
+        r = _m.sqrt(6.0 / (sizes[i] + sizes[i + 1]))
+        params.append((rng.uniform(-r, r, (sizes[i + 1], sizes[i])), np.zeros(sizes[i + 1])))
+    X = rng.uniform(0, 1, (n, sizes[0]))
+    if loss == "softmax_xent":
+        Y = np.zeros((n, sizes[-1]))
+        Y[np.arange(n), rng.integers(0, sizes[-1], n)] = 1.0
+    else:
+        Y = rng.uniform(-1, 1, (n, sizes[-1]))
+    OD.mlp_step(params, X, Y, acts, loss, mode=mode)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        OD.mlp_step(params, X, Y, acts, loss, mode=mode)
+        reps += 1
+        if time.perf_counter() - t0 > 2.0:
+            break
+    sec = (time.perf_counter() - t0) / reps
+    return {"workload": name, "value": round(n / sec, 2), "unit": "samples/s",
+            "kind": "port", "mode": mode,
+            "cores": 1 if mode == "exact" else len(os.sched_getaffinity(0)),
+            "sample": f"{n} rows of the {batch}-row batch" if rows else f"full batch {batch}",
+            "s_per_step_sample": round(sec, 4)}
+
+
 def reference_arm(args, world, rank):
     if rank != 0:
         return None
@@ -498,6 +537,12 @@ def reference_arm(args, world, rank):
         "config": {"workload": "c2 fused broadcast sigma.(a.*x.+b) + gradient (bounded CPU sample)"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "secondary": [
+            cpu_baseline_mlp("c1 MLP 784-32-10 train step (reference matmul order)", (784, 32, 10),
+                             ("sigmoid", "identity"), 128, "softmax_xent", "exact"),
+            cpu_baseline_mlp("c4 MLP 4x4096 train step (numpy-BLAS fp64, row slice)", (4096,) * 5,
+                             ("tanh",) * 3 + ("identity",), 65536, "mse", "blas", rows=256),
+        ],
         "wall_s": round(time.perf_counter() - t0, 1),
     }
 
@@ -531,6 +576,8 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             rec["cpu_baseline"] = cpu_baseline_broadcast(rows=args.ref_rows)
+            rec["cpu_baseline"]["secondary"] = [
+                cpu_baseline_mlp("c1", (784, 32, 10), ("sigmoid", "identity"), 128, "softmax_xent", "exact")]
         print(json.dumps(rec), flush=True)
     if dist is not None:
         dist.barrier()

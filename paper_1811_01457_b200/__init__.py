@@ -12,14 +12,19 @@ Kernels are hand-written CUDA for sm_100a behind the C ABI in
 ``include/sgb200.h`` (``_lib/libsgb200.so``); there is no CPU fallback.
 """
 
+from .dense import Chain, ChainEngine, Dense, DenseLayer
 from .fused import (DEFAULT_STEP_LIMIT, EvalError, check_errors, fused_map, fused_map_grad,
                     fused_map_pullback, fused_map_with_partials, set_step_limit)
+from .gpu_machine import GpuMachine, eval_function, grad
+from .tape import Tape
+from .train import DataParallel, Trainer
 from .ir import BOOL, F64, I64, Module, Type, tensor_type
 from .irtext import parse_ir
 from .runtime import DomainError, RuntimeUnavailable
 
 __all__ = [
-    "BOOL", "DEFAULT_STEP_LIMIT", "DomainError", "EvalError", "F64", "I64", "Module",
-    "RuntimeUnavailable", "Type", "check_errors", "fused_map", "fused_map_grad",
-    "fused_map_pullback", "fused_map_with_partials", "parse_ir", "set_step_limit", "tensor_type",
+    "BOOL", "Chain", "ChainEngine", "DEFAULT_STEP_LIMIT", "DataParallel", "Dense", "DenseLayer",
+    "DomainError", "EvalError", "F64", "GpuMachine", "I64", "Module", "RuntimeUnavailable", "Tape",
+    "Trainer", "Type", "check_errors", "eval_function", "fused_map", "fused_map_grad",
+    "fused_map_pullback", "fused_map_with_partials", "grad", "parse_ir", "set_step_limit", "tensor_type",
 ]
