@@ -281,8 +281,16 @@ struct Launch {
   long long rpb;
 };
 
+long long env_ll(const char* name, long long dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoll(e) : dflt;
+}
+
+// Resident blocks per SM the grid is sized for.  Tuned on B200 (tools/ew_sweep.sh):
+// the forward kernel streams best with fewer, longer-lived blocks; the gradient
+// kernel (64-register budget, SG_GRAD_MINB 4) with 8.
 Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* args, int k,
-            const void* const* extra_ptrs, int n_extra) {
+            const void* const* extra_ptrs, int n_extra, long long per_sm = 8) {
   Launch L;
   const int esz = dtype == SG_F64 ? 8 : 4;
   int vec = 16 / esz;
@@ -302,7 +310,7 @@ Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* arg
   L.bdy = 256 / bdx;
   long long gx = (cv + bdx - 1) / bdx;
   L.gx = (unsigned)gx;
-  long long target = (long long)ctx->num_sms * 8;
+  long long target = (long long)ctx->num_sms * per_sm;
   long long gy = std::max<long long>(1, std::min<long long>((s.R + L.bdy - 1) / L.bdy,
                                                              (target + gx - 1) / gx));
   gy = std::min<long long>(gy, 65535);
@@ -330,6 +338,8 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   bool has_col = false;
   for (int i = 0; i < k; ++i) has_col |= kinds[i] == SG_COL;
   src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n";
+  // tuning overrides, e.g. SGB200_EW_DEFINES="#define SG_UNROLL 8"
+  if (const char* extra = std::getenv("SGB200_EW_DEFINES")) src << extra << "\n";
   src << "#define SG_KINDS {";
   for (int i = 0; i < std::max(1, k); ++i) src << (i ? "," : "") << (i < k ? kinds[i] : 0);
   src << "}\n";
@@ -559,7 +569,7 @@ int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg
   Shape2D s;
   canonicalise(k, args, out, s);
   const void* extra[] = {y->ptr};
-  Launch L = plan(ctx, s, kern->dtype, args, k, extra, 1);
+  Launch L = plan(ctx, s, kern->dtype, args, k, extra, 1, env_ll("SGB200_EW_FWD_BLOCKS_PER_SM", 4));
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -607,7 +617,8 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   canonicalise(k, args, out, s);
   std::vector<const void*> extra = {ybar->ptr, y ? y->ptr : nullptr};
   for (int i = 0; i < k; ++i) extra.push_back(s.kinds[i] == SG_FULL ? argbars[i].ptr : nullptr);
-  Launch L = plan(ctx, s, kern->dtype, args, k, extra.data(), (int)extra.size());
+  Launch L = plan(ctx, s, kern->dtype, args, k, extra.data(), (int)extra.size(),
+                  env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", 8));
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;

@@ -28,7 +28,7 @@
 #define SG_GUNROLL 2  // rows in flight per thread, gradient (register budget)
 #endif
 #ifndef SG_GRAD_MINB
-#define SG_GRAD_MINB 3
+#define SG_GRAD_MINB 4
 #endif
 
 struct D { T p; T t[SG_KT]; };
