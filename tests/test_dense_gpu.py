@@ -144,6 +144,43 @@ def test_cuda_graph_replay_matches_eager_and_is_deterministic():
     assert l1[-1] < l1[0]  # it trains
 
 
+def test_data_parallel_trainer_over_nccl_world1():
+    """The DP code path (NCCL process group, bucketed async all-reduce issued
+    from inside the pullback, broadcast of initial params) on the one GPU a
+    box has: with world size 1 it must reproduce the single-GPU step."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(5)
+        sizes, acts = (256, 512, 128), ("tanh", "identity")
+        B = 1024
+        X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+        Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+
+        def run(dp):
+            chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(2)]).init_params(
+                np.random.default_rng(9))
+            tr = Trainer(chain, B, loss="mse", lr=0.002, precision="bf16", dp=dp)
+            losses = [float(tr.step(X, Y).item()) for _ in range(3)]
+            return losses, tr.engine.P.clone()
+
+        l0, p0 = run(False)
+        l1, p1 = run(True)
+        assert l0 == l1
+        assert torch.equal(p0, p1)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_data_parallel_shards_sum_to_full_gradient():
     """Single-GPU check of the DP math: shard gradients scaled by the global
     1/B sum to the full-batch gradient (the all-reduce itself is covered by
