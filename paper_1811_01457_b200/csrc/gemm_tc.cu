@@ -215,13 +215,68 @@ struct KParams {
   int kb_per_split;   // k-blocks per split
   float* part;        // [splits][M][ld_part] when splits > 1
   long long ld_part;
+  int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
 };
+
+// ----------------------------------------------------- TMA-store epilogue
+// Each epilogue warp owns a 4 KB, 1024-byte aligned staging slot.  A 32x32
+// chunk is written row-per-lane in the TMA swizzled layout (conflict-free
+// 16-byte stores) and one lane issues a bulk tensor store, so the global
+// writes are fully coalesced and asynchronous.
+constexpr int STAGE_SLOT = 4096;
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// bf16 rows are 64 B: SWIZZLE_64B puts 16-byte chunk c of row r at c ^ ((r >> 1) & 3)
+__device__ __forceinline__ void stage_bf16(uint8_t* slot, const float (&v)[32], int lane) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * c + 2 * j], v[8 * c + 2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(slot + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+// fp32 rows are 128 B: SWIZZLE_128B puts chunk c of row r at c ^ (r & 7)
+__device__ __forceinline__ void stage_f32(uint8_t* slot, const float (&v)[32], int lane) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(slot + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+// warp-collective: stage one chunk and bulk-store it at (n0, row0)
+template <bool BF16>
+__device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap* map, const float (&v)[32], int lane,
+                                               int n0, int row0) {
+  if (lane == 0) bulk_wait_read0();  // the slot's previous store has been read out
+  __syncwarp();
+  if (BF16) stage_bf16(slot, v, lane);
+  else stage_f32(slot, v, lane);
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map, slot, n0, row0);
+    bulk_commit();
+  }
+}
 
 // One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
-                                          bool grp_ok, int n0, int lane, int split) {
+                                          bool grp_ok, int n0, int lane, int split, uint8_t* slot,
+                                          const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
   const int nn = full ? 32 : p.N - n0;
@@ -229,17 +284,12 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     if (row_ok) store_row_f32(p.part + ((long long)split * p.M + m) * p.ld_part + n0, v, nn);
     return;
   }
+  if (!grp_ok) return;  // the whole 32-row group is past M (warp-uniform)
   if (!row_ok) {
-    // rows past M contribute zeros to their group's column sums; groups
-    // entirely past M do not exist in the [ceil(M/32)][N] partial buffer
-    if (e.colsum && grp_ok) {
+    // rows past M: zeros for the column sums; TMA clips them on store
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-      warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
-    }
-    return;
-  }
-  if (e.mode == SG_EPI_BIAS_ACT) {
+    for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+  } else if (e.mode == SG_EPI_BIAS_ACT) {
     if (e.bias) {
       float bv[32];
       if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
@@ -262,8 +312,15 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
     act_grad_chunk(v, h, e.act);
   }
-  if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, nn);
-  if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, nn);
+  const int row0 = m - lane;
+  if (e.out_f32) {
+    if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0);
+    else if (row_ok) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, nn);
+  }
+  if (e.out_bf16) {
+    if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0);
+    else if (row_ok) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, nn);
+  }
   // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
   // transpose-reduce destroys v, so it runs after the stores
   if (e.colsum) warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
@@ -272,6 +329,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
 template <int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
                  const KParams p) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
@@ -287,6 +345,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
   uint64_t* acc_full = empty_bar + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint8_t* stage_slots = smem + STAGES * STAGE_BYTES + 1024;  // 8 x 4 KB epilogue staging
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -423,7 +482,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
-        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles);
+        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles,
+                  stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -434,6 +494,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
       }
     }
   }
+  if (warp >= EPI_WARP0 && lane == 0) bulk_wait0();  // staged stores drained before smem goes away
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -496,6 +557,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
 template <int STAGES, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                      const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
                       const KParams p) {
   constexpr int PM = 256, BN = 256, HALF = 128;
   constexpr int A_BYTES = HALF * BK * 2;
@@ -511,6 +573,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_co
   uint64_t* acc_full = empty_bar + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint8_t* stage_slots = smem + STAGES * STAGE_BYTES + 1024;  // 8 x 4 KB epilogue staging
 
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -664,7 +727,8 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_co
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;
-        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles);
+        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles,
+                  stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -675,6 +739,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_co
       }
     }
   }
+  if (warp >= EPI_WARP0 && lane == 0) bulk_wait0();  // staged stores drained before smem goes away
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // the peer may still be reading our smem / signalling our barriers
@@ -724,6 +789,38 @@ int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer
   return SG_OK;
 }
 
+// Output maps for the TMA-store epilogue: box 32 x 32, swizzle matching
+// stage_bf16 (64B) / stage_f32 (128B).  Returns false when the buffer does
+// not meet TMA's alignment rules (the epilogue then stores directly).
+bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, long long M, long long ld) {
+  const long long esz = bf16 ? 2 : 4;
+  if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || M <= 0 || N <= 0) return false;
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& mf32) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("SGB200_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  std::memset(&mlp, 0, sizeof mlp);
+  std::memset(&mf32, 0, sizeof mf32);
+  p.tma_lp = p.tma_f32 = 0;
+  if (!enabled || p.splits > 1) return;
+  if (g.epi.out_bf16) p.tma_lp = make_out_map(&mlp, g.epi.out_bf16, true, g.N, g.M, g.epi.ld_bf16);
+  if (g.epi.out_f32) p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32);
+}
+
 // split-K finalize: out = sum_s part[s] in ascending s (deterministic)
 __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
                                 long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
@@ -742,7 +839,8 @@ template <int BN, bool A_MN, bool B_MN>
 int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   constexpr int STAGE = tc::BM * tc::BK * 2 + BN * tc::BK * 2;
   constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::STAGE_SLOT;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
@@ -772,7 +870,9 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0};
+  CUtensorMap mlp, mf32;
+  out_maps(g, p, mlp, mf32);
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
@@ -781,7 +881,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, p);
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     const long long total = (long long)g.M * g.N;
@@ -799,7 +899,8 @@ template <bool A_MN, bool B_MN>
 int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   constexpr int STAGES = 6;
   constexpr int STAGE = 128 * tc::BK * 2 * 2;
-  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::STAGE_SLOT;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
@@ -828,7 +929,9 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0};
+  CUtensorMap mlp, mf32;
+  out_maps(g, p, mlp, mf32);
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
@@ -837,7 +940,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, p);
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     const long long total = (long long)g.M * g.N;
