@@ -115,6 +115,33 @@ def fused_cases():
     return {"cases": cases, "grad_mapped": grads, "errors": errors}
 
 
+def fuzz_cases(n_programs=60, width=16):
+    """Random scalar sub-functions fused over vectors, reference partials."""
+    from ssagrad import print_ir
+    from ssagrad.progen import random_program
+
+    rng = random.Random(7)
+    m = Module()
+    out = []
+    k = 0
+    while len(out) < n_programs and k < 10 * n_programs:
+        name = f"fz{k}"
+        k += 1
+        fn = random_program(m, rng, name, scalar_only=True)
+        if any(ty.kind != "f64" for _, ty in fn.params):
+            continue
+        args = tuple(DenseTensor(f32([rng.uniform(-2, 2) for _ in range(width)])) for _ in fn.params)
+        try:
+            primal, parts = fused_map_with_partials(m, name, args)
+        except (EvalError, OverflowError, ZeroDivisionError):
+            continue
+        if not all(np.isfinite(p.data).all() for p in [primal] + list(parts)):
+            continue
+        out.append({"fn": name, "args": [enc(a) for a in args], "primal": enc(primal),
+                    "partials": [enc(p) for p in parts]})
+    return {"ir": print_ir(m), "cases": out}
+
+
 # ----------------------------------------------------------------- tensor
 def tensor_cases():
     rng = np.random.default_rng(5)
@@ -284,6 +311,8 @@ def main():
         json.dump(fused_cases(), f, indent=0)
     with open(os.path.join(HERE, "machine.json"), "w") as f:
         json.dump(machine_cases(), f, indent=0)
+    with open(os.path.join(HERE, "fuzz.json"), "w") as f:
+        json.dump(fuzz_cases(), f, indent=0)
     np.savez_compressed(os.path.join(HERE, "tensor.npz"), **tensor_cases())
     np.savez_compressed(os.path.join(HERE, "mlp_c1_b32.npz"),
                         **chain_case((784, 32, 10), ("sigmoid", "identity"), 32, "softmax_xent", 1))

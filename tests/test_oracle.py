@@ -116,3 +116,21 @@ def test_dense_backward_matches_reference_seed():
     assert max_rel(dx, z["dX"]) <= 1e-15
     assert max_rel(dW, z["dW0"]) <= 1e-15
     assert max_rel(db, z["db0"]) <= 1e-15
+
+
+def test_oracle_reproduces_fuzz_corpus_exactly():
+    import json
+    import os
+
+    from conftest import GOLDEN
+    from paper_1811_01457_b200.irtext import parse_ir
+
+    with open(os.path.join(GOLDEN, "fuzz.json")) as f:
+        d = json.load(f)
+    m = parse_ir(d["ir"])
+    for case in d["cases"][:20]:
+        args = [decode(a) for a in case["args"]]
+        primal, parts = OS.fused_map_with_partials(m, case["fn"], args)
+        assert np.array_equal(primal, decode(case["primal"])), case["fn"]
+        for p, g in zip(parts, case["partials"]):
+            assert np.array_equal(p, decode(g)), case["fn"]
