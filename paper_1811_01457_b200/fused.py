@@ -306,6 +306,24 @@ def fused_map_grad(module, name: str, args, ybar, *, want_primal: bool = False,
     return y, tuple(outs)
 
 
+def reduce_to(x, shape, *, out=None, stream=None):
+    """``tensor.reduce_to`` (tensor.py:327-345) on the device: sum the
+    broadcast-expanded axes of ``x`` down to ``shape`` (``()`` -> float)."""
+    import torch
+
+    xd = _as_device(x)
+    shape = tuple(shape)
+    if out is None:
+        out = torch.empty(shape or (1,), dtype=xd.dtype, device="cuda")
+    od = rt.tensor_desc(out)
+    if not shape:
+        od.ndim = 0
+    ad = rt.tensor_desc(xd)
+    rt.check(rt.load_library().sg_reduce_to(rt.context(), ctypes.byref(ad), None, ctypes.byref(od),
+                                            rt.stream_ptr(stream)), "reduce_to")
+    return float(out.item()) if not shape else out
+
+
 def fused_map_pullback(partials, arg_types, ybar):
     """``reduce_like(ybar * partial_i, type_i)`` -- reference forward_ad.py:226-235."""
     import torch
