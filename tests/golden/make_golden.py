@@ -306,6 +306,37 @@ def machine_cases():
     return out
 
 
+def dan_train_case():
+    """Everything the reference's DAN `train` (nn_train.py:418-450) needs,
+    frozen: augmented loss IR (batch 32), eval IR (n = 320), the synthetic
+    data and initial parameters, and the reference's own epoch records for
+    lam = 0 and lam = 1 (the acceptance criterion 7 configuration)."""
+    from dataclasses import replace
+
+    from ssagrad import augment, print_ir, train
+    from ssagrad.nn_train import DANConfig, build_eval_ir, build_loss_ir, init_params, make_synthetic
+
+    cfg = DANConfig()
+    sizes = (cfg.trunk_sizes, cfg.head_sizes, cfg.head_sizes)
+    m = Module()
+    loss_fn = build_loss_ir(m, sizes, cfg.batch_size)
+    augment(m, loss_fn.name)
+    data = make_synthetic(cfg)
+    eval_fn = build_eval_ir(m, sizes, len(data))
+    params = init_params(sizes, random.Random(cfg.seed + 1))
+    hist = {}
+    for lam in (0.0, 1.0):
+        hist[str(lam)] = train(replace(cfg, lam=lam)).records
+    return {
+        "ir": print_ir(m), "loss_fn": loss_fn.name, "eval_fn": eval_fn.name,
+        "cfg": {"lr": cfg.lr, "epochs": cfg.epochs, "batch_size": cfg.batch_size, "seed": cfg.seed},
+        "X": [s.x.flat() for s in data], "yc": [s.y_c for s in data], "yd": [s.y_d for s in data],
+        "params": [enc(t) for l in params.layers() for t in (l.W, l.b)],
+        "n_trunk": len(params.trunk), "n_head": len(params.class_head),
+        "history": hist,
+    }
+
+
 def main():
     with open(os.path.join(HERE, "fused.json"), "w") as f:
         json.dump(fused_cases(), f, indent=0)
@@ -313,6 +344,8 @@ def main():
         json.dump(machine_cases(), f, indent=0)
     with open(os.path.join(HERE, "fuzz.json"), "w") as f:
         json.dump(fuzz_cases(), f, indent=0)
+    with open(os.path.join(HERE, "dan_train.json"), "w") as f:
+        json.dump(dan_train_case(), f)
     np.savez_compressed(os.path.join(HERE, "tensor.npz"), **tensor_cases())
     np.savez_compressed(os.path.join(HERE, "mlp_c1_b32.npz"),
                         **chain_case((784, 32, 10), ("sigmoid", "identity"), 32, "softmax_xent", 1))

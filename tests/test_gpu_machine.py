@@ -123,3 +123,55 @@ func @f(%x: tensor<4xf64>) -> f64 {
     assert e.message == f"log of non-positive value {0.5 - 1.0!r}"
     s = eval_function(m, "f", (np.array([2.0, 3.0, 4.0, 5.0]),))[0]
     assert abs(s - float(np.sum(np.log(np.array([1.0, 2.0, 3.0, 4.0]))))) <= 1e-14
+
+
+def _probe_acc(H, yd, alpha=0.1):
+    """Host restatement of nn_train._domain_probe_acc (nn_train.py:378-393):
+    test-side evaluation only (the probe is not on the accelerated path)."""
+    X = np.column_stack([H, np.ones(H.shape[0])])
+    t = np.array([1.0 if y == 1 else -1.0 for y in yd])
+    acc = 0.0
+    for tr, te in ((slice(0, None, 2), slice(1, None, 2)), (slice(1, None, 2), slice(0, None, 2))):
+        gram = X[tr].T @ X[tr] + alpha * np.eye(X.shape[1])
+        w = np.linalg.solve(gram, X[tr].T @ t[tr])
+        acc += float(np.mean((X[te] @ w >= 0.0) == (t[te] > 0.0)))
+    return acc / 2.0
+
+
+@gpu
+@pytest.mark.parametrize("lam", ["0.0", "1.0"])
+def test_dan_training_reproduces_frozen_history(lam):
+    """Acceptance criterion 7 (test_acceptance.py:293-322): the reference's
+    50-epoch DAN trainings, every epoch record, reproduced on the GPU."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1811_01457_b200.dan import train_epochs
+    from paper_1811_01457_b200.gpu_machine import GpuMachine
+
+    with open(os.path.join(GOLDEN, "dan_train.json")) as f:
+        d = json.load(f)
+    m = parse_ir(d["ir"])
+    cfg = d["cfg"]
+    X = np.array(d["X"])
+    yc, yd = np.array(d["yc"], dtype=np.float64), np.array(d["yd"], dtype=np.float64)
+    params = [torch.tensor(decode(p), dtype=torch.float64, device="cuda") for p in d["params"]]
+    ref = d["history"][lam]
+    got = []
+
+    def on_epoch(epoch, ps, c_mean, d_mean):
+        yc_hat, yd_hat, H = GpuMachine(m).call(d["eval_fn"], tuple(ps) + (X,))
+        yc_hat, H = yc_hat.cpu().numpy(), H.cpu().numpy()
+        got.append({"epoch": epoch, "c_loss": c_mean, "d_loss": d_mean,
+                    "class_acc": float(np.mean((yc_hat >= 0.5) == (yc == 1))),
+                    "domain_probe_acc": _probe_acc(H, [int(v) for v in yd])})
+
+    train_epochs(m, d["loss_fn"], params, X, yc, yd, lam=float(lam), lr=cfg["lr"],
+                 epochs=cfg["epochs"], batch_size=cfg["batch_size"], seed=cfg["seed"], on_epoch=on_epoch)
+    assert len(got) == len(ref)
+    worst = 0.0
+    for g, r in zip(got, ref):
+        worst = max(worst, abs(g["c_loss"] - r["c_loss"]), abs(g["d_loss"] - r["d_loss"]))
+        assert g["class_acc"] == r["class_acc"], g
+        assert g["domain_probe_acc"] == r["domain_probe_acc"], g
+    assert worst <= 1e-9, worst
