@@ -167,24 +167,24 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
 // 8 columns (one 32-byte sector) x 32 row groups per block: many blocks even
 // for narrow layers, each thread folds g = ty, ty+32, ... then a fixed fold over ty.
-__global__ void __launch_bounds__(256) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
-                                                         float* out) {
-  __shared__ double red[32][9];
+__global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
+                                                          float* out) {
+  constexpr int RG = 128;  // row groups per block (1024 threads = 8 columns x 128)
+  __shared__ double red[RG][9];
   const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
   const long long j = blockIdx.x * 8ll + tx;
   double acc = 0.0;
   if (j < N) {
 #pragma unroll 4
-    for (long long g = ty; g < G; g += 32) acc += (double)part[g * ldp + j];
+    for (long long g = ty; g < G; g += RG) acc += (double)part[g * ldp + j];
   }
   red[ty][tx] = acc;
   __syncthreads();
-  if (ty == 0 && j < N) {
-    double s = red[0][tx];
-#pragma unroll
-    for (int y = 1; y < 32; ++y) s += red[y][tx];
-    out[j] = (float)s;
+  for (int s = RG / 2; s > 0; s >>= 1) {  // fixed-order tree over the row groups
+    if (ty < s) red[ty][tx] += red[ty + s][tx];
+    __syncthreads();
   }
+  if (ty == 0 && j < N) out[j] = (float)red[0][tx];
 }
 
 // --- reduce_to over rows in the reference's order: sequential ascending fold
@@ -413,7 +413,7 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
   if (N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
-  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 256, 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
+  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 1024, 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
                                                                                              out);
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;

@@ -822,17 +822,45 @@ void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& 
 }
 
 // split-K finalize: out = sum_s part[s] in ascending s (deterministic)
+// blockIdx.y = row, threads over 4-column groups (no 64-bit divides, float4 loads)
 __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
                                 long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
-  const long long total = (long long)M * N;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long m = e / N, n = e - m * N;
-    float acc = part[m * ldp + n];
-    for (int s = 1; s < S; ++s) acc += part[((long long)s * M + m) * ldp + n];
-    if (out) out[m * ld_out + n] = acc;
-    if (out_lp) out_lp[m * ld_lp + n] = __float2bfloat16_rn(acc);
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (n >= N) return;
+  const bool vec = n + 4 <= N && (ldp % 4) == 0;
+  for (long long m = blockIdx.y; m < M; m += gridDim.y) {
+  float acc[4];
+  if (vec) {
+    float4 a = *reinterpret_cast<const float4*>(part + m * ldp + n);
+    acc[0] = a.x, acc[1] = a.y, acc[2] = a.z, acc[3] = a.w;
+    for (int s = 1; s < S; ++s) {
+      const float4 b = *reinterpret_cast<const float4*>(part + ((long long)s * M + m) * ldp + n);
+      acc[0] += b.x, acc[1] += b.y, acc[2] += b.z, acc[3] += b.w;
+    }
+  } else {
+    for (int j = 0; j < 4; ++j) {
+      acc[j] = n + j < N ? part[m * ldp + n + j] : 0.0f;
+      for (int s = 1; s < S; ++s)
+        if (n + j < N) acc[j] += part[((long long)s * M + m) * ldp + n + j];
+    }
   }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (n + j >= N) break;
+    if (out) out[m * ld_out + n + j] = acc[j];
+    if (out_lp) out_lp[m * ld_lp + n + j] = __float2bfloat16_rn(acc[j]);
+  }
+  }
+}
+
+static int launch_splitk_reduce(const float* part, int splits, const GemmArgs& g, long long ld_part,
+                                cudaStream_t st) {
+  const unsigned gx = (unsigned)(((g.N + 3) / 4 + 255) / 256);
+  const unsigned gy = (unsigned)(g.M < 65535 ? g.M : 65535);
+  k_splitk_reduce<<<dim3(gx, gy), 256, 0, st>>>(part, splits, g.M, g.N, ld_part, g.epi.out_f32, g.epi.ld_f32,
+                                                 g.epi.out_bf16, g.epi.ld_bf16);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -884,12 +912,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
-    const long long total = (long long)g.M * g.N;
-    long long blocks = (total + 255) / 256;
-    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
-    k_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(part, splits, g.M, g.N, p.ld_part, g.epi.out_f32,
-                                                      g.epi.ld_f32, g.epi.out_bf16, g.epi.ld_bf16);
-    SG_CUDA_TRY(cudaGetLastError());
+    if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
   }
   return SG_OK;
@@ -943,12 +966,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
-    const long long total = (long long)g.M * g.N;
-    long long blocks = (total + 255) / 256;
-    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
-    k_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(part, splits, g.M, g.N, p.ld_part, g.epi.out_f32,
-                                                      g.epi.ld_f32, g.epi.out_bf16, g.epi.ld_bf16);
-    SG_CUDA_TRY(cudaGetLastError());
+    if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
   }
   return SG_OK;
