@@ -118,6 +118,9 @@ SG_API int sg_ew_variant_count(sg_kernel* kern);
  *                        product and sum rounded (no FMA): bit-exact with the
  *                        reference kernel's order restated in fp32.
  *   SG_PREC_STRICT_FP64  same in f64: bit-exact with the unmodified reference.
+ *   SG_PREC_TF32         A,B f32 -> tcgen05 kind::tf32 (operands rounded to
+ *                        TF32 by the tensor cores, fp32 accumulate); lda/ldb
+ *                        multiples of 4, 16-byte aligned; aux is f32.
  * epilogue (per output element, v = the dot product):
  *   SG_EPI_STORE     out = v
  *   SG_EPI_BIAS_ACT  out_pre = v + bias[n];  out = act(v + bias[n])
@@ -128,6 +131,7 @@ SG_API int sg_ew_variant_count(sg_kernel* kern);
 #define SG_PREC_BF16 0
 #define SG_PREC_STRICT_FP32 1
 #define SG_PREC_STRICT_FP64 2
+#define SG_PREC_TF32 3
 
 #define SG_EPI_STORE 0
 #define SG_EPI_BIAS_ACT 1

@@ -13,7 +13,8 @@ struct GemmEpilogue {
   int mode;                    // SG_EPI_STORE / SG_EPI_BIAS_ACT / SG_EPI_ACT_GRAD
   int act;                     // SG_ACT_*
   const float* bias;           // [N]                                (BIAS_ACT)
-  const __nv_bfloat16* aux;    // saved activation h [M][ld_aux]     (ACT_GRAD)
+  const __nv_bfloat16* aux;    // saved activation h [M][ld_aux]     (ACT_GRAD, BF16 precision)
+  const float* aux_f32;        // same, fp32                         (ACT_GRAD, TF32 precision)
   long long ld_aux;
   float* out_pre;              // optional fp32 z+b before activation (BIAS_ACT)
   long long ld_pre;
@@ -44,16 +45,16 @@ __device__ __forceinline__ void warp_colsum_store(float (&v)[32], float* dst, in
 
 struct GemmArgs {
   int M, N, K;
-  const __nv_bfloat16* A;
+  const void* A;  // bf16, or fp32 with tf32 (operands read as TF32 by the tensor cores)
   long long lda;
   bool a_mn;  // A stored [K][M] (MN-major) instead of [M][K]
-  const __nv_bfloat16* B;
+  const void* B;
   long long ldb;
   bool b_mn;  // B stored [K][N] instead of [N][K]
   GemmEpilogue epi;
 };
 
-int launch_gemm_bf16(const GemmArgs& g, int num_sms, cudaStream_t st);
+int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st);
 
 namespace strict {
 struct StrictArgs {
@@ -108,6 +109,18 @@ __device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const float (
   }
 }
 
+__device__ __forceinline__ void load_row_f32(const float* src, float (&v)[32], int n) {
+  if (n == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(src + i));
+      v[i] = f.x, v[i + 1] = f.y, v[i + 2] = f.z, v[i + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i < n ? __ldg(src + i) : 0.0f;
+  }
+}
 __device__ __forceinline__ void load_row_bf16(const __nv_bfloat16* src, float (&v)[32], int n) {
   if (n == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
 #pragma unroll

@@ -23,22 +23,25 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
   int rc = ctx_activate(ctx);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (d->precision == SG_PREC_BF16) {
+  if (d->precision == SG_PREC_BF16 || d->precision == SG_PREC_TF32) {
+    const bool tf32 = d->precision == SG_PREC_TF32;
     if (d->K == 0) return fail(SG_EINVAL, "gemm: K must be positive");
+    if (tf32 && d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
     GemmArgs g{};
     g.M = (int)d->M;
     g.N = (int)d->N;
     g.K = (int)d->K;
-    g.A = (const __nv_bfloat16*)d->A;
+    g.A = d->A;
     g.lda = d->lda;
     g.a_mn = d->a_mn_major != 0;
-    g.B = (const __nv_bfloat16*)d->B;
+    g.B = d->B;
     g.ldb = d->ldb;
     g.b_mn = d->b_mn_major != 0;
     g.epi.mode = d->epilogue;
     g.epi.act = d->act;
     g.epi.bias = (const float*)d->bias;
-    g.epi.aux = (const __nv_bfloat16*)d->aux;
+    g.epi.aux = tf32 ? nullptr : (const __nv_bfloat16*)d->aux;
+    g.epi.aux_f32 = tf32 ? (const float*)d->aux : nullptr;
     g.epi.ld_aux = d->ld_aux;
     g.epi.out_pre = (float*)d->out_pre;
     g.epi.ld_pre = d->ld_pre;
@@ -48,7 +51,7 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     g.epi.ld_bf16 = d->ld_lp;
     g.epi.colsum = d->colsum;
     g.epi.ld_colsum = d->ld_colsum;
-    return launch_gemm_bf16(g, ctx_num_sms(ctx), st);
+    return launch_gemm_tc(g, tf32, ctx_num_sms(ctx), st);
   }
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
     if (d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");

@@ -38,8 +38,22 @@ namespace sg {
 namespace tc {
 
 constexpr int BM = 128;           // UMMA M (cta_group::1)
-constexpr int BK = 64;            // 64 bf16 = one 128-byte swizzle row
-constexpr int UMMA_K = 16;
+// A k-block is one 128-byte swizzle row of K: 64 bf16 or 32 fp32 (TF32)
+// elements; one UMMA_K step is 32 bytes of K (16 bf16 / 8 TF32).  Stage
+// bytes per k-block are therefore the same for both operand types.
+template <bool TF32> struct Elem {
+  static constexpr int BK = TF32 ? 32 : 64;
+  static constexpr int UMMA_K = TF32 ? 8 : 16;
+  static constexpr int KSTEPS = BK / UMMA_K;          // 4
+  static constexpr uint32_t MN_CHUNK = BK * 128;      // MN-major: EPR x BK box bytes (= LBO)
+  static constexpr uint32_t MN_KSTEP = UMMA_K * 128;  // MN-major: next UMMA_K K-rows
+  // MN-major 32-bit operands only exist in the 128B swizzle with 32-byte
+  // atoms (layout type 1, TMA SWIZZLE_128B_ATOM_32B): 4-row swizzle groups,
+  // so the K-direction group stride (SBO) is 512 B instead of 1024 B.
+  static constexpr uint32_t MN_SBO = TF32 ? 512 : 1024;
+  static constexpr uint32_t MN_LAYOUT = TF32 ? 1 : 2;
+};
+constexpr int ROW_BYTES = 128;
 constexpr int NUM_THREADS = 384;  // 12 warps: TMA, MMA, TMEM, idle, 8 epilogue
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;      // two per TMEM lane quadrant, each takes half the columns
@@ -95,14 +109,23 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+template <bool TF32>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if (TF32)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 // 32 lanes x 32 consecutive fp32 columns: thread t of warp q gets lane 32q+t
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -122,19 +145,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 // UMMA shared-memory descriptor, 128B swizzle (layout type 2), sm_100 version bit.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
-// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, M x N, operand majors.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: fp32 accumulate (bit 4), A/B format at bits 7/10
+// (kind::f16: 1 = bf16; kind::tf32: 2 = tf32), operand majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_tc(int M, int N, bool a_mn, bool b_mn, bool tf32) {
+  return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // ------------------------------------------------------------- epilogue
@@ -309,7 +333,8 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
     float h[32];
-    load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
+    if (e.aux_f32) load_row_f32(e.aux_f32 + (long long)m * e.ld_aux + n0, h, nn);
+    else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
     act_grad_chunk(v, h, e.act);
   }
   const int row0 = m - lane;
@@ -326,17 +351,19 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   if (e.colsum) warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+template <bool TF32, int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
                  const KParams p) {
-  constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
+  using E = Elem<TF32>;
+  constexpr int BK = E::BK;
+  constexpr int A_BYTES = BM * ROW_BYTES;
+  constexpr int B_BYTES = BN * ROW_BYTES;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
   static_assert(TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM allocation");
-  constexpr uint32_t IDESC = idesc_bf16(BM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = idesc_tc(BM, BN, A_MN, B_MN, TF32);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -404,13 +431,13 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 64 * BK * 2, &tma_a, &full_bar[stage], tc.m0 + 64 * j, k0);
+            for (int j = 0; j < BM / BK; ++j) tma_load_2d(sa + j * E::MN_CHUNK, &tma_a, &full_bar[stage], tc.m0 + BK * j, k0);
           } else {
             tma_load_2d(sa, &tma_a, &full_bar[stage], k0, tc.m0);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 64 * BK * 2, &tma_b, &full_bar[stage], tc.n0 + 64 * j, k0);
+            for (int j = 0; j < BN / BK; ++j) tma_load_2d(sb + j * E::MN_CHUNK, &tma_b, &full_bar[stage], tc.n0 + BK * j, k0);
           } else {
             tma_load_2d(sb, &tma_b, &full_bar[stage], k0, tc.n0);
           }
@@ -440,12 +467,12 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constan
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            // K-major: next 16 K-elements are +32 B inside the swizzle row;
-            // MN-major: next 16 K-rows are +16*128 B (two 8-row core groups)
-            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 64 * BK * 2, 1024) : sdesc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 64 * BK * 2, 1024) : sdesc(sb + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+          for (int k = 0; k < E::KSTEPS; ++k) {
+            // K-major: the next UMMA_K elements are +32 B inside the swizzle row;
+            // MN-major: the next UMMA_K K-rows are +UMMA_K*128 B
+            const uint64_t ad = A_MN ? sdesc(sa + k * E::MN_KSTEP, E::MN_CHUNK, E::MN_SBO, E::MN_LAYOUT) : sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + k * E::MN_KSTEP, E::MN_CHUNK, E::MN_SBO, E::MN_LAYOUT) : sdesc(sb + k * 32, 16, 1024);
+            tc_mma<TF32>(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc_commit(&empty_bar[stage]);  // smem stage free once these MMAs retire
           if (++stage == STAGES) {
@@ -537,14 +564,23 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+template <bool TF32>
 __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if (TF32)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on the barrier in both CTAs
   asm volatile(
@@ -554,17 +590,19 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
       : "memory");
 }
 
-template <int STAGES, bool A_MN, bool B_MN>
+template <bool TF32, int STAGES, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
-gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
                       const KParams p) {
   constexpr int PM = 256, BN = 256, HALF = 128;
-  constexpr int A_BYTES = HALF * BK * 2;
-  constexpr int B_BYTES = HALF * BK * 2;
+  using E = Elem<TF32>;
+  constexpr int BK = E::BK;
+  constexpr int A_BYTES = HALF * ROW_BYTES;
+  constexpr int B_BYTES = HALF * ROW_BYTES;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;
-  constexpr uint32_t IDESC = idesc_bf16(PM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = idesc_tc(PM, BN, A_MN, B_MN, TF32);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -650,13 +688,13 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_co
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / 64; ++j) tma_load_2d_pair(sa + j * 64 * BK * 2, &tma_a, fb, am + 64 * j, k0);
+            for (int j = 0; j < HALF / BK; ++j) tma_load_2d_pair(sa + j * E::MN_CHUNK, &tma_a, fb, am + BK * j, k0);
           } else {
             tma_load_2d_pair(sa, &tma_a, fb, k0, am);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / 64; ++j) tma_load_2d_pair(sb + j * 64 * BK * 2, &tma_b, fb, bn + 64 * j, k0);
+            for (int j = 0; j < HALF / BK; ++j) tma_load_2d_pair(sb + j * E::MN_CHUNK, &tma_b, fb, bn + BK * j, k0);
           } else {
             tma_load_2d_pair(sb, &tma_b, fb, k0, bn);
           }
@@ -686,10 +724,10 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_co
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 64 * BK * 2, 1024) : sdesc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 64 * BK * 2, 1024) : sdesc(sb + k * 32, 16, 1024);
-            tc_mma_pair(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+          for (int k = 0; k < E::KSTEPS; ++k) {
+            const uint64_t ad = A_MN ? sdesc(sa + k * E::MN_KSTEP, E::MN_CHUNK, E::MN_SBO, E::MN_LAYOUT) : sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + k * E::MN_KSTEP, E::MN_CHUNK, E::MN_SBO, E::MN_LAYOUT) : sdesc(sb + k * 32, 16, 1024);
+            tc_mma_pair<TF32>(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
           if (++stage == STAGES) {
@@ -774,16 +812,21 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [outer][ld] buffer, box {64, box_outer}, 128B swizzle.
-int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld, int box_outer) {
+// 2-D operand tensor map over a row-major [outer][ld] buffer (bf16, or fp32
+// read as TF32), box {one 128-byte row, box_outer}, 128B swizzle.
+int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld, int box_outer,
+             bool tf32, bool mn_major) {
   EncodeTiled enc = encode_fn();
   if (!enc) return fail(SG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const int esz = tf32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)(tc::ROW_BYTES / esz), (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
   return SG_OK;
@@ -863,29 +906,30 @@ static int launch_splitk_reduce(const float* part, int splits, const GemmArgs& g
   return SG_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <bool TF32, int BN, bool A_MN, bool B_MN>
 int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
-  constexpr int STAGE = tc::BM * tc::BK * 2 + BN * tc::BK * 2;
+  constexpr int BK = tc::Elem<TF32>::BK;
+  constexpr int STAGE = tc::BM * tc::ROW_BYTES + BN * tc::ROW_BYTES;
   constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
   constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::STAGE_SLOT;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
-  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, tc::BM);
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, tc::BM, TF32, false);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN);
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN, TF32, false);
   if (rc) return rc;
-  auto kern = tc::gemm_bf16_kernel<BN, STAGES, A_MN, B_MN>;
+  auto kern = tc::gemm_tc_kernel<TF32, BN, STAGES, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
   const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN);
-  const int num_kb = (g.K + tc::BK - 1) / tc::BK;
+  const int num_kb = (g.K + BK - 1) / BK;
   // split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
   // layer: M = N = 1024, K = batch): plain-store epilogues only
   int splits = 1, kb_per = num_kb;
@@ -918,22 +962,23 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   return SG_OK;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool TF32, bool A_MN, bool B_MN>
 int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  constexpr int BK = tc::Elem<TF32>::BK;
   constexpr int STAGES = 6;
-  constexpr int STAGE = 128 * tc::BK * 2 * 2;
+  constexpr int STAGE = 128 * tc::ROW_BYTES * 2;
   // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
   constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::STAGE_SLOT;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
-  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, 128);
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, 128, TF32, false);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128);
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false);
   if (rc) return rc;
-  auto kern = tc::gemm_bf16_pair_kernel<STAGES, A_MN, B_MN>;
+  auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -941,7 +986,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int pairs_avail = num_sms / 2;
   const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
-  const int num_kb = (g.K + tc::BK - 1) / tc::BK;
+  const int num_kb = (g.K + BK - 1) / BK;
   int splits = 1, kb_per = num_kb;
   if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && tiles * 2 <= pairs_avail && num_kb >= 8) {
     int s = pairs_avail / tiles;
@@ -972,36 +1017,44 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   return SG_OK;
 }
 
-template <int BN>
+template <bool TF32, int BN>
 int run_bn(const GemmArgs& g, int num_sms, cudaStream_t st) {
-  if (!g.a_mn && !g.b_mn) return run<BN, false, false>(g, num_sms, st);
-  if (!g.a_mn && g.b_mn) return run<BN, false, true>(g, num_sms, st);
-  if (g.a_mn && g.b_mn) return run<BN, true, true>(g, num_sms, st);
-  return run<BN, true, false>(g, num_sms, st);
+  if (!g.a_mn && !g.b_mn) return run<TF32, BN, false, false>(g, num_sms, st);
+  if (!g.a_mn && g.b_mn) return run<TF32, BN, false, true>(g, num_sms, st);
+  if (g.a_mn && g.b_mn) return run<TF32, BN, true, true>(g, num_sms, st);
+  return run<TF32, BN, true, false>(g, num_sms, st);
 }
 
-}  // namespace
-
-int launch_gemm_bf16(const GemmArgs& g, int num_sms, cudaStream_t st) {
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return fail(SG_EINVAL, "gemm: empty problem");
-  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!aligned(g.A) || !aligned(g.B)) return fail(SG_EINVAL, "gemm: A and B must be 16-byte aligned");
-  if (g.lda % 8 || g.ldb % 8) return fail(SG_EINVAL, "gemm: lda/ldb must be multiples of 8 elements");
-  if (g.lda < (g.a_mn ? g.M : g.K) || g.ldb < (g.b_mn ? g.N : g.K))
-    return fail(SG_EINVAL, "gemm: leading dimension smaller than the row");
-  if (g.N <= 64) return run_bn<64>(g, num_sms, st);
-  if (g.N <= 128) return run_bn<128>(g, num_sms, st);
+template <bool TF32>
+int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  if (g.N <= 64) return run_bn<TF32, 64>(g, num_sms, st);
+  if (g.N <= 128) return run_bn<TF32, 128>(g, num_sms, st);
   static const bool pair_ok = [] {
     const char* e = std::getenv("SGB200_GEMM_PAIR");
     return !(e && e[0] == '0');
   }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
-    if (!g.a_mn && !g.b_mn) return run_pair<false, false>(g, num_sms, st);
-    if (!g.a_mn && g.b_mn) return run_pair<false, true>(g, num_sms, st);
-    if (g.a_mn && g.b_mn) return run_pair<true, true>(g, num_sms, st);
-    return run_pair<true, false>(g, num_sms, st);
+    if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false>(g, num_sms, st);
+    if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true>(g, num_sms, st);
+    if (g.a_mn && g.b_mn) return run_pair<TF32, true, true>(g, num_sms, st);
+    return run_pair<TF32, true, false>(g, num_sms, st);
   }
-  return run_bn<256>(g, num_sms, st);
+  return run_bn<TF32, 256>(g, num_sms, st);
+}
+
+}  // namespace
+
+int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return fail(SG_EINVAL, "gemm: empty problem");
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!aligned(g.A) || !aligned(g.B)) return fail(SG_EINVAL, "gemm: A and B must be 16-byte aligned");
+  const int row_mult = tf32 ? 4 : 8;  // 16-byte TMA strides
+  if (g.lda % row_mult || g.ldb % row_mult)
+    return fail(SG_EINVAL, tf32 ? "gemm: lda/ldb must be multiples of 4 elements (TF32)"
+                                : "gemm: lda/ldb must be multiples of 8 elements");
+  if (g.lda < (g.a_mn ? g.M : g.K) || g.ldb < (g.b_mn ? g.N : g.K))
+    return fail(SG_EINVAL, "gemm: leading dimension smaller than the row");
+  return tf32 ? dispatch<true>(g, num_sms, st) : dispatch<false>(g, num_sms, st);
 }
 
 }  // namespace sg

@@ -16,7 +16,7 @@ import ctypes
 
 from . import runtime as rt
 
-PREC = {"bf16": 0, "strict_fp32": 1, "strict_fp64": 2}
+PREC = {"bf16": 0, "strict_fp32": 1, "strict_fp64": 2, "tf32": 3}
 EPI = {"store": 0, "bias_act": 1, "act_grad": 2}
 ACT = {"identity": 0, "sigmoid": 1, "tanh": 2, "relu": 3}
 

@@ -6,6 +6,10 @@
 * STRICT_FP32: bit-exact vs the fp32 restatement of tensor.py:351-361
   (oracle/csrc/strict_gemm.c);
 * STRICT_FP64: bit-exact vs the unmodified reference (golden tensor.npz).
+* TF32 tensor-core path (fp32 operands): inputs exactly representable in
+  TF32 -> rel <= 1e-5 of sum|a*b| (accumulation order only); arbitrary fp32
+  inputs -> rel <= 2^-9 of sum|a*b| (the tensor cores drop 13 mantissa bits
+  of each operand: <= 2^-10 relative each).
 """
 
 import numpy as np
@@ -58,6 +62,66 @@ def test_bf16_tensor_core_gemm(M, N, K, layout):
     gemm(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, out=out)
     torch.cuda.synchronize()
     check_close(out.double().cpu().numpy(), a, b.T)
+
+
+def tf32_exact(x):
+    # clear the low 13 mantissa bits: exactly representable in TF32
+    u = x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)
+    return u.view(np.float32)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 200, 104), (7, 10, 32), (129, 257, 136),
+                                   (1024, 768, 512), (520, 300, 200), (256, 256, 8192)])
+@pytest.mark.parametrize("layout", ["kk", "k_mn", "mn_mn", "mn_k"])
+def test_tf32_tensor_core_gemm(M, N, K, layout):
+    rng = np.random.default_rng(M * 5 + N * 11 + K)
+    a_mn = layout.startswith("mn")
+    b_mn = layout.endswith("_mn")
+
+    def pad_ld(x):  # leading dimension multiple of 4 elements
+        rows, cols = x.shape
+        ld = (cols + 3) // 4 * 4
+        buf = torch.zeros((rows, ld), dtype=torch.float32, device="cuda")
+        buf[:, :cols] = torch.from_numpy(x)
+        return buf[:, :cols]
+
+    for exact, tol in ((True, 1e-5), (False, 2.0 ** -9)):
+        a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+        b = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+        if exact:
+            a, b = tf32_exact(a), tf32_exact(b)
+        A = pad_ld(a.T.copy() if a_mn else a)
+        B = pad_ld(b.T.copy() if b_mn else b)
+        out = torch.full((M, N), float("nan"), device="cuda")
+        gemm(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, precision="tf32", out=out)
+        torch.cuda.synchronize()
+        check_close(out.double().cpu().numpy(), a.astype(np.float64), b.astype(np.float64).T, tol=tol)
+
+
+def test_tf32_epilogues():
+    rng = np.random.default_rng(3)
+    M, N, K = 256, 384, 192
+    a = tf32_exact(rng.uniform(-1, 1, (M, K)))
+    w = tf32_exact(rng.uniform(-1, 1, (N, K)))
+    bias = rng.uniform(-0.5, 0.5, N).astype(np.float32)
+    A, W, bt = (torch.from_numpy(v).cuda() for v in (a, w, bias))
+    z = a.astype(np.float64) @ w.astype(np.float64).T + bias
+    out = torch.empty((M, N), device="cuda")
+    pre = torch.empty((M, N), device="cuda")
+    gemm(A, W, precision="tf32", epilogue="bias_act", act="tanh", bias=bt, out=out, out_pre=pre)
+    torch.cuda.synchronize()
+    assert np.abs(pre.double().cpu().numpy() - z).max() <= 1e-4
+    assert np.abs(out.double().cpu().numpy() - np.tanh(z)).max() <= 2e-4
+    # act' epilogue with an fp32 saved activation
+    h = rng.uniform(0.05, 0.95, (M, K)).astype(np.float32)
+    dy = tf32_exact(rng.uniform(-1, 1, (M, N)))
+    out = torch.empty((M, K), device="cuda")
+    gemm(torch.from_numpy(dy).cuda(), W, b_mn=True, precision="tf32", epilogue="act_grad", act="sigmoid",
+         aux=torch.from_numpy(h).cuda(), out=out)
+    torch.cuda.synchronize()
+    hq = h.astype(np.float64)
+    want = (dy.astype(np.float64) @ w.astype(np.float64)) * hq * (1 - hq)
+    assert np.abs(out.double().cpu().numpy() - want).max() <= 1e-4
 
 
 def test_bf16_epilogues():
