@@ -412,8 +412,11 @@ def _timed(fn, steps, warmup, dist, stream, per_step_events=None):
     return max_over_ranks(dist, s.elapsed_time(t)) / steps, evs
 
 
-def dense_c3_bench(args, dist, peaks):
-    """c3: one Dense 4096->4096 (sigmoid) fwd + pullback, batch 8192, bf16 tensor cores."""
+TF32_PEAK_TFLOPS = 1100.0  # B200_PROFILING.md dense TF32 figure (no measured TF32 peak in MEASURED_PEAKS.json)
+
+
+def dense_c3_bench(args, dist, peaks, precision="bf16"):
+    """c3: one Dense 4096->4096 (sigmoid) fwd + pullback, batch 8192, bf16 or TF32 tensor cores."""
     import torch
 
     from paper_1811_01457_b200 import runtime as rt
@@ -422,28 +425,34 @@ def dense_c3_bench(args, dist, peaks):
 
     M, D = 8192, 4096
     g = torch.Generator(device="cuda").manual_seed(3)
-    layer = DenseLayer(M, D, D, "sigmoid")
+    layer = DenseLayer(M, D, D, "sigmoid", precision=precision)
     r = (6.0 / (2 * D)) ** 0.5
     layer.W.copy_((torch.rand((D, D), generator=g, device="cuda") * 2 - 1) * r)
-    layer.Wb.copy_(layer.W.to(torch.bfloat16))
+    if layer.Wb is not layer.W:
+        layer.Wb.copy_(layer.W.to(torch.bfloat16))
     layer.b.copy_((torch.rand(D, generator=g, device="cuda") * 2 - 1) * 0.01)
-    layer.X.copy_((torch.rand((M, D), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    layer.X.copy_((torch.rand((M, D), generator=g, device="cuda") * 2 - 1).to(layer.X.dtype))
+    tf32 = precision == "tf32"
+    Wop = layer.W if tf32 else layer.Wb
     ybar = torch.rand((M, D), generator=g, device="cuda") * 2 - 1
     stream = torch.cuda.current_stream()
     lib, ctx = _lib(), rt.context()
 
     def step(ev):
         if ev: ev[0].record(stream)
-        gemm(layer.X, layer.Wb, epilogue="bias_act", act="sigmoid", bias=layer.b, out_lp=layer.H)
+        if tf32:
+            gemm(layer.X, Wop, precision="tf32", epilogue="bias_act", act="sigmoid", bias=layer.b, out=layer.H)
+        else:
+            gemm(layer.X, Wop, epilogue="bias_act", act="sigmoid", bias=layer.b, out_lp=layer.H)
         if ev: ev[1].record(stream)
         rt.check(lib.sg_act_grad(ctx, _p(ybar), _dt(ybar), ybar.stride(0), _p(layer.H), _dt(layer.H),
                                  layer.H.stride(0), M, D, ACT["sigmoid"], _p(layer.dZ), _dt(layer.dZ),
                                  layer.dZ.stride(0), None, 0, 0, _p(layer.colsum), layer.colsum.stride(0),
                                  rt.stream_ptr()))
         if ev: ev[2].record(stream)
-        gemm(layer.dZ, layer.Wb, b_mn=True, out=layer.dX)
+        gemm(layer.dZ, Wop, b_mn=True, precision=precision, out=layer.dX)
         if ev: ev[3].record(stream)
-        gemm(layer.dZ, layer.X, a_mn=True, b_mn=True, out=layer.dW)
+        gemm(layer.dZ, layer.X, a_mn=True, b_mn=True, precision=precision, out=layer.dW)
         if ev: ev[4].record(stream)
         rt.check(lib.sg_colsum_finalize(ctx, _p(layer.colsum), (M + 31) // 32, layer.colsum.stride(0), D,
                                         _p(layer.db), rt.stream_ptr()))
@@ -455,19 +464,22 @@ def dense_c3_bench(args, dist, peaks):
     gf = 2.0 * M * D * D
     gemm_ms = kms["fwd_gemm"] + kms["dX_gemm"] + kms["dW_gemm"]
     achieved = 3 * gf / (gemm_ms * 1e-3) / 1e12
+    esz = 4 if tf32 else 2
+    peak = TF32_PEAK_TFLOPS if tf32 else peaks["bf16_tflops"]
     return {
-        "workload": "c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, bf16 tcgen05",
+        "workload": f"c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, {precision} tcgen05",
         "value": round(3 * gf / (ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
         "flops_per_step": 3 * gf,
         "kernels_ms": {k: round(v, 4) for k, v in kms.items()},
         "gemm_TFLOPs": {k: round(gf / (kms[k] * 1e-3) / 1e12, 1) for k in ("fwd_gemm", "dX_gemm", "dW_gemm")},
-        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (fwd, dX, dW aggregated)",
-                     "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": round(achieved / peaks["bf16_tflops"], 4), "peak_kind": "burst",
-                     "traffic": traffic_of("gemm_bf16_fwd_c3", True),
-                     "traffic_algorithmic_bytes": 2 * (M * D + D * D) + 2 * M * D},
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel / gemm_tc_pair_kernel (fwd, dX, dW aggregated)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4),
+                     "peak_kind": "spec dense TF32 (B200_PROFILING.md)" if tf32 else "burst",
+                     "traffic": None if tf32 else traffic_of("gemm_bf16_fwd_c3", True),
+                     "traffic_algorithmic_bytes": esz * (M * D + D * D + M * D)},
         "gpu_launches_per_step": 5,
-        "l2": "working set ~544 MB per step > 126 MB L2",
+        "l2": f"working set ~{808 if tf32 else 544} MB per step > 126 MB L2",
     }
 
 
@@ -518,6 +530,8 @@ def secondary_benches(args, world, rank, dist):
         try:
             if w == "c3" and world == 1:
                 out.append(dense_c3_bench(args, dist, peaks))
+            elif w == "c3tf32" and world == 1:
+                out.append(dense_c3_bench(args, dist, peaks, precision="tf32"))
             elif w == "c4":
                 out.append(mlp_bench(args, world, rank, dist, peaks, "c4", (4096,) * 5,
                                      ("tanh",) * 3 + ("identity",), 65536, "mse", graph=False))
@@ -616,7 +630,7 @@ def main():
     ap.add_argument("--rows", type=int, default=R_ROWS)
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--secondary", default="c1,c3,c4,c5",
+    ap.add_argument("--secondary", default="c1,c3,c3tf32,c4,c5",
                     help="comma list of extra workloads measured in the same run (c1,c3,c4,c5)")
     ap.add_argument("--dense-steps", type=int, default=20)
     ap.add_argument("--mlp-steps", type=int, default=10)

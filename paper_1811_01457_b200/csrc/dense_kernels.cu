@@ -105,9 +105,16 @@ __device__ __forceinline__ void st8_f32(float* p, const V8& x) {
   reinterpret_cast<float4*>(p)[1] = make_float4(x.v[4], x.v[5], x.v[6], x.v[7]);
 }
 
-__global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long long ldy, const __nv_bfloat16* h,
+__device__ __forceinline__ V8 ld8(const float* p) { return ld8_f32(p); }
+__device__ __forceinline__ V8 ld8(const __nv_bfloat16* p) { return ld8_bf16(p); }
+__device__ __forceinline__ void st8(float* p, const V8& v) { st8_f32(p, v); }
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const V8& v) { st8_bf16(p, v); }
+
+// HT/DT: bf16 (BF16 tensor-core chain) or float (TF32 chain)
+template <class HT, class DT>
+__global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long long ldy, const HT* h,
                                                      long long ldh, long long M, long long N, int act,
-                                                     __nv_bfloat16* dz, long long lddz, float* colsum,
+                                                     DT* dz, long long lddz, float* colsum,
                                                      long long ldc) {
   const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
   if (c >= N) return;
@@ -116,20 +123,21 @@ __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long lon
 #pragma unroll 4
   for (long long r = r0; r < r1; ++r) {
     const V8 yb = ld8_f32(ybar + r * ldy + c);
-    const V8 hv = ld8_bf16(h + r * ldh + c);
+    const V8 hv = ld8(h + r * ldh + c);
     V8 o;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       o.v[j] = yb.v[j] * act_grad_h(hv.v[j], act);
       acc[j] += o.v[j];
     }
-    st8_bf16(dz + r * lddz + c, o);
+    st8(dz + r * lddz + c, o);
   }
   if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
 }
 
+template <class DT>
 __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, const float* y, long long ldy,
-                                                long long M, long long N, float scale, __nv_bfloat16* dz,
+                                                long long M, long long N, float scale, DT* dz,
                                                 long long lddz, float* colsum, long long ldc, double* loss_part) {
   __shared__ double red[256];
   const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
@@ -151,7 +159,7 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
         acc[j] += o.v[j];
       }
       lsum += (double)l;
-      st8_bf16(dz + r * lddz + c, o);
+      st8(dz + r * lddz + c, o);
     }
     if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
   }
@@ -382,13 +390,17 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
   int rc = ctx_activate(ctx);
   if (rc) return rc;
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (ybar_dtype == SG_F32 && h_dtype == SG_BF16 && dz_dtype == SG_BF16 && !dz2 && N % 8 == 0 &&
-      ld_y % 8 == 0 && ld_h % 8 == 0 && ld_dz % 8 == 0 && a16(ybar) && a16(h) && a16(dz) &&
+  if (ybar_dtype == SG_F32 && (h_dtype == SG_BF16 || h_dtype == SG_F32) && h_dtype == dz_dtype && !dz2 &&
+      N % 8 == 0 && ld_y % 8 == 0 && ld_h % 8 == 0 && ld_dz % 8 == 0 && a16(ybar) && a16(h) && a16(dz) &&
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
     dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
-    dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
-                                                            ld_h, M, N, act, (__nv_bfloat16*)dz, ld_dz, colsum,
-                                                            ld_colsum);
+    if (h_dtype == SG_BF16)
+      dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
+                                                              ld_h, M, N, act, (__nv_bfloat16*)dz, ld_dz, colsum,
+                                                              ld_colsum);
+    else
+      dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const float*)h, ld_h, M,
+                                                              N, act, (float*)dz, ld_dz, colsum, ld_colsum);
     SG_CUDA_TRY(cudaGetLastError());
     return SG_OK;
   }
@@ -448,14 +460,19 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
   cudaStream_t st = (cudaStream_t)stream;
   long long blocks = 0;
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (kind == SG_LOSS_MSE && dtype == SG_F32 && dz_dtype == SG_BF16 && !dz2 && N % 8 == 0 && ld_z % 8 == 0 &&
+  if (kind == SG_LOSS_MSE && dtype == SG_F32 && (dz_dtype == SG_BF16 || dz_dtype == SG_F32) && !dz2 &&
+      N % 8 == 0 && ld_z % 8 == 0 &&
       ld_y % 8 == 0 && ld_dz % 8 == 0 && a16(z) && a16(y) && a16(dz) &&
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
     dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
     blocks = (long long)g8.x * g8.y;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
-    dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
-                                     (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part);
+    if (dz_dtype == SG_BF16)
+      dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                       (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part);
+    else
+      dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                       (float*)dz, ld_dz, colsum, ld_colsum, loss_part);
   } else if (kind == SG_LOSS_MSE) {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
     if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");

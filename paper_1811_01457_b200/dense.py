@@ -131,17 +131,24 @@ class DenseLayer:
                 dX = dZ . W            -- GEMM, W read MN-major
                 dW = dZ^T . X          -- GEMM, both operands MN-major
                 db = colsum(dZ)        -- finalize of the partial sums
+
+    precision "bf16": bf16 operands/activations (W has a bf16 shadow);
+    "tf32": fp32 operands/activations read as TF32 by the tensor cores.
     """
 
-    def __init__(self, M: int, fan_in: int, fan_out: int, act: str = "sigmoid"):
+    def __init__(self, M: int, fan_in: int, fan_out: int, act: str = "sigmoid", precision: str = "bf16"):
         import torch
 
+        if precision not in ("bf16", "tf32"):
+            raise ValueError(f"DenseLayer precision must be bf16 or tf32, not {precision!r}")
         dev = torch.device("cuda", torch.cuda.current_device())
         self.M, self.K, self.N, self.act = M, fan_in, fan_out, act
-        bf = torch.bfloat16
+        self.precision = precision
+        bf = torch.bfloat16 if precision == "bf16" else torch.float32
         self.X = torch.zeros((M, _ld(fan_in)), dtype=bf, device=dev)[:, :fan_in]
         self.W = torch.zeros((fan_out, _ld(fan_in)), dtype=torch.float32, device=dev)[:, :fan_in]
-        self.Wb = torch.zeros((fan_out, _ld(fan_in)), dtype=bf, device=dev)[:, :fan_in]
+        self.Wb = (torch.zeros((fan_out, _ld(fan_in)), dtype=bf, device=dev)[:, :fan_in]
+                   if precision == "bf16" else self.W)
         self.b = torch.zeros(fan_out, dtype=torch.float32, device=dev)
         self.H = torch.zeros((M, _ld(fan_out)), dtype=bf, device=dev)[:, :fan_out]
         self.dZ = torch.zeros((M, _ld(fan_out)), dtype=bf, device=dev)[:, :fan_out]
@@ -154,13 +161,17 @@ class DenseLayer:
         import torch
 
         self.W.copy_(torch.as_tensor(np.asarray(W), dtype=torch.float32))
-        self.Wb.copy_(self.W.to(torch.bfloat16))
+        if self.Wb is not self.W:
+            self.Wb.copy_(self.W.to(torch.bfloat16))
         self.b.copy_(torch.as_tensor(np.asarray(b), dtype=torch.float32))
 
     def forward(self, X=None):
         if X is not None:
             self.X.copy_(X, non_blocking=True)
-        gemm(self.X, self.Wb, epilogue="bias_act", act=self.act, bias=self.b, out_lp=self.H)
+        if self.precision == "tf32":
+            gemm(self.X, self.W, precision="tf32", epilogue="bias_act", act=self.act, bias=self.b, out=self.H)
+        else:
+            gemm(self.X, self.Wb, epilogue="bias_act", act=self.act, bias=self.b, out_lp=self.H)
         return self.H
 
     def pullback(self, ybar, need_dx: bool = True):
@@ -170,9 +181,10 @@ class DenseLayer:
                                  self.H.stride(0), self.M, self.N, ACT[self.act], _p(self.dZ), _dt(self.dZ),
                                  self.dZ.stride(0), None, 0, 0, _p(self.colsum), self.colsum.stride(0), st),
                  "sg_act_grad")
+        p = self.precision
         if need_dx:
-            gemm(self.dZ, self.Wb, b_mn=True, out=self.dX)
-        gemm(self.dZ, self.X, a_mn=True, b_mn=True, out=self.dW)
+            gemm(self.dZ, self.W if p == "tf32" else self.Wb, b_mn=True, precision=p, out=self.dX)
+        gemm(self.dZ, self.X, a_mn=True, b_mn=True, precision=p, out=self.dW)
         rt.check(lib.sg_colsum_finalize(ctx, _p(self.colsum), (self.M + 31) // 32, self.colsum.stride(0),
                                         self.N, _p(self.db), st), "sg_colsum_finalize")
         return self.dX, self.dW, self.db
@@ -190,8 +202,11 @@ class ChainEngine:
 
         if loss not in LOSSES:
             raise ValueError(f"unknown loss {loss!r}")
-        if precision not in ("bf16", "strict_fp32", "strict_fp64"):
+        if precision not in ("bf16", "tf32", "strict_fp32", "strict_fp64"):
             raise ValueError(f"unknown precision {precision!r}")
+        # tensor-core modes: bf16 (bf16 operands, bf16 shadow of W) and tf32 (fp32
+        # operands read as TF32); both use the fused colsum bias-gradient stage
+        self.tc = precision in ("bf16", "tf32")
         self.chain = chain
         self.B = int(batch)
         self.loss_kind = loss
@@ -203,7 +218,7 @@ class ChainEngine:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.mdt = torch.float64 if precision == "strict_fp64" else torch.float32  # master dtype
         self.adt = torch.bfloat16 if precision == "bf16" else self.mdt          # activation dtype
-        self.gprec = "bf16" if precision == "bf16" else precision
+        self.gprec = precision
 
         # flat parameter layout [W0, b0, W1, b1, ...], 64-element (256 B) aligned segments
         off = 0
@@ -286,6 +301,9 @@ class ChainEngine:
             if self.precision == "bf16":
                 gemm(self.H[l], Wop, epilogue="bias_act", act=self.acts[l], bias=self.b[l],
                      out_lp=None if last else self.H[l + 1], out=self.Zt if last else None)
+            elif self.precision == "tf32":
+                gemm(self.H[l], Wop, precision="tf32", epilogue="bias_act", act=self.acts[l], bias=self.b[l],
+                     out=self.Zt if last else self.H[l + 1])
             else:
                 gemm(self.H[l], Wop, precision=self.gprec, epilogue="bias_act", act=self.acts[l],
                      bias=self.b[l], out=self.Zt if last else self.H[l + 1])
@@ -308,7 +326,7 @@ class ChainEngine:
         dL = self.sizes[-1]
         dz = self.dZ[top % 2][:, :dL]
         ident = self.acts[top] == "identity"
-        strict = self.precision != "bf16"
+        strict = not self.tc
         target = dz if ident else self.dH
         rt.check(lib.sg_loss(ctx, LOSSES[self.loss_kind], _p(self.Zt), _dt(self.Zt), self.Zt.stride(0),
                              _p(self.Y), self.Y.stride(0), self.B, dL, self.scale, _p(self.loss),
@@ -331,7 +349,7 @@ class ChainEngine:
             ctx, st = rt.context(), rt.stream_ptr()
             d_out, d_in = self.sizes[l + 1], self.sizes[l]
             dz = self.dZ[l % 2][:, :d_out]
-            strict = self.precision != "bf16"
+            strict = not self.tc
             # dW = dZ^T . H[l]   (rules.py:113-115 second cotangent, then _transpose)
             gemm(dz, self.H[l], a_mn=True, b_mn=True, precision=self.gprec, out=self.gW[l])
             # db = reduce_like(dZ, (out,))   (rules.py:45-46)
@@ -349,6 +367,9 @@ class ChainEngine:
                 if strict:
                     gemm(dz, Wop, b_mn=True, precision=self.gprec, epilogue="act_grad",
                          act=self.acts[l - 1], aux=self.H[l], out=dzn)
+                elif self.precision == "tf32":
+                    gemm(dz, Wop, b_mn=True, precision="tf32", epilogue="act_grad", act=self.acts[l - 1],
+                         aux=self.H[l], out=dzn, colsum=self.colsum)
                 else:
                     gemm(dz, Wop, b_mn=True, epilogue="act_grad", act=self.acts[l - 1], aux=self.H[l],
                          out_lp=dzn, colsum=self.colsum)
