@@ -188,12 +188,16 @@ SG_API int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t l
 
 #define SG_LOSS_SOFTMAX_XENT 0
 #define SG_LOSS_MSE 1
+#define SG_LOSS_BCE 2
 /* Fused loss forward + gradient over logits z [M][N] and targets y:
  *   SOFTMAX_XENT: loss = -scale * sum y log softmax(z);  dz = (p * rowsum(y) - y) * scale
  *                 (the c1 loss IR: exp / reduce_sum(axis=1) / div / log / mul, scale = 1/n)
  *   MSE:          loss = scale * sum (z - y)^2;           dz = 2 (z - y) * scale
+ *   BCE:          one-logit head + clamped mean BCE (nn_train.py:209-227):
+ *                 p = sigmoid(z) clamped to [1e-7, 1-1e-7];
+ *                 loss = -scale * sum y log p + (1-y) log(1-p);  dz = 0 where clamped
  * `loss` (device f64) receives the total; loss_part is scratch of n_part doubles
- * (>= ceil(N/32)*ceil(M/256) for MSE, ceil(M/256) for softmax).  Under data
+ * (>= ceil(N/32)*ceil(M/256) for MSE and BCE, ceil(M/256) for softmax).  Under data
  * parallelism scale = 1/global_batch so shard gradients sum to the full one. */
 SG_API int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_z, const void* y,
                    int64_t ld_y, int64_t M, int64_t N, double scale, double* loss, double* loss_part,
@@ -205,6 +209,50 @@ SG_API int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, i
                   void* shadow_bf16, void* stream);
 SG_API int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,
                    void* stream);
+
+/* ------------------------------------------------------ Dense layer
+ * One Dense layer as the reference builds it (nn_train.py:189-210:
+ * transpose(W) / matmul / add / activation) and its pullback (rules.py:45-46,
+ * 82-94, 113-124), composed from the kernels above in one call each.
+ * Operand dtype = the precision's activation dtype: bf16 (SG_PREC_BF16),
+ * f32 (SG_PREC_TF32, SG_PREC_STRICT_FP32), f64 (SG_PREC_STRICT_FP64). */
+typedef struct sg_dense_desc {
+  int64_t batch, fan_in, fan_out;
+  int32_t precision; /* SG_PREC_* */
+  int32_t act;       /* SG_ACT_* of this layer */
+  const void* X;     /* layer input [batch][ldx] */
+  int64_t ldx;
+  const void* W; /* [fan_out][ldw] (bf16 copy for BF16) */
+  int64_t ldw;
+  const void* b; /* [fan_out] f32 (f64 for STRICT_FP64) */
+} sg_dense_desc;
+
+/* H = act(X W^T + b) in the activation dtype (NULL to skip); H_f32: optional
+ * f32 copy (BF16 only, e.g. the logits a loss reads); Z: optional
+ * pre-activation z + b (f32 / f64). */
+SG_API int sg_dense_forward(sg_ctx* ctx, const sg_dense_desc* d, void* H, int64_t ldh, void* H_f32, int64_t ld_hf,
+                            void* Z, int64_t ldz, void* stream);
+
+typedef struct sg_dense_grad {
+  const void* dZ; /* dL/d(z + b) [batch][ld_dz], activation dtype (sg_act_grad / sg_loss make it) */
+  int64_t ld_dz;
+  const float* colsum_in; /* optional per-32-row partial column sums of dZ (BF16/TF32), else computed */
+  int64_t ld_colsum_in;
+  int32_t act_prev; /* SG_ACT_* of the layer below: dX = (dZ W) .* act_prev'(X) -- its dZ.
+                       SG_ACT_IDENTITY: plain dX = dZ W */
+  void* dX;         /* optional [batch][ld_dx] (NULL: first layer, dX not needed) */
+  int64_t ld_dx;
+  int32_t dx_dtype; /* SG_BF16 or SG_F32 for BF16; the activation dtype otherwise */
+  float* colsum_out; /* optional partial column sums of dX (BF16/TF32); may alias colsum_in:
+                        db is finalised before dX is computed */
+  int64_t ld_colsum_out;
+  void* dW; /* [fan_out][ld_dw] f32 (f64 for STRICT_FP64) */
+  int64_t ld_dw;
+  void* db; /* [fan_out] f32 (f64) */
+} sg_dense_grad;
+
+/* dW = dZ^T X, db = colsum(dZ), dX = dZ W [.* act_prev'(X)]; in that order. */
+SG_API int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* g, void* stream);
 
 /* out = reduce_to(a .* b, out_shape); b may be NULL.  The contraction of
  * `fused_map_pullback` (forward_ad.py:232-235) and `reduce_to`

@@ -151,6 +151,39 @@ def mse(z: np.ndarray, Y: np.ndarray):
     return tot * (1.0 / n), (d * (1.0 / n)) + (d * (1.0 / n))
 
 
+BCE_LO, BCE_HI = 1e-7, 1.0 - 1e-7
+
+
+def bce(z: np.ndarray, Y: np.ndarray):
+    """One-logit head + clamped mean BCE: ``_batch_head``'s reshape/sigmoid
+    (nn_train.py:209-210) then ``_bce_mean`` (nn_train.py:213-227):
+    p = sigmoid(z); p2 = clamp via lt/select, gt/select into [1e-7, 1-1e-7];
+    loss = reduce_sum(y log p2 + (1-y) log(1-p2), all) * (-1/n).
+    Gradient in the pullback's order (rules.py:53-58 mul, :77-79 log,
+    select passes the cotangent only where the prediction was kept,
+    :87-89 sigmoid).  z, Y: (n, 1).  Returns (loss, dL/dz (n, 1))."""
+    n = z.shape[0]
+    zf = z.reshape(n)
+    y = Y.reshape(n)
+    p = 1.0 / (1.0 + np.exp(-zf))
+    under = p < BCE_LO
+    p1 = np.where(under, BCE_LO, p)
+    over = p1 > BCE_HI
+    p2 = np.where(over, BCE_HI, p1)
+    yn = 1.0 - y
+    pn = 1.0 - p2
+    s = y * np.log(p2) + yn * np.log(pn)
+    loss = float(np.cumsum(s)[-1]) * (-1.0 / n)
+    g = np.full(n, -1.0 / n)
+    p2bar = -((g * yn) / pn) + (g * y) / p2
+    pbar = np.where(under | over, 0.0, p2bar)
+    dz = pbar * (p * (1.0 - p))
+    return loss, dz.reshape(n, 1)
+
+
+LOSS_FNS = {"softmax_xent": softmax_xent, "mse": mse, "bce": bce}
+
+
 def mlp_step(params, X, Y, acts, loss="softmax_xent", lr=0.05, mode="blas"):
     """One training step of a Dense chain: forward, loss, pullback, SGD.
 
@@ -162,7 +195,7 @@ def mlp_step(params, X, Y, acts, loss="softmax_xent", lr=0.05, mode="blas"):
         zb, h = dense_forward(hs[-1], W, b, act, mode)
         zs.append(zb)
         hs.append(h)
-    lv, gbar = (softmax_xent if loss == "softmax_xent" else mse)(hs[-1], Y)
+    lv, gbar = LOSS_FNS[loss](hs[-1], Y)
     grads = [None] * len(params)
     for l in range(len(params) - 1, -1, -1):
         W, b = params[l]

@@ -206,6 +206,18 @@ __global__ void k_colsum_strict(const T* x, long long ld, long long M, long long
   out[j] = acc;
 }
 
+// --- per-32-row column sums of x (bias-gradient stage 1 when no producer fused it)
+template <class T>
+__global__ void __launch_bounds__(256) k_colsum_part(const T* x, long long ld, long long M, long long N, float* part,
+                                                     long long ldp) {
+  const long long c = blockIdx.x * 256ll + threadIdx.x;
+  if (c >= N) return;
+  const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
+  float acc = 0.0f;
+  for (long long r = r0; r < r1; ++r) acc += (float)x[r * ld + c];
+  part[g * ldp + c] = acc;
+}
+
 // --- losses.  Per-block loss partial sums (fixed order) -> loss_part[block]
 // MSE: loss = sum((z-y)^2) * scale; dz = d*scale + d*scale (rules.py:53-58 on mul(d,d))
 template <class T>
@@ -239,6 +251,56 @@ __global__ void __launch_bounds__(256) k_mse(const T* z, long long ldz, const T*
     __syncthreads();
   }
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+}
+
+// clamped binary cross-entropy on logits (nn_train.py:209-227):
+//   p = sigmoid(z); p2 = clamp(p, lo, hi) via lt/select + gt/select;
+//   loss = -scale * sum(y log p2 + (1-y) log(1-p2));
+//   dz = [p kept] * (-(g(1-y))/(1-p2) + (g y)/p2) * (p (1-p)),  g = -scale
+// (pullback order: rules.py mul/log/sub, select passes only kept entries, sigmoid).
+// Evaluated in f64 whatever the logit dtype: the clamp bounds 1e-7 / 1-1e-7
+// are not representable in f32 (1-1e-7 rounds to 1-2^-23, and log(1-p)
+// of a saturated prediction would move by 0.18), and the head is one column.
+template <class T>
+__global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T* y, long long ldy, long long M,
+                                             long long N, T scale, void* dz, int dzd, long long lddz, void* dz2,
+                                             int dz2d, long long lddz2, float* colsum, long long ldc,
+                                             double* loss_part) {
+  __shared__ double red[256];
+  const long long c = blockIdx.x * 32ll + threadIdx.x;
+  const long long g = blockIdx.y * 8ll + threadIdx.y;
+  const long long r0 = g * 32;
+  const double lo = 1e-7, hi = 1.0 - 1e-7, one = 1.0;
+  double lsum = 0.0;
+  if (r0 < M && c < N) {
+    double acc = 0.0;
+    const long long r1 = r0 + 32 < M ? r0 + 32 : M;
+    for (long long r = r0; r < r1; ++r) {
+      const double zz = (double)z[r * ldz + c], yy = (double)y[r * ldy + c];
+      const double p = one / (one + exp(-zz));
+      const bool under = p < lo;
+      const double p1 = under ? lo : p;
+      const bool over = p1 > hi;
+      const double p2 = over ? hi : p1;
+      const double yn = one - yy, pn = one - p2;
+      lsum += yy * log(p2) + yn * log(pn);
+      const double gs = -(double)scale;
+      const double pbar = (under || over) ? 0.0 : -((gs * yn) / pn) + (gs * yy) / p2;
+      const double v = pbar * (p * (one - p));
+      st_as(dz, dzd, r * lddz + c, v);
+      if (dz2) st_as(dz2, dz2d, r * lddz2 + c, v);
+      acc += v;
+    }
+    if (colsum) colsum[g * ldc + c] = (float)acc;
+  }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  red[tid] = lsum;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s) red[tid] += red[tid + s];
+    __syncthreads();
+  }
+  if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * -(double)scale;
 }
 
 // softmax cross-entropy, warp per row (N <= 1024):
@@ -380,6 +442,23 @@ inline unsigned cap_grid(long long n, int block, long long cap) {
 inline bool fdt(int d) { return d == SG_F32 || d == SG_F64; }
 }  // namespace
 
+namespace sg {
+// stage 1 of a bias gradient for an already materialised dZ (bf16 / f32)
+int colsum_partials(const void* x, int dtype, long long ld, long long M, long long N, float* part, long long ldp,
+                    cudaStream_t st) {
+  const dim3 grid((unsigned)((N + 255) / 256), (unsigned)((M + 31) / 32));
+  if (grid.y > 65535) return fail(SG_EINVAL, "colsum: M too large");
+  if (dtype == SG_BF16)
+    dk::k_colsum_part<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, ld, M, N, part, ldp);
+  else if (dtype == SG_F32)
+    dk::k_colsum_part<float><<<grid, 256, 0, st>>>((const float*)x, ld, M, N, part, ldp);
+  else
+    return fail(SG_EINVAL, "colsum: bf16/f32 only");
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+}  // namespace sg
+
 extern "C" {
 
 int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y, const void* h, int32_t h_dtype,
@@ -484,6 +563,19 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
                                                        ld_colsum, loss_part);
     else
       dk::k_mse<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
+                                                      (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
+                                                      colsum, ld_colsum, loss_part);
+  } else if (kind == SG_LOSS_BCE) {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
+    if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
+    blocks = (long long)grid.x * grid.y;
+    if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
+    if (dtype == SG_F64)
+      dk::k_bce<double><<<grid, dim3(32, 8), 0, st>>>((const double*)z, ld_z, (const double*)y, ld_y, M, N,
+                                                       scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
+                                                       ld_colsum, loss_part);
+    else
+      dk::k_bce<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
                                                       (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
                                                       colsum, ld_colsum, loss_part);
   } else if (kind == SG_LOSS_SOFTMAX_XENT) {

@@ -36,10 +36,10 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import runtime as rt
-from .gemm import ACT, gemm
+from .gemm import ACT
 from .tape import Tape, TapeEntry
 
-LOSSES = {"softmax_xent": 0, "mse": 1}
+LOSSES = {"softmax_xent": 0, "mse": 1, "bce": 2}
 
 
 def _ld(d: int) -> int:
@@ -90,6 +90,28 @@ class Chain:
 
 
 # ---------------------------------------------------------------- C binding
+class DenseDesc(ctypes.Structure):  # sg_dense_desc
+    _fields_ = [
+        ("batch", ctypes.c_int64), ("fan_in", ctypes.c_int64), ("fan_out", ctypes.c_int64),
+        ("precision", ctypes.c_int32), ("act", ctypes.c_int32),
+        ("X", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+        ("W", ctypes.c_void_p), ("ldw", ctypes.c_int64),
+        ("b", ctypes.c_void_p),
+    ]
+
+
+class DenseGrad(ctypes.Structure):  # sg_dense_grad
+    _fields_ = [
+        ("dZ", ctypes.c_void_p), ("ld_dz", ctypes.c_int64),
+        ("colsum_in", ctypes.c_void_p), ("ld_colsum_in", ctypes.c_int64),
+        ("act_prev", ctypes.c_int32),
+        ("dX", ctypes.c_void_p), ("ld_dx", ctypes.c_int64), ("dx_dtype", ctypes.c_int32),
+        ("colsum_out", ctypes.c_void_p), ("ld_colsum_out", ctypes.c_int64),
+        ("dW", ctypes.c_void_p), ("ld_dw", ctypes.c_int64),
+        ("db", ctypes.c_void_p),
+    ]
+
+
 _bound = False
 
 
@@ -106,7 +128,10 @@ def _lib():
                                 I64, P, I64, P]
         lib.sg_sgd.argtypes = [P, P, P, I32, I64, D, P, P]
         lib.sg_cast.argtypes = [P, P, I32, P, I32, I64, P]
-        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast"):
+        lib.sg_dense_forward.argtypes = [P, ctypes.POINTER(DenseDesc), P, I64, P, I64, P, I64, P]
+        lib.sg_dense_backward.argtypes = [P, ctypes.POINTER(DenseDesc), ctypes.POINTER(DenseGrad), P]
+        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast",
+                  "sg_dense_forward", "sg_dense_backward"):
             getattr(lib, n).restype = ctypes.c_int
         _bound = True
     return lib
@@ -118,6 +143,48 @@ def _p(t):
 
 def _dt(t):
     return rt.dtype_code(t.dtype)
+
+
+def _ldt(t):
+    return 0 if t is None else t.stride(0)
+
+
+def dense_desc(X, W, b, act: str, precision: str) -> DenseDesc:
+    """sg_dense_desc of one layer: X [batch][fan_in], W [fan_out][fan_in] (the
+    precision's operand dtype), b [fan_out]."""
+    from .gemm import PREC
+
+    d = DenseDesc()
+    d.batch, d.fan_in = X.shape
+    d.fan_out = W.shape[0]
+    d.precision, d.act = PREC[precision], ACT[act]
+    d.X, d.ldx = _p(X), _ldt(X)
+    d.W, d.ldw = _p(W), _ldt(W)
+    d.b = _p(b)
+    return d
+
+
+def dense_forward(desc: DenseDesc, H=None, H_f32=None, Z=None, stream=None) -> None:
+    """sg_dense_forward: H = act(X W^T + b) (nn_train.py:189-196) in one GEMM."""
+    rt.check(_lib().sg_dense_forward(rt.context(), ctypes.byref(desc), _p(H), _ldt(H), _p(H_f32), _ldt(H_f32),
+                                     _p(Z), _ldt(Z), rt.stream_ptr(stream)), "sg_dense_forward")
+
+
+def dense_backward(desc: DenseDesc, dZ, dW, db, dX=None, act_prev: str = "identity", colsum_in=None,
+                   colsum_out=None, stream=None) -> None:
+    """sg_dense_backward: dW = dZ^T X, db = colsum(dZ), dX = dZ W [.* act_prev'(X)]
+    (rules.py:45-46, 82-94, 113-124)."""
+    g = DenseGrad()
+    g.dZ, g.ld_dz = _p(dZ), _ldt(dZ)
+    g.colsum_in, g.ld_colsum_in = _p(colsum_in), _ldt(colsum_in)
+    g.act_prev = ACT[act_prev]
+    g.dX, g.ld_dx = _p(dX), _ldt(dX)
+    g.dx_dtype = _dt(dX) if dX is not None else 0
+    g.colsum_out, g.ld_colsum_out = _p(colsum_out), _ldt(colsum_out)
+    g.dW, g.ld_dw = _p(dW), _ldt(dW)
+    g.db = _p(db)
+    rt.check(_lib().sg_dense_backward(rt.context(), ctypes.byref(desc), ctypes.byref(g), rt.stream_ptr(stream)),
+             "sg_dense_backward")
 
 
 class DenseLayer:
@@ -168,11 +235,11 @@ class DenseLayer:
     def forward(self, X=None):
         if X is not None:
             self.X.copy_(X, non_blocking=True)
-        if self.precision == "tf32":
-            gemm(self.X, self.W, precision="tf32", epilogue="bias_act", act=self.act, bias=self.b, out=self.H)
-        else:
-            gemm(self.X, self.Wb, epilogue="bias_act", act=self.act, bias=self.b, out_lp=self.H)
+        dense_forward(self.desc(), H=self.H)
         return self.H
+
+    def desc(self) -> DenseDesc:
+        return dense_desc(self.X, self.Wb, self.b, self.act, self.precision)
 
     def pullback(self, ybar, need_dx: bool = True):
         lib = _lib()
@@ -181,12 +248,8 @@ class DenseLayer:
                                  self.H.stride(0), self.M, self.N, ACT[self.act], _p(self.dZ), _dt(self.dZ),
                                  self.dZ.stride(0), None, 0, 0, _p(self.colsum), self.colsum.stride(0), st),
                  "sg_act_grad")
-        p = self.precision
-        if need_dx:
-            gemm(self.dZ, self.W if p == "tf32" else self.Wb, b_mn=True, precision=p, out=self.dX)
-        gemm(self.dZ, self.X, a_mn=True, b_mn=True, precision=p, out=self.dW)
-        rt.check(lib.sg_colsum_finalize(ctx, _p(self.colsum), (self.M + 31) // 32, self.colsum.stride(0),
-                                        self.N, _p(self.db), st), "sg_colsum_finalize")
+        dense_backward(self.desc(), self.dZ, self.dW, self.db, dX=self.dX if need_dx else None,
+                       colsum_in=self.colsum)
         return self.dX, self.dW, self.db
 
     def flops(self, need_dx: bool = True) -> float:
@@ -260,6 +323,8 @@ class ChainEngine:
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         n_part = max(1, ((dmax + 31) // 32) * ((B + 31) // 32))
         self.loss_part = torch.zeros(n_part, dtype=torch.float64, device=dev)
+        self.descs = [dense_desc(self.H[l], self.Ws[l] if precision == "bf16" else self.W[l], self.b[l],
+                                 self.acts[l], precision) for l in range(self.L)]
         self.tape = Tape()
         self.grad_ready = None  # optional callback(layer_index) when layer l's gradients are written
         if chain.layers[0].W is not None:
@@ -297,16 +362,10 @@ class ChainEngine:
         L = self.L
         for l in range(L):
             last = l == L - 1
-            Wop = self.Ws[l] if self.precision == "bf16" else self.W[l]
             if self.precision == "bf16":
-                gemm(self.H[l], Wop, epilogue="bias_act", act=self.acts[l], bias=self.b[l],
-                     out_lp=None if last else self.H[l + 1], out=self.Zt if last else None)
-            elif self.precision == "tf32":
-                gemm(self.H[l], Wop, precision="tf32", epilogue="bias_act", act=self.acts[l], bias=self.b[l],
-                     out=self.Zt if last else self.H[l + 1])
+                dense_forward(self.descs[l], H=None if last else self.H[l + 1], H_f32=self.Zt if last else None)
             else:
-                gemm(self.H[l], Wop, precision=self.gprec, epilogue="bias_act", act=self.acts[l],
-                     bias=self.b[l], out=self.Zt if last else self.H[l + 1])
+                dense_forward(self.descs[l], H=self.Zt if last else self.H[l + 1])
             self.tape.push(TapeEntry(f"dense{l}", (self.H[l], self.W[l]),
                                      self._make_backward(l), self._ready(l)))
         return self.Zt
@@ -345,34 +404,15 @@ class ChainEngine:
     # ----------------------------------------------------------- pullback
     def _make_backward(self, l):
         def backward(_ctx):
-            lib = _lib()
-            ctx, st = rt.context(), rt.stream_ptr()
             d_out, d_in = self.sizes[l + 1], self.sizes[l]
             dz = self.dZ[l % 2][:, :d_out]
-            strict = not self.tc
-            # dW = dZ^T . H[l]   (rules.py:113-115 second cotangent, then _transpose)
-            gemm(dz, self.H[l], a_mn=True, b_mn=True, precision=self.gprec, out=self.gW[l])
-            # db = reduce_like(dZ, (out,))   (rules.py:45-46)
-            if strict:
-                rt.check(lib.sg_colsum_strict(ctx, _p(dz), _dt(dz), dz.stride(0), self.B, d_out,
-                                              _p(self.gb[l]), st), "sg_colsum_strict")
-            else:
-                rt.check(lib.sg_colsum_finalize(ctx, _p(self.colsum), (self.B + 31) // 32,
-                                                self.colsum.stride(0), d_out, _p(self.gb[l]), st),
-                         "sg_colsum_finalize")
-            if l > 0:
-                # dH[l] = dZ . W, fused with act' of the layer below -> dZ[l-1]
-                dzn = self.dZ[(l - 1) % 2][:, :d_in]
-                Wop = self.Ws[l] if self.precision == "bf16" else self.W[l]
-                if strict:
-                    gemm(dz, Wop, b_mn=True, precision=self.gprec, epilogue="act_grad",
-                         act=self.acts[l - 1], aux=self.H[l], out=dzn)
-                elif self.precision == "tf32":
-                    gemm(dz, Wop, b_mn=True, precision="tf32", epilogue="act_grad", act=self.acts[l - 1],
-                         aux=self.H[l], out=dzn, colsum=self.colsum)
-                else:
-                    gemm(dz, Wop, b_mn=True, epilogue="act_grad", act=self.acts[l - 1], aux=self.H[l],
-                         out_lp=dzn, colsum=self.colsum)
+            cs = self.colsum if self.tc else None
+            # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
+            # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below
+            dense_backward(self.descs[l], dz, self.gW[l], self.gb[l],
+                           dX=self.dZ[(l - 1) % 2][:, :d_in] if l > 0 else None,
+                           act_prev=self.acts[l - 1] if l > 0 else "identity",
+                           colsum_in=cs, colsum_out=cs if l > 0 else None)
         return backward
 
     def pullback(self):

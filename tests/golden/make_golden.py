@@ -33,6 +33,7 @@ from ssagrad.forward_ad import fused_map_pullback, fused_map_with_partials  # no
 from ssagrad.interp import EvalError  # noqa: E402
 from ssagrad.ir import F64, tensor_type  # noqa: E402
 from ssagrad.structure import SEmitter, flatten  # noqa: E402
+from ssagrad import nn_train  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
@@ -170,7 +171,7 @@ def build_chain_loss(module, name, sizes, acts, n, loss):
         b = em.param(f"b{k}", tensor_type(sizes[k + 1]))
         pairs.append((w, b))
     x = em.param("X", tensor_type(n, sizes[0]))
-    y = em.param("Y", tensor_type(n, sizes[-1]))
+    y = em.param("Y", tensor_type(n) if loss == "bce" else tensor_type(n, sizes[-1]))
     h = x
     for (w, b), act in zip(pairs, acts):  # nn_train.py:189-196
         wt = em.emit("transpose", (w,), None, "wt")
@@ -191,6 +192,15 @@ def build_chain_loss(module, name, sizes, acts, n, loss):
         sq = em.emit("mul", (d, d), None, "sq")
         tot = em.emit("reduce_sum", (sq,), {"axis": "all"}, "tot")
         sc = em.const_f64(1.0 / n, "sc")
+    elif loss == "bce":  # one-logit head + clamped mean BCE, emitted by the reference itself
+        flatz = em.emit("reshape", (h,), {"shape": (n,)}, "logit")  # _batch_head, nn_train.py:209-210
+        p = em.emit("sigmoid", (flatz,), None, "hat")
+        lob = em.emit("bcast", (em.const_f64(1e-7, "lo"),), {"shape": (n,)}, "lob")
+        hib = em.emit("bcast", (em.const_f64(1.0 - 1e-7, "hi"),), {"shape": (n,)}, "hib")
+        ones = em.emit("bcast", (em.const_f64(1.0, "one"),), {"shape": (n,)}, "ones")
+        l = nn_train._bce_mean(em, p, y, n, lob, hib, ones, "c")  # nn_train.py:213-227
+        module.add(flatten(em.finish((l,))))
+        return
     else:  # "dot": loss = sum(h * Y), i.e. pull back the seed Y through the chain
         t = em.emit("mul", (h, y), None, "t")
         tot = em.emit("reduce_sum", (t,), {"axis": "all"}, "tot")
@@ -199,7 +209,7 @@ def build_chain_loss(module, name, sizes, acts, n, loss):
     module.add(flatten(em.finish((l,))))
 
 
-def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot"):
+def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot", last_scale=1.0):
     rng = np.random.default_rng(seed)
     module = Module()
     build_chain_loss(module, "chain", sizes, acts, n, loss)
@@ -207,11 +217,13 @@ def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot"):
     for k in range(len(sizes) - 1):
         fi, fo = sizes[k], sizes[k + 1]
         r = np.sqrt(6.0 / (fi + fo))  # init_params, nn_train.py:130-140
-        W = f32(rng.uniform(-r, r, (fo, fi)))
+        W = f32(rng.uniform(-r, r, (fo, fi)) * (last_scale if k == len(sizes) - 2 else 1.0))
         b = f32(rng.uniform(-0.1, 0.1, fo))
         params.append((W, b))
     X = f32(rng.uniform(0, 1, (n, sizes[0])))
-    if y_kind == "onehot":
+    if y_kind == "binary":
+        Y = rng.integers(0, 2, n).astype(np.float64)
+    elif y_kind == "onehot":
         Y = np.zeros((n, sizes[-1]))
         Y[np.arange(n), rng.integers(0, sizes[-1], n)] = 1.0
     else:
@@ -224,7 +236,7 @@ def chain_case(sizes, acts, n, loss, seed, lr=0.05, y_kind="onehot"):
     g = grad(module, "chain", tuple(args))
     fn = module.get("chain")
     # inputs are float32-representable: store them as float32 (exact)
-    out = {"X": X.astype(np.float32), "Y": Y.astype(np.float32), "loss": np.array([loss_v]),
+    out = {"X": X.astype(np.float32), "Y": Y.reshape(n, -1).astype(np.float32), "loss": np.array([loss_v]),
            "sizes": np.array(sizes), "lr": np.array([lr])}
     for k, (W, b) in enumerate(params):
         out[f"W{k}"], out[f"b{k}"] = W.astype(np.float32), b.astype(np.float32)
@@ -337,6 +349,14 @@ def dan_train_case():
     }
 
 
+def save_bce():
+    # binary classifier with the DAN head/loss recipe; large first-layer weights
+    # push some predictions into the clamp range (select gradients = 0)
+    np.savez_compressed(os.path.join(HERE, "mlp_bce.npz"),
+                        **chain_case((12, 16, 1), ("tanh", "identity"), 48, "bce", 4, y_kind="binary",
+                                     last_scale=24.0))
+
+
 def main():
     with open(os.path.join(HERE, "fused.json"), "w") as f:
         json.dump(fused_cases(), f, indent=0)
@@ -352,6 +372,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "mlp_mse.npz"),
                         **chain_case((24, 24, 24, 24), ("tanh", "tanh", "identity"), 16, "mse", 2,
                                      y_kind="uniform"))
+    save_bce()
     np.savez_compressed(os.path.join(HERE, "dense_sigmoid.npz"),
                         **chain_case((40, 24), ("sigmoid",), 16, "dot", 3, y_kind="uniform"))
     print("golden fixtures written to", HERE)

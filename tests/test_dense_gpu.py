@@ -45,6 +45,7 @@ def chain_from(z, acts):
 @pytest.mark.parametrize("name,acts,loss", [
     ("mlp_c1_b32.npz", ("sigmoid", "identity"), "softmax_xent"),
     ("mlp_mse.npz", ("tanh", "tanh", "identity"), "mse"),
+    ("mlp_bce.npz", ("tanh", "identity"), "bce"),  # 19 of 48 predictions clamped
 ])
 def test_chain_gradients_match_reference(precision, name, acts, loss):
     z = load_npz(name)
@@ -208,3 +209,36 @@ def test_data_parallel_shards_sum_to_full_gradient():
         e.forward(); e.loss_and_seed(); e.pullback()
         acc += e.G
     assert nrel(acc.cpu().numpy(), full.G.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32", "strict_fp32"])
+def test_dense_abi_backward_without_fused_partials(precision):
+    """sg_dense_backward computing db itself (no producer-fused colsum), with
+    the lower layer's act' fused into dX, vs a float64 restatement."""
+    from paper_1811_01457_b200.dense import dense_backward, dense_desc, dense_forward
+
+    rng = np.random.default_rng(5)
+    B, fi, fo = 200, 72, 136
+    dt = torch.bfloat16 if precision == "bf16" else torch.float32
+    X = torch.from_numpy(rng.uniform(0.05, 0.95, (B, fi)).astype(np.float32)).to(dt).cuda()
+    W = torch.from_numpy(rng.uniform(-0.3, 0.3, (fo, fi)).astype(np.float32)).to(dt).cuda()
+    b = torch.from_numpy(rng.uniform(-0.1, 0.1, fo).astype(np.float32)).cuda()
+    dZ = torch.from_numpy(rng.uniform(-1, 1, (B, fo)).astype(np.float32)).to(dt).cuda()
+    d = dense_desc(X, W, b, "tanh", precision)
+    H = torch.empty((B, fo), dtype=dt, device="cuda")
+    dense_forward(d, H=H)
+    dW = torch.empty((fo, fi), device="cuda")
+    db = torch.empty(fo, device="cuda")
+    dX = torch.empty((B, fi), dtype=dt, device="cuda")
+    dense_backward(d, dZ, dW, db, dX=dX, act_prev="sigmoid")
+    torch.cuda.synchronize()
+    x, w, z = (t.double().cpu().numpy() for t in (X, W, dZ))
+    tol = {"bf16": 1e-2, "tf32": 3e-3, "strict_fp32": 1e-5}[precision]
+    assert nrel(H.double().cpu(), np.tanh(x @ w.T + b.double().cpu().numpy())) <= tol
+    assert nrel(dW.double().cpu(), z.T @ x) <= tol
+    assert nrel(db.double().cpu(), z.sum(axis=0)) <= 1e-5
+    assert nrel(dX.double().cpu(), (z @ w) * x * (1 - x)) <= tol
+    if precision == "strict_fp32":  # partial column sums are a tensor-core feature
+        cs = torch.zeros(((B + 31) // 32, fo), device="cuda")
+        with pytest.raises(ValueError, match="tensor-core"):
+            dense_backward(d, dZ, dW, db, colsum_in=cs)

@@ -93,6 +93,7 @@ def test_reduce_to_matches_reference():
 @pytest.mark.parametrize("name,acts,loss", [
     ("mlp_c1_b32.npz", ("sigmoid", "identity"), "softmax_xent"),
     ("mlp_mse.npz", ("tanh", "tanh", "identity"), "mse"),
+    ("mlp_bce.npz", ("tanh", "identity"), "bce"),
 ])
 def test_mlp_step_matches_reference(name, acts, loss):
     z = load_npz(name)
