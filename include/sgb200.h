@@ -13,7 +13,7 @@
  *   SG_EDOMAIN       1  DomainError / EvalError   (tensor.py:25-26, interp.py:26-35)
  *   SG_EINVAL        2  ValueError (shapes, arguments)    (tensor.py:118-119, 358-359)
  *   SG_ECUDA         3  CUDA / NVRTC failure
- *   SG_ENCCL         4  collective failure (reserved; DP uses torch.distributed/NCCL)
+ *   SG_ENCCL         4  collective (NCCL) failure
  * sg_last_error() returns the message of the last failing call on this thread.
  */
 #ifndef SGB200_H
@@ -253,6 +253,24 @@ typedef struct sg_dense_grad {
 
 /* dW = dZ^T X, db = colsum(dZ), dX = dZ W [.* act_prev'(X)]; in that order. */
 SG_API int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* g, void* stream);
+
+/* ------------------------------------------- data parallelism (NCCL)
+ * minibatch rows sharded over ranks (one process per GPU),
+ * losses scaled by the global 1/B, and the flat gradient buffer (order
+ * [W0, b0, W1, b1, ...], nn_train.py:99-103) all-reduced (SUM) in per-layer
+ * buckets.  The communicator owns a comm stream: sg_dp_allreduce forks from
+ * the caller's stream (event), reduces on the comm stream, and sg_dp_wait
+ * joins it back -- stream-ordered and CUDA-graph capturable.  NCCL is
+ * resolved at run time (dlopen libnccl.so.2); sg_dp_available() says
+ * whether it was found.  The 128-byte unique id from rank 0's
+ * sg_dp_unique_id reaches the other ranks over the host's rendezvous. */
+typedef struct sg_dp sg_dp;
+SG_API int sg_dp_available(void);
+SG_API int sg_dp_unique_id(uint8_t* out, size_t n);
+SG_API int sg_dp_init(sg_ctx* ctx, const uint8_t* unique_id, size_t n, int rank, int world, sg_dp** out);
+SG_API int sg_dp_allreduce(sg_dp* dp, void* buf, int64_t n, int32_t dtype, void* stream);
+SG_API int sg_dp_wait(sg_dp* dp, void* stream);
+SG_API int sg_dp_finalize(sg_dp* dp);
 
 /* out = reduce_to(a .* b, out_shape); b may be NULL.  The contraction of
  * `fused_map_pullback` (forward_ad.py:232-235) and `reduce_to`

@@ -13,6 +13,8 @@ that layer's dW/db are enqueued, so they overlap the rest of the pullback.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from .dense import Chain, ChainEngine
@@ -53,16 +55,91 @@ class DataParallel:
         self.dist.broadcast(P, src=src, group=self.group)
 
 
+class NcclDataParallel:
+    """The same bucketed all-reduce through the library's own NCCL
+    communicator (``sg_dp_*``, include/sgb200.h): each bucket forks from the
+    compute stream onto the communicator's stream and ``finish`` joins it
+    back, all stream-ordered -- so a data-parallel step, collectives
+    included, can be captured in one CUDA graph.  ``torch.distributed`` is
+    only the rendezvous (the 128-byte NCCL id from rank 0) and the one-time
+    parameter broadcast.
+    """
+
+    def __init__(self, G, buckets, group=None):
+        import torch.distributed as dist
+
+        from . import runtime as rt
+
+        self.dist, self.rt = dist, rt
+        self.G = G
+        self.buckets = list(buckets)
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        lib = rt.load_library()
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        U8 = ctypes.POINTER(ctypes.c_uint8)
+        lib.sg_dp_unique_id.argtypes = [U8, SZ]
+        lib.sg_dp_init.argtypes = [P, U8, SZ, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
+        lib.sg_dp_allreduce.argtypes = [P, P, I64, I32, P]
+        lib.sg_dp_wait.argtypes = [P, P]
+        lib.sg_dp_finalize.argtypes = [P]
+        self.lib = lib
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            rt.check(lib.sg_dp_unique_id(uid, 128), "sg_dp_unique_id")
+        box = [bytes(uid)]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(box, src=src, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        h = ctypes.c_void_p()
+        rt.check(lib.sg_dp_init(rt.context(), uid, 128, self.rank, self.world, ctypes.byref(h)), "sg_dp_init")
+        self.handle = h
+        self.dtype = rt.dtype_code(G.dtype)
+
+    def ready(self, i: int) -> None:
+        lo, hi = self.buckets[i]
+        self.rt.check(self.lib.sg_dp_allreduce(self.handle, self.G[lo:hi].data_ptr(), hi - lo, self.dtype,
+                                               self.rt.stream_ptr()), "sg_dp_allreduce")
+
+    def finish(self) -> None:
+        self.rt.check(self.lib.sg_dp_wait(self.handle, self.rt.stream_ptr()), "sg_dp_wait")
+
+    def broadcast_params(self, P, src: int = 0) -> None:
+        self.dist.broadcast(P, src=src, group=self.group)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.sg_dp_finalize(self.handle)
+            self.handle = None
+
+
+def _default_dp_backend(group) -> str:
+    import torch.distributed as dist
+
+    from . import runtime as rt
+
+    if dist.get_backend(group) != "nccl":
+        return "torch"
+    try:
+        return "sg" if rt.load_library().sg_dp_available() else "torch"
+    except rt.RuntimeUnavailable:
+        return "torch"
+
+
 class Trainer:
     """Dense-chain training on one GPU, optionally data-parallel over a process group.
 
     ``batch`` is the GLOBAL minibatch; with ``dp`` each rank holds
     ``batch / world`` rows (weak per-rank work shrinks, strong scaling of
-    the global step).
+    the global step).  ``dp_backend``: "sg" (the library's NCCL
+    communicator, default under an NCCL process group; CUDA-graph capturable)
+    or "torch" (``torch.distributed`` async all-reduce; the gloo CPU path).
     """
 
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", lr: float = 0.05,
-                 precision: str = "bf16", dp: bool = False, group=None, graph: bool = False):
+                 precision: str = "bf16", dp: bool = False, group=None, graph: bool = False,
+                 dp_backend: str | None = None):
         self.lr = float(lr)
         self.world = 1
         if dp:
@@ -75,13 +152,19 @@ class Trainer:
         self.engine = ChainEngine(chain, self.local_batch, loss, precision, global_batch=batch)
         self.dp = None
         if dp:
-            self.dp = DataParallel(self.engine.G, self.engine.bucket_bounds, group)
+            backend = dp_backend or _default_dp_backend(group)
+            if backend not in ("sg", "torch"):
+                raise ValueError(f"unknown dp backend {backend!r}")
+            cls = NcclDataParallel if backend == "sg" else DataParallel
+            self.dp = cls(self.engine.G, self.engine.bucket_bounds, group)
             self.engine.grad_ready = self.dp.ready
             self.dp.broadcast_params(self.engine.P)
             if self.engine.S is not None:
                 self.engine.S.copy_(self.engine.P.to(self.engine.S.dtype))
         self.graph = None
-        self.use_graph = graph and self.dp is None
+        # torch.distributed's async work handles are host-side objects; the
+        # library's communicator is stream-ordered and can live in a graph
+        self.use_graph = graph and (self.dp is None or isinstance(self.dp, NcclDataParallel))
         self._eager_steps = 0
 
     def _device_step(self):

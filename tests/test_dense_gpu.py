@@ -153,7 +153,9 @@ def test_cuda_graph_replay_matches_eager_and_is_deterministic():
 def test_data_parallel_trainer_over_nccl_world1():
     """The DP code path (NCCL process group, bucketed async all-reduce issued
     from inside the pullback, broadcast of initial params) on the one GPU a
-    box has: with world size 1 it must reproduce the single-GPU step."""
+    box has: with world size 1 it must reproduce the single-GPU step -- for
+    both all-reduce backends (torch.distributed, and the library's own NCCL
+    communicator sg_dp_*, eager and captured in a CUDA graph)."""
     import os
     import socket
 
@@ -172,17 +174,27 @@ def test_data_parallel_trainer_over_nccl_world1():
         X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
         Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
 
-        def run(dp):
+        from paper_1811_01457_b200.train import NcclDataParallel
+
+        def run(dp, backend=None, graph=False):
             chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(2)]).init_params(
                 np.random.default_rng(9))
-            tr = Trainer(chain, B, loss="mse", lr=0.002, precision="bf16", dp=dp)
+            tr = Trainer(chain, B, loss="mse", lr=0.002, precision="bf16", dp=dp, dp_backend=backend,
+                         graph=graph)
+            if backend == "sg":
+                assert isinstance(tr.dp, NcclDataParallel)
+                assert tr.use_graph == graph
             losses = [float(tr.step(X, Y).item()) for _ in range(3)]
+            if tr.dp is not None and hasattr(tr.dp, "close"):
+                torch.cuda.synchronize()
+                tr.dp.close()
             return losses, tr.engine.P.clone()
 
         l0, p0 = run(False)
-        l1, p1 = run(True)
-        assert l0 == l1
-        assert torch.equal(p0, p1)
+        for backend, graph in (("torch", False), ("sg", False), ("sg", True)):
+            l1, p1 = run(True, backend, graph)
+            assert l0 == l1, backend
+            assert torch.equal(p0, p1), backend
     finally:
         dist.destroy_process_group()
 
