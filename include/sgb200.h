@@ -166,6 +166,12 @@ typedef struct sg_gemm_desc {
    * (BF16 precision): the bias gradient's first reduction stage, see sg_colsum_finalize */
   float* colsum;
   int64_t ld_colsum;
+  /* batched GEMM (the reference's bmm, tensor.py:364-369, one per lane):
+   * batch >= 1 independent problems, operands/outputs `stride_*` elements
+   * apart (out_lp uses stride_lp).  batch 0 is treated as 1.  Batched calls
+   * take the STORE / BIAS_ACT epilogues (bias shared) without colsum/out_pre. */
+  int64_t batch;
+  int64_t stride_a, stride_b, stride_out, stride_lp;
 } sg_gemm_desc;
 
 SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);

@@ -52,6 +52,9 @@ struct GemmArgs {
   long long ldb;
   bool b_mn;  // B stored [K][N] instead of [N][K]
   GemmEpilogue epi;
+  int batch = 1;             // independent GEMMs (bmm lanes)
+  long long sa = 0, sb = 0;  // operand batch strides (elements)
+  long long so_f32 = 0, so_lp = 0;  // output batch strides (elements)
 };
 
 int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st);
@@ -73,6 +76,8 @@ struct StrictArgs {
   long long ld_pre;
   void* out;
   long long ld_out;
+  int batch = 1;  // blockIdx.z: independent GEMMs with these element strides
+  long long sa = 0, sb = 0, so = 0;
 };
 }  // namespace strict
 int launch_gemm_strict(const strict::StrictArgs& g, bool f64, cudaStream_t st);

@@ -20,6 +20,10 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
   if (d->epilogue < SG_EPI_STORE || d->epilogue > SG_EPI_ACT_GRAD) return fail(SG_EINVAL, "gemm: bad epilogue");
   if (d->act < SG_ACT_IDENTITY || d->act > SG_ACT_RELU) return fail(SG_EINVAL, "gemm: bad activation");
   if (d->epilogue == SG_EPI_ACT_GRAD && !d->aux) return fail(SG_EINVAL, "gemm: ACT_GRAD needs aux");
+  const long long batch = d->batch < 1 ? 1 : d->batch;
+  if (batch > 65535) return fail(SG_EINVAL, "gemm: at most 65535 batch entries");
+  if (batch > 1 && (d->stride_a < 0 || d->stride_b < 0 || d->stride_out < 0 || d->stride_lp < 0))
+    return fail(SG_EINVAL, "gemm: negative batch stride");
   int rc = ctx_activate(ctx);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -51,13 +55,19 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     g.epi.ld_bf16 = d->ld_lp;
     g.epi.colsum = d->colsum;
     g.epi.ld_colsum = d->ld_colsum;
+    g.batch = (int)batch;
+    g.sa = d->stride_a;
+    g.sb = d->stride_b;
+    g.so_f32 = d->stride_out;
+    g.so_lp = d->stride_lp;
     return launch_gemm_tc(g, tf32, ctx_num_sms(ctx), st);
   }
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
     if (d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
     strict::StrictArgs g{(int)d->M, (int)d->N, (int)d->K, d->A, d->lda, d->a_mn_major != 0,
                          d->B, d->ldb, d->b_mn_major != 0, d->epilogue, d->act, d->bias, d->aux,
-                         d->ld_aux, d->out_pre, d->ld_pre, d->out, d->ld_out};
+                         d->ld_aux, d->out_pre, d->ld_pre, d->out, d->ld_out, (int)batch, d->stride_a,
+                         d->stride_b, d->stride_out};
     return launch_gemm_strict(g, d->precision == SG_PREC_STRICT_FP64, st);
   }
   return fail(SG_EINVAL, "gemm: unknown precision");

@@ -46,8 +46,9 @@ template <class T>
 __global__ void __launch_bounds__(256) strict_gemm_kernel(const StrictArgs g) {
   __shared__ T As[TK][TM + 1];
   __shared__ T Bs[TK][TN + 1];
-  const T* A = reinterpret_cast<const T*>(g.A);
-  const T* B = reinterpret_cast<const T*>(g.B);
+  const long long bz = blockIdx.z;  // batch entry (bmm lane, tensor.py:364-369)
+  const T* A = reinterpret_cast<const T*>(g.A) + bz * g.sa;
+  const T* B = reinterpret_cast<const T*>(g.B) + bz * g.sb;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tid = threadIdx.x;
   const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(256) strict_gemm_kernel(const StrictArgs g) {
     }
     __syncthreads();
   }
-  T* out = reinterpret_cast<T*>(g.out);
+  T* out = g.out ? reinterpret_cast<T*>(g.out) + bz * g.so : nullptr;
   const T* bias = reinterpret_cast<const T*>(g.bias);
   const T* aux = reinterpret_cast<const T*>(g.aux);
   T* pre = reinterpret_cast<T*>(g.out_pre);
@@ -115,8 +116,10 @@ __global__ void __launch_bounds__(256) strict_gemm_kernel(const StrictArgs g) {
 }  // namespace strict
 
 int launch_gemm_strict(const strict::StrictArgs& g, bool f64, cudaStream_t st) {
-  dim3 grid((g.N + strict::TN - 1) / strict::TN, (g.M + strict::TM - 1) / strict::TM);
-  if (grid.y > 65535) return fail(SG_EINVAL, "strict GEMM: M too large");
+  dim3 grid((g.N + strict::TN - 1) / strict::TN, (g.M + strict::TM - 1) / strict::TM, g.batch);
+  if (grid.y > 65535 || g.batch > 65535 || g.batch < 1) return fail(SG_EINVAL, "strict GEMM: M or batch too large");
+  if (g.batch > 1 && (g.out_pre || g.mode == SG_EPI_ACT_GRAD))
+    return fail(SG_EINVAL, "strict GEMM: batched GEMMs take the STORE / BIAS_ACT epilogues without out_pre");
   if (f64)
     strict::strict_gemm_kernel<double><<<grid, 256, 0, st>>>(g);
   else

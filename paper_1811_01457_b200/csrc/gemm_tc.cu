@@ -96,11 +96,12 @@ __device__ __forceinline__ void fence_barrier_init() {
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+// Operand maps are 3-D {row, rows, batch}: c2 is the batch index (0 for a plain GEMM).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -240,6 +241,8 @@ struct KParams {
   float* part;        // [splits][M][ld_part] when splits > 1
   long long ld_part;
   int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
+  int batch;            // independent GEMMs (bmm lanes), >= 1
+  long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
 };
 
 // ----------------------------------------------------- TMA-store epilogue
@@ -249,10 +252,10 @@ struct KParams {
 // writes are fully coalesced and asynchronous.
 constexpr int STAGE_SLOT = 4096;
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -282,7 +285,7 @@ __device__ __forceinline__ void stage_f32(uint8_t* slot, const float (&v)[32], i
 // warp-collective: stage one chunk and bulk-store it at (n0, row0)
 template <bool BF16>
 __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap* map, const float (&v)[32], int lane,
-                                               int n0, int row0) {
+                                               int n0, int row0, int bidx) {
   if (lane == 0) bulk_wait_read0();  // the slot's previous store has been read out
   __syncwarp();
   if (BF16) stage_bf16(slot, v, lane);
@@ -290,7 +293,7 @@ __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap*
   fence_proxy_async();
   __syncwarp();
   if (lane == 0) {
-    tma_store_2d(map, slot, n0, row0);
+    tma_store_3d(map, slot, n0, row0, bidx);
     bulk_commit();
   }
 }
@@ -299,7 +302,7 @@ __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap*
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
-                                          bool grp_ok, int n0, int lane, int split, uint8_t* slot,
+                                          bool grp_ok, int n0, int lane, int split, int bidx, uint8_t* slot,
                                           const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -339,12 +342,12 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   }
   const int row0 = m - lane;
   if (e.out_f32) {
-    if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0);
-    else if (row_ok) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, v, nn);
+    if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx);
+    else if (row_ok) store_row_f32(e.out_f32 + bidx * p.so_f32 + (long long)m * e.ld_f32 + n0, v, nn);
   }
   if (e.out_bf16) {
-    if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0);
-    else if (row_ok) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, v, nn);
+    if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0, bidx);
+    else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
   }
   // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
   // transpose-reduce destroys v, so it runs after the stores
@@ -378,8 +381,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   const int lane = threadIdx.x % 32;
   const int m_tiles = (p.M + BM - 1) / BM;
   const int n_tiles = (p.N + BN - 1) / BN;
-  const int out_tiles = m_tiles * n_tiles;
-  const int tiles = out_tiles * p.splits;  // work items: (split, output tile)
+  const int tiles_pb = m_tiles * n_tiles;   // output tiles per batch entry
+  const int out_tiles = tiles_pb * p.batch;
+  const int tiles = out_tiles * p.splits;  // work items: (split, batch, output tile)
   const int num_kb_total = (p.K + BK - 1) / BK;
   // k-block range of work item t
   auto kb_range = [&](int t, int& kb0, int& kb1) {
@@ -420,7 +424,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const TileCoord tc = tile_of(t % out_tiles, m_tiles, n_tiles, BN);
+        const int u = t % out_tiles, bidx = u / tiles_pb;
+        const TileCoord tc = tile_of(u - bidx * tiles_pb, m_tiles, n_tiles, BN);
         int kb0, kb1;
         kb_range(t, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -431,15 +436,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / BK; ++j) tma_load_2d(sa + j * E::MN_CHUNK, &tma_a, &full_bar[stage], tc.m0 + BK * j, k0);
+            for (int j = 0; j < BM / BK; ++j)
+              tma_load_3d(sa + j * E::MN_CHUNK, &tma_a, &full_bar[stage], tc.m0 + BK * j, k0, bidx);
           } else {
-            tma_load_2d(sa, &tma_a, &full_bar[stage], k0, tc.m0);
+            tma_load_3d(sa, &tma_a, &full_bar[stage], k0, tc.m0, bidx);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / BK; ++j) tma_load_2d(sb + j * E::MN_CHUNK, &tma_b, &full_bar[stage], tc.n0 + BK * j, k0);
+            for (int j = 0; j < BN / BK; ++j)
+              tma_load_3d(sb + j * E::MN_CHUNK, &tma_b, &full_bar[stage], tc.n0 + BK * j, k0, bidx);
           } else {
-            tma_load_2d(sb, &tma_b, &full_bar[stage], k0, tc.n0);
+            tma_load_3d(sb, &tma_b, &full_bar[stage], k0, tc.n0, bidx);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -498,7 +505,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const TileCoord tc = tile_of(t % out_tiles, m_tiles, n_tiles, BN);
+      const int u = t % out_tiles, bidx = u / tiles_pb;
+      const TileCoord tc = tile_of(u - bidx * tiles_pb, m_tiles, n_tiles, BN);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int m = tc.m0 + q * 32 + lane;
@@ -509,7 +517,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
-        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles,
+        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles, bidx,
                   stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
       }
       tc_fence_before();
@@ -556,12 +564,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   // not the epilogue's global stores to be acknowledged
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
-                                                 int c1) {
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
+                                                 int c1, int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 template <bool TF32>
@@ -619,7 +627,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   const int lane = threadIdx.x % 32;
   const int m_tiles = (p.M + PM - 1) / PM;
   const int n_tiles = (p.N + BN - 1) / BN;
-  const int out_tiles = m_tiles * n_tiles;
+  const int tiles_pb = m_tiles * n_tiles;
+  const int out_tiles = tiles_pb * p.batch;
   const int tiles = out_tiles * p.splits;
   const int num_kb_total = (p.K + BK - 1) / BK;
   const int pair = blockIdx.x / 2, pairs = gridDim.x / 2;
@@ -630,7 +639,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   };
   auto coord = [&](int t) {
     constexpr int G = 8;  // grouped raster over 256-row pair tiles
-    const int u = t % out_tiles;
+    const int u = (t % out_tiles) % tiles_pb;
     const int per_group = G * n_tiles;
     const int group = u / per_group;
     const int first_m = group * G;
@@ -676,6 +685,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       uint32_t phase = 0;
       for (int t = pair; t < tiles; t += pairs) {
         const TileCoord tc = coord(t);
+        const int bidx = (t % out_tiles) / tiles_pb;
         const int am = tc.m0 + (int)rank * HALF, bn = tc.n0 + (int)rank * HALF;
         int kb0, kb1;
         kb_range(t, kb0, kb1);
@@ -688,15 +698,17 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / BK; ++j) tma_load_2d_pair(sa + j * E::MN_CHUNK, &tma_a, fb, am + BK * j, k0);
+            for (int j = 0; j < HALF / BK; ++j)
+              tma_load_3d_pair(sa + j * E::MN_CHUNK, &tma_a, fb, am + BK * j, k0, bidx);
           } else {
-            tma_load_2d_pair(sa, &tma_a, fb, k0, am);
+            tma_load_3d_pair(sa, &tma_a, fb, k0, am, bidx);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / BK; ++j) tma_load_2d_pair(sb + j * E::MN_CHUNK, &tma_b, fb, bn + BK * j, k0);
+            for (int j = 0; j < HALF / BK; ++j)
+              tma_load_3d_pair(sb + j * E::MN_CHUNK, &tma_b, fb, bn + BK * j, k0, bidx);
           } else {
-            tma_load_2d_pair(sb, &tma_b, fb, k0, bn);
+            tma_load_3d_pair(sb, &tma_b, fb, k0, bn, bidx);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -754,6 +766,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     uint32_t acc_phase = 0;
     for (int t = pair; t < tiles; t += pairs) {
       const TileCoord tc = coord(t);
+      const int bidx = (t % out_tiles) / tiles_pb;
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row0 = tc.m0 + (int)rank * HALF + q * 32;
@@ -765,7 +778,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;
-        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles,
+        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles, bidx,
                   stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
       }
       tc_fence_before();
@@ -814,16 +827,18 @@ EncodeTiled encode_fn() {
 
 // 2-D operand tensor map over a row-major [outer][ld] buffer (bf16, or fp32
 // read as TF32), box {one 128-byte row, box_outer}, 128B swizzle.
+// 3-D over `batch` such buffers `sbatch` elements apart (batch 1: a plain matrix).
 int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld, int box_outer,
-             bool tf32, bool mn_major) {
+             bool tf32, bool mn_major, int batch, long long sbatch) {
   EncodeTiled enc = encode_fn();
   if (!enc) return fail(SG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int esz = tf32 ? 4 : 2;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(tc::ROW_BYTES / esz), (cuuint32_t)box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  if (batch <= 1) sbatch = ld * outer;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * esz), (cuuint64_t)(sbatch * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)(tc::ROW_BYTES / esz), (cuuint32_t)box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                    const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -835,16 +850,20 @@ int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer
 // Output maps for the TMA-store epilogue: box 32 x 32, swizzle matching
 // stage_bf16 (64B) / stage_f32 (128B).  Returns false when the buffer does
 // not meet TMA's alignment rules (the epilogue then stores directly).
-bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, long long M, long long ld) {
+bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, long long M, long long ld, int batch,
+                  long long sbatch) {
   const long long esz = bf16 ? 2 : 4;
-  if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || M <= 0 || N <= 0) return false;
+  if (batch <= 1) sbatch = ld * M;
+  if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || (sbatch * esz) % 16 || M <= 0 ||
+      N <= 0)
+    return false;
   EncodeTiled enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * esz), (cuuint64_t)(sbatch * esz)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                    const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -860,8 +879,10 @@ void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& 
   std::memset(&mf32, 0, sizeof mf32);
   p.tma_lp = p.tma_f32 = 0;
   if (!enabled || p.splits > 1) return;
-  if (g.epi.out_bf16) p.tma_lp = make_out_map(&mlp, g.epi.out_bf16, true, g.N, g.M, g.epi.ld_bf16);
-  if (g.epi.out_f32) p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32);
+  if (g.epi.out_bf16)
+    p.tma_lp = make_out_map(&mlp, g.epi.out_bf16, true, g.N, g.M, g.epi.ld_bf16, g.batch, g.so_lp);
+  if (g.epi.out_f32)
+    p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32, g.batch, g.so_f32);
 }
 
 // split-K finalize: out = sum_s part[s] in ascending s (deterministic)
@@ -916,11 +937,11 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
-  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, tc::BM, TF32, false);
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true, g.batch, g.sa);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, tc::BM, TF32, false, g.batch, g.sa);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN, TF32, false);
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true, g.batch, g.sb);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN, TF32, false, g.batch, g.sb);
   if (rc) return rc;
   auto kern = tc::gemm_tc_kernel<TF32, BN, STAGES, A_MN, B_MN>;
   static bool attr_set = false;
@@ -928,12 +949,12 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
-  const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN);
+  const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int num_kb = (g.K + BK - 1) / BK;
   // split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
   // layer: M = N = 1024, K = batch): plain-store epilogues only
   int splits = 1, kb_per = num_kb;
-  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && tiles * 2 <= num_sms && num_kb >= 8) {
+  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && g.batch == 1 && tiles * 2 <= num_sms && num_kb >= 8) {
     int s = num_sms / tiles;
     if (s > num_kb / 4) s = num_kb / 4;
     if (s > 16) s = 16;
@@ -942,7 +963,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
   CUtensorMap mlp, mf32;
   out_maps(g, p, mlp, mf32);
   float* part = nullptr;
@@ -972,11 +993,11 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
-  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, 128, TF32, false);
+  if (A_MN) rc = make_map(&ma, g.A, g.M, g.K, g.lda, BK, TF32, true, g.batch, g.sa);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.lda, 128, TF32, false, g.batch, g.sa);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false);
+  if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true, g.batch, g.sb);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false, g.batch, g.sb);
   if (rc) return rc;
   auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN>;
   static bool attr_set = false;
@@ -985,10 +1006,10 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
     attr_set = true;
   }
   const int pairs_avail = num_sms / 2;
-  const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256) * g.batch;
   const int num_kb = (g.K + BK - 1) / BK;
   int splits = 1, kb_per = num_kb;
-  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && tiles * 2 <= pairs_avail && num_kb >= 8) {
+  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && g.batch == 1 && tiles * 2 <= pairs_avail && num_kb >= 8) {
     int s = pairs_avail / tiles;
     if (s > num_kb / 4) s = num_kb / 4;
     if (s > 16) s = 16;
@@ -997,7 +1018,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
   CUtensorMap mlp, mf32;
   out_maps(g, p, mlp, mf32);
   float* part = nullptr;
@@ -1054,6 +1075,13 @@ int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st) {
                                 : "gemm: lda/ldb must be multiples of 8 elements");
   if (g.lda < (g.a_mn ? g.M : g.K) || g.ldb < (g.b_mn ? g.N : g.K))
     return fail(SG_EINVAL, "gemm: leading dimension smaller than the row");
+  if (g.batch < 1) return fail(SG_EINVAL, "gemm: batch must be >= 1");
+  if (g.batch > 1) {
+    if (g.epi.colsum || g.epi.out_pre || g.epi.mode == SG_EPI_ACT_GRAD)
+      return fail(SG_EINVAL, "gemm: batched GEMMs take the STORE / BIAS_ACT epilogues without colsum / out_pre");
+    if ((g.sa * (tf32 ? 4 : 2)) % 16 || (g.sb * (tf32 ? 4 : 2)) % 16)
+      return fail(SG_EINVAL, "gemm: batch strides must be multiples of 16 bytes");
+  }
   return tf32 ? dispatch<true>(g, num_sms, st) : dispatch<false>(g, num_sms, st);
 }
 

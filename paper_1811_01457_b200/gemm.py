@@ -33,6 +33,9 @@ class GemmDesc(ctypes.Structure):
         ("out", ctypes.c_void_p), ("ld_out", ctypes.c_int64),
         ("out_lp", ctypes.c_void_p), ("ld_lp", ctypes.c_int64),
         ("colsum", ctypes.c_void_p), ("ld_colsum", ctypes.c_int64),
+        ("batch", ctypes.c_int64),
+        ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
+        ("stride_out", ctypes.c_int64), ("stride_lp", ctypes.c_int64),
     ]
 
 
@@ -95,4 +98,39 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     d.out, d.ld_out = _ptr(out), _ld(out)
     d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
     d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
+    rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
+
+
+def _ld3(t):
+    if t is None:
+        return 0, 0
+    if t.dim() != 3 or t.stride(2) != 1:
+        raise ValueError("bmm operands must be 3-D [lanes, rows, cols] with unit column stride")
+    return t.stride(1), t.stride(0)
+
+
+def bmm(A, B, out=None, *, a_mn=False, b_mn=False, precision="bf16", epilogue="store", act="identity",
+        bias=None, out_lp=None, stream=None):
+    """Batched GEMM, one launch: ``out[l] = A[l] . B[l]^T`` per lane l (the
+    reference's ``bmm``, tensor.py:364-369, with ``B`` given ``[lanes, N, K]``
+    or, with ``b_mn``, ``[lanes, K, N]``).  Operands/outputs are 3-D with
+    the lane axis first."""
+    L = A.shape[0]
+    if B.shape[0] != L:
+        raise ValueError(f"bmm lane counts differ: {A.shape} x {B.shape}")
+    Ka, Ma = (A.shape[1], A.shape[2]) if a_mn else (A.shape[2], A.shape[1])
+    Kb, Nb = (B.shape[1], B.shape[2]) if b_mn else (B.shape[2], B.shape[1])
+    if Ka != Kb:
+        raise ValueError(f"bmm shapes {tuple(A.shape)} x {tuple(B.shape)}")
+    d = GemmDesc()
+    d.M, d.N, d.K = int(Ma), int(Nb), int(Ka)
+    (d.lda, d.stride_a), (d.ldb, d.stride_b) = _ld3(A), _ld3(B)
+    d.A, d.a_mn_major, d.B, d.b_mn_major = _ptr(A), int(a_mn), _ptr(B), int(b_mn)
+    d.precision, d.epilogue, d.act = PREC[precision], EPI[epilogue], ACT[act]
+    d.bias = _ptr(bias)
+    d.out, (d.ld_out, d.stride_out) = _ptr(out), _ld3(out)
+    d.out_lp, (d.ld_lp, d.stride_lp) = _ptr(out_lp), _ld3(out_lp)
+    d.batch = int(L)
+    if L == 0 or d.M == 0 or d.N == 0:
+        return
     rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")

@@ -28,7 +28,7 @@ import math
 
 from . import fused as F
 from . import runtime as rt
-from .gemm import gemm
+from .gemm import bmm, gemm
 from .ir import kind_of
 from .irtext import parse_ir
 
@@ -155,6 +155,30 @@ class Tape:
 
 
 EMPTY_TAPE = Tape()
+
+
+class TapeBatch:
+    """One independent tape per lane (interp.py:64-70)."""
+
+    __slots__ = ("lanes",)
+
+    def __init__(self, lanes):
+        self.lanes = tuple(lanes)
+
+
+def _lane_value(v, lane_shape):
+    """A lane's top coerced to the per-lane shape, or None (interp.py:368-380)."""
+    if lane_shape:
+        if _is_tensor(v) and tuple(v.shape) == tuple(lane_shape):
+            return v
+        return None
+    if isinstance(v, bool):
+        return 1.0 if v else 0.0
+    if isinstance(v, (int, float)):
+        return float(v)
+    if _is_tensor(v) and v.dim() == 0:
+        return v
+    return None
 
 
 def _is_tensor(v) -> bool:
@@ -318,10 +342,45 @@ class GpuMachine:
         gemm(a.contiguous(), b.contiguous(), b_mn=True, precision=prec, out=out)
         return out
 
+    def _bmm(self, a, b):
+        """tensor.bmm (tensor.py:364-369): every lane's strict fold in ONE batched launch."""
+        import torch
+
+        if a.dim() != 3 or b.dim() != 3 or a.shape[0] != b.shape[0] or a.shape[2] != b.shape[1]:
+            raise ValueError(f"bmm shapes {tuple(a.shape)} x {tuple(b.shape)}")
+        out = torch.empty((a.shape[0], a.shape[1], b.shape[2]), dtype=a.dtype, device="cuda")
+        prec = "strict_fp64" if a.dtype == torch.float64 else "strict_fp32"
+        bmm(a.contiguous(), b.contiguous(), out, b_mn=True, precision=prec)
+        return out
+
     # ----------------------------------------------------------- tapes
+    # Per-lane traces of vectorised programs (spmd_batch.py, interp.py:271-318):
+    # a TapeBatch holds one persistent tape per lane.
+    def _tape_push(self, t, v, per_lane: bool):
+        if isinstance(t, Tape) and per_lane:
+            t = TapeBatch((t,) * v.shape[0])
+        if isinstance(t, TapeBatch):
+            if per_lane:
+                rows = list(v.unbind(0)) if _is_tensor(v) else list(v)
+                return TapeBatch(tuple(Tape(r, l) for r, l in zip(rows, t.lanes)))
+            return TapeBatch(tuple(Tape(v, l) for l in t.lanes))
+        return Tape(v, t)
+
     def _tape_top(self, t, ty):
-        if kind_of(ty) == "tapes":
-            raise rt.DomainError("batched traces are not supported on the GPU machine")
+        import torch
+
+        if isinstance(t, TapeBatch):
+            lane_shape = tuple(ty.shape[1:])
+            vals = [_lane_value(l.top, lane_shape) if not l.empty else None for l in t.lanes]
+            if lane_shape:
+                z = torch.zeros(lane_shape, dtype=self.dtype, device="cuda")
+                return torch.stack([z if v is None else v for v in vals], 0)
+            host = [0.0 if v is None else v for v in vals]
+            if all(not _is_tensor(v) for v in host):
+                return torch.tensor(host, dtype=self.dtype, device="cuda").reshape(tuple(ty.shape))
+            return torch.stack([v.reshape(()).to(self.dtype) if _is_tensor(v)
+                                else torch.tensor(float(v), dtype=self.dtype, device="cuda")
+                                for v in host]).reshape(tuple(ty.shape))
         if t.empty:
             return self._zero(ty)
         return t.top
@@ -340,6 +399,8 @@ class GpuMachine:
             return torch.zeros(tuple(ty.shape), dtype=self.dtype, device="cuda")
         if k == "tape":
             return EMPTY_TAPE
+        if k == "tapes":
+            return TapeBatch((EMPTY_TAPE,) * int(ty.lanes))
         raise ValueError(f"no zero for {ty}")
 
     # -------------------------------------------------------- dispatch
@@ -382,12 +443,14 @@ class GpuMachine:
             c, x, y = env[a[0]], env[a[1]], env[a[2]]
             if isinstance(c, bool):
                 return x if c else y
+            if isinstance(x, TapeBatch):  # per-lane trace merge (interp.py:233-238)
+                keep = c.ne(0).tolist()
+                return TapeBatch(tuple(xt if k else yt for k, xt, yt in zip(keep, x.lanes, y.lanes)))
             return self._ew("selmask", c, x, y)  # tensor.py:276-281
         if op == "matmul":
             return self._matmul(env[a[0]], env[a[1]])
         if op == "bmm":
-            x, y = env[a[0]], env[a[1]]
-            return torch.stack([self._matmul(x[i], y[i]) for i in range(x.shape[0])])
+            return self._bmm(env[a[0]], env[a[1]])
         if op == "transpose":
             return env[a[0]].transpose(-1, -2).contiguous()
         if op == "reshape":
@@ -425,18 +488,22 @@ class GpuMachine:
         if op == "tape_new":
             return EMPTY_TAPE
         if op == "tape_push":
-            if ins.attrs.get("per_lane"):
-                raise rt.DomainError("batched traces are not supported on the GPU machine")
-            return Tape(env[a[1]], env[a[0]])
+            return self._tape_push(env[a[0]], env[a[1]], bool(ins.attrs.get("per_lane", False)))
         if op == "tape_top":
             return self._tape_top(env[a[0]], ins.attrs["ty"])
         if op == "tape_rest":
             t = env[a[0]]
+            if isinstance(t, TapeBatch):
+                return TapeBatch(tuple(l.rest if not l.empty else l for l in t.lanes))
             return t.rest if not t.empty else t
+        if op == "tape_spread":
+            return TapeBatch((env[a[0]],) * int(ins.attrs["lanes"]))
         if op == "tape_expect_empty":
             t = env[a[0]]
-            if not t.empty:
-                raise rt.DomainError(f"trace should be used up, {len(t)} entries remain")
+            lanes = t.lanes if isinstance(t, TapeBatch) else (t,)
+            left = [len(l) for l in lanes if not l.empty]
+            if left:
+                raise rt.DomainError(f"trace should be used up, {max(left)} entries remain")
             return True
         raise rt.DomainError(f"op '{op}' has no evaluation rule")
 
@@ -480,6 +547,38 @@ def grad(module, name: str, args: tuple, seeds: tuple | None = None, step_limit:
     out = m.call(aug, tuple(args))
     n = len(fn.results)
     cots = m.call(pb, (out[n], out[n + 1]) + tuple(seeds))
+    res = {}
+    i = 0
+    for pv, ty in fn.params:
+        if kind_of(ty) in ("f64", "tensor"):
+            res[pv] = cots[i]
+            i += 1
+    return res
+
+
+def batched_grad(module, name: str, lanes: int, stacked_args: tuple, seeds: tuple,
+                 step_limit: int = DEFAULT_STEP_LIMIT, vectorize=None) -> dict:
+    """``spmd_batch.batched_grad`` (spmd_batch.py:718-745) on the GPU: one
+    batched augmented forward and one batched pullback of the vectorised
+    ``{name}__aug`` / ``{name}__pb`` (lane axis first on every argument and
+    seed); per-lane traces live in :class:`TapeBatch`, and every lane's
+    matmul runs inside ONE batched launch (``bmm``).  The vectorising
+    transform is the reference's (passed in / imported), or the module
+    already holds ``{name}__aug__batched_B{lanes}`` (parsed from text)."""
+    fn = module.get(name)
+    vaug, vpb = f"{name}__aug__batched_B{lanes}", f"{name}__pb__batched_B{lanes}"
+    if vaug not in module.functions or vpb not in module.functions:
+        if vectorize is None:
+            from ssagrad import augment, vectorize  # the reference transforms (host-side IR)
+        else:
+            from ssagrad import augment
+        a, p = augment(module, name)
+        vectorize(module, a.name, lanes)
+        vectorize(module, p.name, lanes)
+    m = GpuMachine(module, step_limit)
+    outs = m.call(vaug, tuple(stacked_args))
+    n = len(fn.results)
+    cots = m.call(vpb, (outs[n], outs[n + 1]) + tuple(seeds))
     res = {}
     i = 0
     for pv, ty in fn.params:

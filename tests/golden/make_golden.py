@@ -318,6 +318,43 @@ def machine_cases():
     return out
 
 
+def spmd_cases():
+    """Vectorised (SPMD lane) aug/pb programs printed by the reference and
+    its batched_grad cotangents (spmd_batch.py:718-745): per-lane traces,
+    lane-divergent loops, and matmul -> bmm for lanes that carry weights."""
+    from ssagrad import augment, batched_grad, print_ir, stack_lanes, vectorize
+    from ssagrad.ir import tensor_type
+    from conftest_ref import ANALYTIC_SRC
+
+    m = parse_ir(ANALYTIC_SRC)
+    rng = np.random.default_rng(17)
+    lanes = 4
+    cases = []
+    for name in ("net", "prod", "cube", "absval", "powloop"):
+        fn = m.get(name)
+        a, p = augment(m, name)
+        vectorize(m, a.name, lanes)
+        vectorize(m, p.name, lanes)
+        per_lane = []
+        for _ in range(lanes):
+            args = []
+            for _, ty in fn.params:
+                if ty.kind == "tensor":
+                    args.append(DenseTensor(f32(rng.uniform(-1.5, 1.5, ty.shape))))
+                elif ty.kind == "i64":
+                    args.append(int(rng.integers(0, 6)))
+                else:
+                    args.append(float(f32(rng.uniform(-2, 2, ()))))
+            per_lane.append(args)
+        stacked = tuple(stack_lanes(ty, [la[i] for la in per_lane]) for i, (_, ty) in enumerate(fn.params))
+        seeds = tuple(stack_lanes(ty, [1.0] * lanes) for ty in fn.results)
+        bg = batched_grad(m, name, lanes, stacked, seeds)
+        cases.append({"fn": name, "lanes": lanes,
+                      "args": [enc(v) for v in stacked], "seeds": [enc(v) for v in seeds],
+                      "grads": [enc(bg[pv]) for pv, ty in fn.params if ty.is_differentiable]})
+    return {"ir": print_ir(m), "cases": cases}
+
+
 def dan_train_case():
     """Everything the reference's DAN `train` (nn_train.py:418-450) needs,
     frozen: augmented loss IR (batch 32), eval IR (n = 320), the synthetic
@@ -349,6 +386,11 @@ def dan_train_case():
     }
 
 
+def save_spmd():
+    with open(os.path.join(HERE, "spmd.json"), "w") as f:
+        json.dump(spmd_cases(), f, indent=0)
+
+
 def save_bce():
     # binary classifier with the DAN head/loss recipe; large first-layer weights
     # push some predictions into the clamp range (select gradients = 0)
@@ -364,6 +406,7 @@ def main():
         json.dump(machine_cases(), f, indent=0)
     with open(os.path.join(HERE, "fuzz.json"), "w") as f:
         json.dump(fuzz_cases(), f, indent=0)
+    save_spmd()
     with open(os.path.join(HERE, "dan_train.json"), "w") as f:
         json.dump(dan_train_case(), f)
     np.savez_compressed(os.path.join(HERE, "tensor.npz"), **tensor_cases())

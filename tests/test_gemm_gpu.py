@@ -184,3 +184,46 @@ def test_strict_fp64_matches_reference_bit_for_bit():
         gemm(A, B, b_mn=True, precision="strict_fp64", out=out)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+@pytest.mark.parametrize("L,M,N,K,layout", [(3, 128, 256, 64, "kk"), (5, 200, 72, 136, "k_mn"),
+                                            (4, 304, 520, 96, "mn_mn"), (2, 512, 512, 256, "kk"),
+                                            (6, 64, 40, 24, "k_mn")])
+def test_batched_tensor_core_gemm(precision, L, M, N, K, layout):
+    """One launch over L independent GEMMs (the reference's bmm, tensor.py:364-369)."""
+    from paper_1811_01457_b200.gemm import bmm
+
+    rng = np.random.default_rng(L * 100 + M)
+    a_mn = layout == "mn_mn"
+    b_mn = layout != "kk"
+    dt = torch.bfloat16 if precision == "bf16" else torch.float32
+    a = rng.uniform(-1, 1, (L, M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (L, N, K)).astype(np.float32)
+    A = torch.from_numpy(a.transpose(0, 2, 1).copy() if a_mn else a).to(dt).cuda()
+    B = torch.from_numpy(b.transpose(0, 2, 1).copy() if b_mn else b).to(dt).cuda()
+    aq = (A.transpose(1, 2) if a_mn else A).double().cpu().numpy()
+    bq = (B.transpose(1, 2) if b_mn else B).double().cpu().numpy()
+    out = torch.full((L, M, N), float("nan"), device="cuda")
+    bmm(A, B, out, a_mn=a_mn, b_mn=b_mn, precision=precision)
+    torch.cuda.synchronize()
+    got = out.double().cpu().numpy()
+    tol = 1e-5 if precision == "bf16" else 2.0 ** -9  # bf16 inputs exact; tf32 rounds operands
+    for l in range(L):
+        check_close(got[l], aq[l], bq[l].T, tol=tol)
+
+
+def test_batched_strict_fp64_equals_per_lane():
+    """Batched strict GEMM == per-lane strict GEMM (itself bit-exact with the reference matmul)."""
+    from paper_1811_01457_b200.gemm import bmm
+
+    rng = np.random.default_rng(9)
+    L, M, K, N = 4, 37, 29, 11
+    a = torch.from_numpy(rng.uniform(-1, 1, (L, M, K))).cuda()
+    b = torch.from_numpy(rng.uniform(-1, 1, (L, K, N))).cuda()
+    out = torch.empty((L, M, N), dtype=torch.float64, device="cuda")
+    bmm(a, b, out, b_mn=True, precision="strict_fp64")
+    for l in range(L):
+        one = torch.empty((M, N), dtype=torch.float64, device="cuda")
+        gemm(a[l], b[l], b_mn=True, precision="strict_fp64", out=one)
+        assert torch.equal(out[l], one)

@@ -175,3 +175,36 @@ def test_dan_training_reproduces_frozen_history(lam):
         assert g["class_acc"] == r["class_acc"], g
         assert g["domain_probe_acc"] == r["domain_probe_acc"], g
     assert worst <= 1e-9, worst
+
+
+def test_reference_printed_spmd_ir_parses():
+    # CPU: vectorised aug/pb programs (per-lane traces, bmm) read back from text
+    with open(os.path.join(GOLDEN, "spmd.json")) as f:
+        d = json.load(f)
+    m = parse_ir(d["ir"])
+    for c in d["cases"]:
+        assert f"{c['fn']}__aug__batched_B{c['lanes']}" in m.functions
+        assert f"{c['fn']}__pb__batched_B{c['lanes']}" in m.functions
+
+
+@gpu
+def test_batched_grad_matches_reference():
+    """spmd_batch.batched_grad (spmd_batch.py:718-745) on the
+    GPU -- per-lane traces (TapeBatch), lane-divergent loop trips (powloop),
+    and lanes carrying weights (@net: matmul -> bmm, one batched launch)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1811_01457_b200.gpu_machine import batched_grad
+
+    with open(os.path.join(GOLDEN, "spmd.json")) as f:
+        d = json.load(f)
+    m = parse_ir(d["ir"])
+    for c in d["cases"]:
+        fn = m.get(c["fn"])
+        g = batched_grad(m, c["fn"], c["lanes"], tuple(decode(a) for a in c["args"]),
+                         tuple(decode(s) for s in c["seeds"]))
+        got = [g[pv] for pv, ty in fn.params if ty.kind in ("f64", "tensor")]
+        assert len(got) == len(c["grads"])
+        for k, (gv, want) in enumerate(zip(got, c["grads"])):
+            assert max_rel(gv, decode(want)) <= 1e-12, (c["fn"], k)
