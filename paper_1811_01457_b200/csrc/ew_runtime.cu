@@ -286,11 +286,13 @@ long long env_ll(const char* name, long long dflt) {
   return e ? std::atoll(e) : dflt;
 }
 
-// Resident blocks per SM the grid is sized for.  Tuned on B200 (tools/ew_sweep.sh):
-// the forward kernel streams best with fewer, longer-lived blocks; the gradient
-// kernel (64-register budget, SG_GRAD_MINB 4) with 8.
+// Blocks per SM the grid is sized for (an upper bound: at most one row per
+// thread-row).  Tuned on B200 (tools/ew_sweep*.sh, c2 shape): the forward
+// kernel streams best with many short-lived blocks (64/SM: ~27 rows each);
+// the gradient kernel amortises its fp64 partial-sum rows over long spans
+// (8/SM, 64-register budget, SG_GRAD_MINB 4).
 Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* args, int k,
-            const void* const* extra_ptrs, int n_extra, long long per_sm = 8) {
+            const void* const* extra_ptrs, int n_extra, long long per_sm = 8, long long max_bdx = 256) {
   Launch L;
   const int esz = dtype == SG_F64 ? 8 : 4;
   int vec = 16 / esz;
@@ -305,7 +307,8 @@ Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* arg
   L.vec = vec;
   long long cv = (s.C + vec - 1) / vec;
   int bdx = 1;
-  while (bdx < cv && bdx < 256) bdx <<= 1;
+  if (max_bdx < 1 || max_bdx > 256) max_bdx = 256;
+  while (bdx < cv && bdx < max_bdx) bdx <<= 1;
   L.bdx = bdx;
   L.bdy = 256 / bdx;
   long long gx = (cv + bdx - 1) / bdx;
@@ -569,7 +572,8 @@ int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg
   Shape2D s;
   canonicalise(k, args, out, s);
   const void* extra[] = {y->ptr};
-  Launch L = plan(ctx, s, kern->dtype, args, k, extra, 1, env_ll("SGB200_EW_FWD_BLOCKS_PER_SM", 4));
+  Launch L = plan(ctx, s, kern->dtype, args, k, extra, 1, env_ll("SGB200_EW_FWD_BLOCKS_PER_SM", 64),
+                  env_ll("SGB200_EW_FWD_BDX", 256));
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -618,7 +622,7 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   std::vector<const void*> extra = {ybar->ptr, y ? y->ptr : nullptr};
   for (int i = 0; i < k; ++i) extra.push_back(s.kinds[i] == SG_FULL ? argbars[i].ptr : nullptr);
   Launch L = plan(ctx, s, kern->dtype, args, k, extra.data(), (int)extra.size(),
-                  env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", 8));
+                  env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", 8), env_ll("SGB200_EW_GRAD_BDX", 256));
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;

@@ -67,16 +67,31 @@ __device__ __forceinline__ VT sg_from_raw(const SgRaw& w) {
   return *reinterpret_cast<const VT*>(&w);
 }
 __device__ __forceinline__ SgRaw sg_to_raw(const VT& v) { return *reinterpret_cast<const SgRaw*>(&v); }
-// operands read once per element: streaming (evict-first) loads
+// operands read once per element.  Plain loads measured faster than
+// evict-first (.cs) ones on B200 (+2-3% on K2); stores stay evict-first.
+#ifndef SG_LD_CS
+#define SG_LD_CS 0
+#endif
+#ifndef SG_ST_CS
+#define SG_ST_CS 1
+#endif
 __device__ __forceinline__ VT sg_ldv_stream(const T* p) {
+#if SG_LD_CS
   return sg_from_raw(__ldcs(reinterpret_cast<const SgRaw*>(p)));
+#else
+  return sg_from_raw(*reinterpret_cast<const SgRaw*>(p));
+#endif
 }
 // broadcast vectors (bias-like, re-read by every row): cached loads
 __device__ __forceinline__ VT sg_ldv(const T* p) {
   return sg_from_raw(__ldg(reinterpret_cast<const SgRaw*>(p)));
 }
 __device__ __forceinline__ void sg_stv(T* p, const VT& v) {
+#if SG_ST_CS
   __stcs(reinterpret_cast<SgRaw*>(p), sg_to_raw(v));
+#else
+  *reinterpret_cast<SgRaw*>(p) = sg_to_raw(v);
+#endif
 }
 
 __device__ __forceinline__ void sg_publish_error(unsigned long long* err, long long elem, int site) {
@@ -134,10 +149,30 @@ __device__ __forceinline__ long long sg_row_end(const SgEwParams& p) {
   long long e = ((long long)blockIdx.y + 1) * p.rows_per_block;
   return e < p.R ? e : p.R;
 }
-// rows of this thread: r0 + ty + it*SG_BDY for it in [0, n)
-__device__ __forceinline__ long long sg_my_rows(long long r0, long long r1, int ty) {
-  const long long lo = r0 + ty;
-  return r1 > lo ? (r1 - lo + SG_BDY - 1) / SG_BDY : 0;
+// Row walk of thread (by, ty): r = base + it * stride, it in [0, n).
+// SG_ROW_IL 0 (default): each block owns the contiguous span [r0, r1);
+// 1: rows interleaved over the whole grid (base = by*BDY + ty, stride =
+// gy*BDY).  Measured on B200 (tools/ew_sweep4.sh): contiguous spans stream
+// faster for both kernels once the forward grid is large.
+#ifndef SG_ROW_IL
+#define SG_ROW_IL 0
+#endif
+struct SgRows {
+  long long base, stride, n;
+};
+__device__ __forceinline__ SgRows sg_rows(const SgEwParams& p, int ty) {
+  SgRows w;
+#if SG_ROW_IL
+  w.base = (long long)blockIdx.y * SG_BDY + ty;
+  w.stride = (long long)gridDim.y * SG_BDY;
+  w.n = p.R > w.base ? (p.R - w.base + w.stride - 1) / w.stride : 0;
+#else
+  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  w.base = r0 + ty;
+  w.stride = SG_BDY;
+  w.n = r1 > w.base ? (r1 - w.base + SG_BDY - 1) / SG_BDY : 0;
+#endif
+  return w;
 }
 
 __device__ __forceinline__ void sg_primal_row(const SgEwParams& p, long long r, long long c,
@@ -162,8 +197,8 @@ sg_ew_forward(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
-  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
-  const long long n = sg_my_rows(r0, r1, ty);
+  const SgRows w = sg_rows(p, ty);
+  const long long n = w.n;
   T* out = reinterpret_cast<T*>(p.out);
   T inv[SG_KT][SG_VEC];
   sg_load_invariant(p, c, inv);
@@ -171,13 +206,13 @@ sg_ew_forward(const SgEwParams p) {
   for (; it + SG_UNROLL <= n; it += SG_UNROLL) {  // full chunks: all loads issued first
     T xs[SG_UNROLL][SG_KT][SG_VEC];
 #pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) sg_load_row(p, r0 + ty + (it + u) * SG_BDY, c, inv, xs[u]);
+    for (int u = 0; u < SG_UNROLL; ++u) sg_load_row(p, w.base + (it + u) * w.stride, c, inv, xs[u]);
 #pragma unroll
-    for (int u = 0; u < SG_UNROLL; ++u) sg_primal_row(p, r0 + ty + (it + u) * SG_BDY, c, xs[u], out);
+    for (int u = 0; u < SG_UNROLL; ++u) sg_primal_row(p, w.base + (it + u) * w.stride, c, xs[u], out);
   }
   for (; it < n; ++it) {
     T xs[SG_KT][SG_VEC];
-    const long long r = r0 + ty + it * SG_BDY;
+    const long long r = w.base + it * w.stride;
     sg_load_row(p, r, c, inv, xs);
     sg_primal_row(p, r, c, xs, out);
   }
@@ -230,7 +265,7 @@ sg_ew_grad(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   const bool active = c < p.C;
-  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const SgRows w = sg_rows(p, ty);
   const T* ybar = reinterpret_cast<const T*>(p.ybar);
 
   SgGradAcc acc;
@@ -246,7 +281,7 @@ sg_ew_grad(const SgEwParams p) {
 #if !SG_HAS_COL
   // no cross-thread work per row: full chunks with all loads issued first
   if (active) {
-    const long long n = sg_my_rows(r0, r1, ty);
+    const long long n = w.n;
     double colsum[SG_KT];
     long long it = 0;
     for (; it + SG_GUNROLL <= n; it += SG_GUNROLL) {
@@ -254,16 +289,16 @@ sg_ew_grad(const SgEwParams p) {
       VT yb[SG_GUNROLL];
 #pragma unroll
       for (int u = 0; u < SG_GUNROLL; ++u) {
-        const long long r = r0 + ty + (it + u) * SG_BDY;
+        const long long r = w.base + (it + u) * w.stride;
         sg_load_row(p, r, c, inv, xs[u]);
         yb[u] = sg_ldv_stream(ybar + r * p.C + c);
       }
 #pragma unroll
       for (int u = 0; u < SG_GUNROLL; ++u)
-        sg_grad_row(p, r0 + ty + (it + u) * SG_BDY, c, xs[u], yb[u], acc, colsum);
+        sg_grad_row(p, w.base + (it + u) * w.stride, c, xs[u], yb[u], acc, colsum);
     }
     for (; it < n; ++it) {
-      const long long r = r0 + ty + it * SG_BDY;
+      const long long r = w.base + it * w.stride;
       T xs[SG_KT][SG_VEC];
       sg_load_row(p, r, c, inv, xs);
       VT yb = sg_ldv_stream(ybar + r * p.C + c);
@@ -274,10 +309,11 @@ sg_ew_grad(const SgEwParams p) {
   // COL operands reduce across the lanes sharing a row: every lane of a
   // group must take the same trip count, so walk the block's row span
   constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
-  const long long rows_span = r1 > r0 ? (r1 - r0 + SG_BDY - 1) / SG_BDY : 0;
+  // the block-uniform trip count: the longest walk of any ty in the block
+  const long long rows_span = sg_rows(p, 0).n;
   for (long long it = 0; it < rows_span; ++it) {
-    const long long r = r0 + ty + it * SG_BDY;
-    const bool live = active && r < r1;
+    const long long r = w.base + it * w.stride;
+    const bool live = active && it < w.n;
     double colsum[SG_KT];
 #pragma unroll
     for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
@@ -332,12 +368,13 @@ sg_ew_pack(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
-  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const SgRows w = sg_rows(p, ty);
   const long long plane = p.R * p.C;
   T* pk = reinterpret_cast<T*>(p.pack);
   T inv[SG_KT][SG_VEC];
   sg_load_invariant(p, c, inv);
-  for (long long r = r0 + ty; r < r1; r += SG_BDY) {
+  for (long long it = 0; it < w.n; ++it) {
+    const long long r = w.base + it * w.stride;
     T xs[SG_KT][SG_VEC];
     sg_load_row(p, r, c, inv, xs);
     VT y, g[SG_KT];
