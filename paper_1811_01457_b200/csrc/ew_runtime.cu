@@ -560,6 +560,12 @@ int sg_ew_compile_only(const char* user_src, int k, int dtype, const int* kinds,
   int rc = nvrtc_compile(build_source(user_src, "compile-only", k, dtype, kinds, L), cubin);
   if (rc) return rc;
   if (cubin_bytes) *cubin_bytes = cubin.size();
+  if (const char* path = std::getenv("SGB200_CUBIN_OUT")) {  // inspection hook (cuobjdump)
+    if (FILE* f = std::fopen(path, "wb")) {
+      std::fwrite(cubin.data(), 1, cubin.size(), f);
+      std::fclose(f);
+    }
+  }
   return SG_OK;
 }
 
