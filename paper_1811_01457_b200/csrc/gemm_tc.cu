@@ -241,6 +241,7 @@ struct KParams {
   float* part;        // [splits][M][ld_part] when splits > 1
   long long ld_part;
   int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
+  int aux_stage;        // ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot
   int batch;            // independent GEMMs (bmm lanes), >= 1
   long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
 };
@@ -298,11 +299,35 @@ __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap*
   }
 }
 
+// ACT_GRAD saved activations through TMA: a 32 x 32 bf16 block (SWIZZLE_64B,
+// the layout stage_bf16 writes) lands in the upper 2 KB of the warp's
+// staging slot, so the next chunk's block is in flight while this one is
+// processed (and the tile's first block while the accumulator is computed).
+constexpr int AUX_OFF = 2048;
+__device__ __forceinline__ void aux_issue(uint8_t* slot, const CUtensorMap* map, uint64_t* bar, int n0, int row0) {
+  mbar_expect_tx(bar, 2048);
+  tma_load_3d(slot + AUX_OFF, map, bar, n0, row0, 0);
+}
+__device__ __forceinline__ void aux_read(const uint8_t* slot, float (&h)[32], int lane) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 w = *reinterpret_cast<const uint4*>(slot + AUX_OFF + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4));
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(b[j]);
+      h[8 * c + 2 * j] = f.x;
+      h[8 * c + 2 * j + 1] = f.y;
+    }
+  }
+}
+
 // One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
-                                          bool grp_ok, int n0, int lane, int split, int bidx, uint8_t* slot,
+                                          bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
+                                          const float (&hs)[32], uint8_t* slot,
                                           const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -335,10 +360,14 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
     act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
-    float h[32];
-    if (e.aux_f32) load_row_f32(e.aux_f32 + (long long)m * e.ld_aux + n0, h, nn);
-    else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
-    act_grad_chunk(v, h, e.act);
+    if (hstaged) {
+      act_grad_chunk(v, hs, e.act);
+    } else {
+      float h[32];
+      if (e.aux_f32) load_row_f32(e.aux_f32 + (long long)m * e.ld_aux + n0, h, nn);
+      else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
+      act_grad_chunk(v, h, e.act);
+    }
   }
   const int row0 = m - lane;
   if (e.out_f32) {
@@ -358,6 +387,7 @@ template <bool TF32, int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
+                 const __grid_constant__ CUtensorMap tma_aux,
                  const KParams p) {
   using E = Elem<TF32>;
   constexpr int BK = E::BK;
@@ -376,6 +406,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   uint8_t* stage_slots = smem + STAGES * STAGE_BYTES + 1024;  // 8 x 4 KB epilogue staging
+  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512);  // one per epilogue warp
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -405,6 +436,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], EPI_WARPS);  // one arrival per epilogue warp
     }
+    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -501,24 +533,37 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const int half = ew / 4;  // which half of the tile's columns
     constexpr int CHUNKS = BN / 32;
     constexpr int CH_PER = CHUNKS / 2;
-    const GemmEpilogue& e = p.epi;
     int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t acc_phase = 0, aux_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int u = t % out_tiles, bidx = u / tiles_pb;
       const TileCoord tc = tile_of(u - bidx * tiles_pb, m_tiles, n_tiles, BN);
+      const int row0 = tc.m0 + q * 32;
+      const int c0 = half * CH_PER, c1 = (half + 1) * CH_PER;
+      uint8_t* slot = stage_slots + ew * STAGE_SLOT;
+      const bool staged = p.aux_stage && row0 < p.M;  // warp-uniform
+      if (staged && lane == 0 && tc.n0 + c0 * 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], tc.n0 + c0 * 32, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const int m = tc.m0 + q * 32 + lane;
+      const int m = row0 + lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
-      for (int c = half * CH_PER; c < (half + 1) * CH_PER; ++c) {
+      for (int c = c0; c < c1; ++c) {
         const int n0 = tc.n0 + c * 32;
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
-        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, tc.m0 + q * 32 < p.M, n0, lane, t / out_tiles, bidx,
-                  stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
+        float h[32];
+        if (staged) {
+          mbar_wait(&aux_bar[ew], aux_phase);
+          aux_phase ^= 1;
+          aux_read(slot, h, lane);
+          fence_proxy_async();  // our reads precede the next async write of the buffer
+          __syncwarp();
+          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
+        }
+        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
+                  &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -602,6 +647,7 @@ template <bool TF32, int STAGES, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
+                      const __grid_constant__ CUtensorMap tma_aux,
                       const KParams p) {
   constexpr int PM = 256, BN = 256, HALF = 128;
   using E = Elem<TF32>;
@@ -620,6 +666,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   uint8_t* stage_slots = smem + STAGES * STAGE_BYTES + 1024;  // 8 x 4 KB epilogue staging
+  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512);  // one per epilogue warp
 
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -664,6 +711,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2 * EPI_WARPS);  // every epilogue warp of both CTAs
     }
+    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -763,23 +811,36 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     const uint32_t acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
     const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
     int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t acc_phase = 0, aux_phase = 0;
     for (int t = pair; t < tiles; t += pairs) {
       const TileCoord tc = coord(t);
       const int bidx = (t % out_tiles) / tiles_pb;
+      const int row0 = tc.m0 + (int)rank * HALF + q * 32;
+      const int c0 = half * CH_PER, c1 = (half + 1) * CH_PER;
+      uint8_t* slot = stage_slots + ew * STAGE_SLOT;
+      const bool staged = p.aux_stage && row0 < p.M;  // warp-uniform
+      if (staged && lane == 0 && tc.n0 + c0 * 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], tc.n0 + c0 * 32, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const int row0 = tc.m0 + (int)rank * HALF + q * 32;
       const int m = row0 + lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
-      for (int c = half * CH_PER; c < (half + 1) * CH_PER; ++c) {
+      for (int c = c0; c < c1; ++c) {
         const int n0 = tc.n0 + c * 32;
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;
-        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles, bidx,
-                  stage_slots + ew * STAGE_SLOT, &tma_olp, &tma_of32);
+        float h[32];
+        if (staged) {
+          mbar_wait(&aux_bar[ew], aux_phase);
+          aux_phase ^= 1;
+          aux_read(slot, h, lane);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
+        }
+        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
+                  &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -868,6 +929,31 @@ bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, lon
                    bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// ACT_GRAD with a bf16 saved activation and a bf16-only output: the aux
+// blocks are TMA-streamed through the free half of each staging slot.
+void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m) {
+  std::memset(&m, 0, sizeof m);
+  p.aux_stage = 0;
+  static const bool enabled = [] {
+    const char* e = std::getenv("SGB200_GEMM_AUX_TMA");
+    return !(e && e[0] == '0');
+  }();
+  const GemmEpilogue& e = g.epi;
+  if (!enabled || e.mode != SG_EPI_ACT_GRAD || !e.aux || e.aux_f32 || e.out_f32 || !p.tma_lp || p.splits > 1 ||
+      g.batch > 1 || (reinterpret_cast<uintptr_t>(e.aux) & 15) || (e.ld_aux * 2) % 16)
+    return;
+  EncodeTiled enc = encode_fn();
+  if (!enc) return;
+  cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)(e.ld_aux * 2), (cuuint64_t)(e.ld_aux * 2 * g.M)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(e.aux), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  p.aux_stage = r == CUDA_SUCCESS;
 }
 
 void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& mf32) {
@@ -963,9 +1049,10 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
-  CUtensorMap mlp, mf32;
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
+  CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
+  aux_map(g, p, maux);
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
@@ -974,7 +1061,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, maux, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
@@ -1018,9 +1105,10 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
-  CUtensorMap mlp, mf32;
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
+  CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
+  aux_map(g, p, maux);
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
@@ -1029,7 +1117,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, p);
+  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, maux, p);
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
