@@ -60,6 +60,8 @@ class Tape:
                 fn()
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
+        # thread-local capture: NCCL's proxy threads (data-parallel steps) keep
+        # making CUDA calls while this thread captures
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
             fn()
         return g

@@ -208,3 +208,23 @@ def test_batched_grad_matches_reference():
         assert len(got) == len(c["grads"])
         for k, (gv, want) in enumerate(zip(got, c["grads"])):
             assert max_rel(gv, decode(want)) <= 1e-12, (c["fn"], k)
+
+
+@gpu
+@pytest.mark.parametrize("key", ["analytic", "corpus"])
+def test_device_tape_backprop_matches_reference(golden, key):
+    """the rule table on the device builder (CudaBuilder),
+    swept over a runtime trace recorded on the GpuMachine (the reference's
+    oracle.trace_grad, oracle.py:140-197), vs the reference's gradients."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1811_01457_b200.taping import trace_grad
+
+    m = parse_ir(golden[key]["ir"])
+    for case in golden[key]["cases"]:
+        fn = m.get(case["fn"])
+        g = trace_grad(m, case["fn"], tuple(_args(case)))
+        got = [g[pv] for pv, ty in fn.params if ty.kind in ("f64", "tensor")]
+        for gv, want in zip(got, case["grads"]):
+            assert max_rel(gv, decode(want)) <= 1e-12, case["fn"]
