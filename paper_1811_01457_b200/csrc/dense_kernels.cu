@@ -303,6 +303,83 @@ __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T*
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * -(double)scale;
 }
 
+// softmax cross-entropy for narrow heads (N <= 128): one warp per row, a
+// 32-warp block per 32-row group, so every row's dependent chain (max ->
+// exp-sum -> log -> probabilities) runs concurrently; the group's column sums
+// and loss are reduced through shared memory in a fixed order.
+template <class T>
+__global__ void __launch_bounds__(1024) k_softmax_xent_rows(const T* z, long long ldz, const T* y, long long ldy,
+                                                            long long M, long long N, T scale, void* dz, int dzd,
+                                                            long long lddz, void* dz2, int dz2d, long long lddz2,
+                                                            float* colsum, long long ldc, double* loss_part) {
+  __shared__ float cs[32][129];
+  __shared__ double red[32];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const long long r = blockIdx.x * 32ll + w;
+  const int nt = (int)((N + 31) / 32);  // <= 4
+  double l = 0.0;
+  T zc[4], yc[4];
+  if (r < M) {
+    T mx = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const long long c = lane + 32ll * t;
+      const bool ok = t < nt && c < N;
+      zc[t] = ok ? z[r * ldz + c] : (T)-INFINITY;
+      yc[t] = ok ? y[r * ldy + c] : (T)0;
+      mx = max(mx, zc[t]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    T se = 0, sy = 0, syz = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (t < nt && lane + 32 * t < N) {
+        const T d = zc[t] - mx;
+        se += exp(d);
+        sy += yc[t];
+        syz += yc[t] * d;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      se += __shfl_xor_sync(0xffffffffu, se, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      syz += __shfl_xor_sync(0xffffffffu, syz, o);
+    }
+    const T lse = log(se);
+    l = (double)(sy * lse - syz);  // -sum y (z - mx - lse)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const long long c = lane + 32ll * t;
+      if (t < nt && c < N) {
+        const T v = (exp(zc[t] - mx - lse) * sy - yc[t]) * scale;
+        st_as(dz, dzd, r * lddz + c, (double)v);
+        if (dz2) st_as(dz2, dz2d, r * lddz2 + c, (double)v);
+        cs[w][c] = (float)v;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (lane + 32 * t < 129) cs[w][lane + 32 * t] = 0.0f;
+  }
+  if (lane == 0) red[w] = l;
+  __syncthreads();
+  if (colsum) {
+    for (int c = threadIdx.x; c < N; c += 1024) {
+      float acc = 0.0f;
+      for (int i = 0; i < 32; ++i) acc += cs[i][c];  // fixed order over the group's rows
+      colsum[blockIdx.x * ldc + c] = acc;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int i = 0; i < 32; ++i) s2 += red[i];
+    loss_part[blockIdx.x] = s2 * (double)scale;
+  }
+}
+
 // softmax cross-entropy, warp per row (N <= 1024):
 //   loss_row = -sum_j y_j log p_j ; dz = (p * sum_j y_j - y) * scale  (scale = 1/n)
 // Lanes own columns lane + 32t; each warp walks 32 consecutive rows so the
@@ -578,6 +655,17 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
       dk::k_bce<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
                                                       (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
                                                       colsum, ld_colsum, loss_part);
+  } else if (kind == SG_LOSS_SOFTMAX_XENT && N <= 128) {
+    blocks = (M + 31) / 32;
+    if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
+    if (dtype == SG_F64)
+      dk::k_softmax_xent_rows<double><<<(unsigned)blocks, 1024, 0, st>>>(
+          (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
+          colsum, ld_colsum, loss_part);
+    else
+      dk::k_softmax_xent_rows<float><<<(unsigned)blocks, 1024, 0, st>>>(
+          (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
+          ld_dz2, colsum, ld_colsum, loss_part);
   } else if (kind == SG_LOSS_SOFTMAX_XENT) {
     if (N > 1024) return fail(SG_EINVAL, "softmax_xent: at most 1024 classes");
     blocks = (M + 255) / 256;
