@@ -15,24 +15,25 @@ namespace sg {
 
 namespace {
 
-// out[j] = sum_g part[g*N + j]: 32 columns x 8 row-groups per block; each
-// thread folds g = ty, ty+8, ... ascending, then a fixed fold over ty.
+// out[j] = sum_g part[g*N + j]: 32 columns x 32 row-groups per block (many
+// independent loads in flight per column strip); each thread folds
+// g = ty, ty+32, ... ascending, then a fixed fold over ty.
 template <class T>
-__global__ void __launch_bounds__(256) k_sum_cols(const double* __restrict__ part, long long G, long long N,
-                                                  T* __restrict__ out) {
-  __shared__ double red[8][33];
+__global__ void __launch_bounds__(1024) k_sum_cols(const double* __restrict__ part, long long G, long long N,
+                                                   T* __restrict__ out) {
+  __shared__ double red[32][33];
   const long long j = blockIdx.x * 32ll + threadIdx.x;
   double acc = 0.0;
   if (j < N) {
 #pragma unroll 4
-    for (long long g = threadIdx.y; g < G; g += 8) acc += part[g * N + j];
+    for (long long g = threadIdx.y; g < G; g += 32) acc += part[g * N + j];
   }
   red[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && j < N) {
     double s = red[0][threadIdx.x];
 #pragma unroll
-    for (int y = 1; y < 8; ++y) s += red[y][threadIdx.x];
+    for (int y = 1; y < 32; ++y) s += red[y][threadIdx.x];
     out[j] = (T)s;
   }
 }
@@ -151,12 +152,12 @@ int launch_sum_partials(const double* part, long long G, long long N, void* out,
     if (blockwise)
       k_sum_block<float><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (float*)out);
     else
-      k_sum_cols<float><<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, s>>>(part, G, N, (float*)out);
+      k_sum_cols<float><<<(unsigned)((N + 31) / 32), dim3(32, 32), 0, s>>>(part, G, N, (float*)out);
   } else {
     if (blockwise)
       k_sum_block<double><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (double*)out);
     else
-      k_sum_cols<double><<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, s>>>(part, G, N, (double*)out);
+      k_sum_cols<double><<<(unsigned)((N + 31) / 32), dim3(32, 32), 0, s>>>(part, G, N, (double*)out);
   }
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
