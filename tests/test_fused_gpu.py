@@ -219,3 +219,49 @@ def test_fuzz_corpus_matches_reference():
         for c, g in zip(cots, case["partials"]):
             worst = max(worst, max_rel(c, decode(g)))
     assert worst <= 1e-11, worst
+
+
+def test_c2_full_size_against_fp64(fused_module):
+    """BASELINE c2 at its full size (2^28 fp32 elements, a, b of shape (4096,)):
+    the device path vs an fp64 evaluation of the same op (torch, test-side
+    only): y and xbar elementwise <= 1e-6 (reference rel metric), abar/bbar (65536-term column
+    sums) within 1e-6 * sum|terms|; the 8-chunk row split the e2e bench uses
+    gives the same xbar bit for bit."""
+    R, C = 1 << 16, 1 << 12
+    g = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.rand((R, C), generator=g, device="cuda") * 4 - 2
+    yb = torch.rand((R, C), generator=g, device="cuda") * 2 - 1
+    a = torch.rand(C, generator=g, device="cuda") * 4 - 2
+    b = torch.rand(C, generator=g, device="cuda") * 4 - 2
+    y, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", [a, x, b], yb, want_primal=True)
+    # fp64 restatement, row block by row block (bounded memory)
+    abs_a = torch.zeros(C, dtype=torch.float64, device="cuda")
+    abs_b = torch.zeros_like(abs_a)
+    ref_a = torch.zeros_like(abs_a)
+    ref_b = torch.zeros_like(abs_a)
+    worst_y = worst_x = 0.0
+    for r0 in range(0, R, 8192):
+        xs, ys = x[r0:r0 + 8192].double(), yb[r0:r0 + 8192].double()
+        s = torch.sigmoid(a.double() * xs + b.double())
+        ds = s * (1 - s)
+        # the reference suite's metric |u - v| / max(1, |u|, |v|) (conftest.py:137-144)
+        gy, want_x = y[r0:r0 + 8192].double(), ys * ds * a.double()
+        gx = dx[r0:r0 + 8192].double()
+        worst_y = max(worst_y, float(((gy - s).abs() / torch.maximum(gy.abs(), s.abs()).clamp_min(1.0)).max()))
+        worst_x = max(worst_x, float(((gx - want_x).abs()
+                                      / torch.maximum(gx.abs(), want_x.abs()).clamp_min(1.0)).max()))
+        ta, tb = ys * ds * xs, ys * ds
+        ref_a += ta.sum(0)
+        ref_b += tb.sum(0)
+        abs_a += ta.abs().sum(0)
+        abs_b += tb.abs().sum(0)
+    assert worst_y <= 1e-6 and worst_x <= 1e-6, (worst_y, worst_x)
+    assert bool(((da.double() - ref_a).abs() <= 1e-6 * abs_a.clamp_min(1.0)).all())
+    assert bool(((db.double() - ref_b).abs() <= 1e-6 * abs_b.clamp_min(1.0)).all())
+    # the chunked public-API path of the e2e bench
+    dx2 = torch.empty_like(dx)
+    for r0 in range(0, R, R // 8):
+        _, (_, part, _) = F.fused_map_grad(fused_module, "affsig", [a, x[r0:r0 + R // 8], b],
+                                           yb[r0:r0 + R // 8])
+        dx2[r0:r0 + R // 8] = part
+    assert torch.equal(dx, dx2)
