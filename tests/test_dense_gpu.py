@@ -254,3 +254,34 @@ def test_dense_abi_backward_without_fused_partials(precision):
         cs = torch.zeros(((B + 31) // 32, fo), device="cuda")
         with pytest.raises(ValueError, match="tensor-core"):
             dense_backward(d, dZ, dW, db, colsum_in=cs)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_dense_layer_c3_full_size(precision):
+    """BASELINE c3 at its full size (Dense 4096->4096, batch 8192, sigmoid):
+    forward and pullback vs an fp64 evaluation of the same layer on the same
+    (bf16-rounded / fp32) operands (torch, test-side only)."""
+    M, D = 8192, 4096
+    g = torch.Generator(device="cuda").manual_seed(7)
+    layer = DenseLayer(M, D, D, "sigmoid", precision=precision)
+    r = (6.0 / (2 * D)) ** 0.5
+    W = (torch.rand((D, D), generator=g, device="cuda") * 2 - 1) * r
+    b = (torch.rand(D, generator=g, device="cuda") * 2 - 1) * 0.01
+    layer.set_params(W.cpu().numpy(), b.cpu().numpy())
+    X = (torch.rand((M, D), generator=g, device="cuda") * 2 - 1).to(layer.X.dtype)
+    ybar = torch.rand((M, D), generator=g, device="cuda") * 2 - 1
+    H = layer.forward(X).double()
+    dX, dW, db = (t.double() for t in layer.pullback(ybar))
+    torch.cuda.synchronize()
+    x64, w64 = X.double(), layer.Wb.double()
+    s = torch.sigmoid(x64 @ w64.T + b.double())
+    dz = ybar.double() * s * (1 - s)
+
+    def nrel_t(u, v):
+        return float((u - v).abs().max() / v.abs().max())
+
+    tol = TOL[precision]
+    assert nrel_t(H, s) <= tol
+    assert nrel_t(dX, dz @ w64) <= tol
+    assert nrel_t(dW, dz.T @ x64) <= tol
+    assert nrel_t(db, dz.sum(0)) <= tol
