@@ -55,6 +55,24 @@ class DataParallel:
         self.dist.broadcast(P, src=src, group=self.group)
 
 
+def nccl_unique_id(group=None) -> bytes:
+    """Rank 0's 128-byte NCCL id (``sg_dp_unique_id``), broadcast to every
+    rank of ``group`` over the host rendezvous (host-only: runs on gloo too)."""
+    import torch.distributed as dist
+
+    from . import runtime as rt
+
+    lib = rt.load_library()
+    lib.sg_dp_unique_id.argtypes = [ctypes.POINTER(ctypes.c_uint8), ctypes.c_size_t]
+    uid = (ctypes.c_uint8 * 128)()
+    if dist.get_rank(group) == 0:
+        rt.check(lib.sg_dp_unique_id(uid, 128), "sg_dp_unique_id")
+    box = [bytes(uid)]
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast_object_list(box, src=src, group=group)
+    return box[0]
+
+
 class NcclDataParallel:
     """The same bucketed all-reduce through the library's own NCCL
     communicator (``sg_dp_*``, include/sgb200.h): each bucket forks from the
@@ -85,13 +103,7 @@ class NcclDataParallel:
         lib.sg_dp_wait.argtypes = [P, P]
         lib.sg_dp_finalize.argtypes = [P]
         self.lib = lib
-        uid = (ctypes.c_uint8 * 128)()
-        if self.rank == 0:
-            rt.check(lib.sg_dp_unique_id(uid, 128), "sg_dp_unique_id")
-        box = [bytes(uid)]
-        src = 0 if group is None else dist.get_global_rank(group, 0)
-        dist.broadcast_object_list(box, src=src, group=group)
-        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_unique_id(group))
         h = ctypes.c_void_p()
         rt.check(lib.sg_dp_init(rt.context(), uid, 128, self.rank, self.world, ctypes.byref(h)), "sg_dp_init")
         self.handle = h

@@ -114,3 +114,41 @@ def test_layout_matches_engine_rule():
     n, segs = _layout((784, 32, 10))
     assert all(wo % 64 == 0 and bo % 64 == 0 for wo, bo, _, _ in segs)
     assert n % 64 == 0
+
+
+def _id_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_01457_b200.train import nccl_unique_id
+
+        q.put((rank, nccl_unique_id()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_unique_id_rendezvous():
+    """The NCCL communicator's rendezvous (train.nccl_unique_id): every rank
+    receives rank 0's 128-byte id from sg_dp_unique_id (host-only path)."""
+    from paper_1811_01457_b200 import runtime as rt
+
+    try:
+        if not rt.load_library().sg_dp_available():
+            pytest.skip("libnccl.so.2 not found")
+    except rt.RuntimeUnavailable:
+        pytest.skip("library not built")
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    ids = dict(q.get(timeout=10) for _ in range(world))
+    for p in procs:
+        assert p.exitcode == 0
+    assert len(ids[0]) == 128 and any(ids[0])
+    assert ids[0] == ids[1] == ids[2]
