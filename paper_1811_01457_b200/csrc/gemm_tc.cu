@@ -242,6 +242,7 @@ struct KParams {
   long long ld_part;
   int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
   int aux_stage;        // ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot
+  int raster;           // CTA-pair kernel: M-tiles per raster group
   int batch;            // independent GEMMs (bmm lanes), >= 1
   long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
 };
@@ -685,7 +686,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     kb1 = min(num_kb_total, kb0 + p.kb_per_split);
   };
   auto coord = [&](int t) {
-    constexpr int G = 8;  // grouped raster over 256-row pair tiles
+    const int G = p.raster;  // grouped raster over 256-row pair tiles
     const int u = (t % out_tiles) % tiles_pb;
     const int per_group = G * n_tiles;
     const int group = u / per_group;
@@ -1049,7 +1050,8 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, g.batch, g.so_f32, g.so_lp};
+  if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
   aux_map(g, p, maux);
@@ -1105,7 +1107,8 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, g.batch, g.so_f32, g.so_lp};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, g.batch, g.so_f32, g.so_lp};
+  if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
   aux_map(g, p, maux);
