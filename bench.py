@@ -250,37 +250,53 @@ def broadcast_bench(args, world, rank, local, dist):
 
     # pipelined e2e: row chunks on three streams so H2D of chunk i+1, the
     # kernels of chunk i and D2H of chunk i-1 overlap (PCIe is full duplex);
-    # the broadcast-axis cotangents are summed over chunks with reduce_to
-    nch = 8 if R % 8 == 0 else 1
+    # the broadcast-axis cotangents are summed over chunks with reduce_to.
+    # Consecutive steps overlap too: a chunk's buffers are reused as soon as
+    # the previous step is done with them (per-chunk events guard the
+    # write-after-read hazards), so the pipeline fills once per timed run.
+    nch = next(c for c in (32, 16, 8, 1) if R % c == 0)
     rc = R // nch
     s_in, s_cp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     apart = torch.empty((nch, C), device="cuda")
     bpart = torch.empty((nch, C), device="cuda")
+    read_done = [None] * nch   # kernels of the previous step finished reading dx_in/dyb_in[chunk]
+    out_done = [None] * nch    # D2H of the previous step finished reading y/xbar[chunk]
+    red_done = [None]          # previous step's abar/bbar copied out
 
     def e2e_pipelined():
         start_ev = torch.cuda.Event()
         start_ev.record(stream)
-        for s in (s_in, s_cp, s_out):
-            s.wait_event(start_ev)
+        for st in (s_in, s_cp, s_out):
+            st.wait_event(start_ev)
         for i in range(nch):
             sl = slice(i * rc, (i + 1) * rc)
             with torch.cuda.stream(s_in):
+                if read_done[i] is not None:
+                    s_in.wait_event(read_done[i])
                 dx_in[sl].copy_(hx[sl], non_blocking=True)
                 dyb_in[sl].copy_(hyb[sl], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(s_in)
             s_cp.wait_event(ev_in)
+            if out_done[i] is not None:
+                s_cp.wait_event(out_done[i])
             with torch.cuda.stream(s_cp):
                 F.fused_map(module, "affsig", [a, dx_in[sl], b], out=y[sl], check=False, stream=s_cp)
                 F.fused_map_grad(module, "affsig", [a, dx_in[sl], b], dyb_in[sl], check=False, stream=s_cp,
                                  outs=[apart[i], xbar[sl], bpart[i]])
                 ev_c = torch.cuda.Event()
                 ev_c.record(s_cp)
+            read_done[i] = ev_c
             s_out.wait_event(ev_c)
             with torch.cuda.stream(s_out):
                 hy[sl].copy_(y[sl], non_blocking=True)
                 hxb[sl].copy_(xbar[sl], non_blocking=True)
+                ev_o = torch.cuda.Event()
+                ev_o.record(s_out)
+            out_done[i] = ev_o
         with torch.cuda.stream(s_cp):
+            if red_done[0] is not None:
+                s_cp.wait_event(red_done[0])
             F.reduce_to(apart, (C,), out=abar, stream=s_cp)
             F.reduce_to(bpart, (C,), out=bbar, stream=s_cp)
             ev_r = torch.cuda.Event()
@@ -289,20 +305,48 @@ def broadcast_bench(args, world, rank, local, dist):
         with torch.cuda.stream(s_out):
             ha.copy_(abar, non_blocking=True)
             hb.copy_(bbar, non_blocking=True)
-        for s in (s_in, s_cp, s_out):
-            stream.wait_stream(s)
+            ev_ro = torch.cuda.Event()
+            ev_ro.record(s_out)
+        red_done[0] = ev_ro
+
+    def join_all():
+        for st in (s_in, s_cp, s_out):
+            stream.wait_stream(st)
 
     e2e_pipelined()
+    join_all()
     torch.cuda.synchronize()
     barrier(dist)
     s3, t3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s3.record(stream)
     for _ in range(e2e_steps):
         e2e_pipelined()
+    join_all()
     t3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(dist, s3.elapsed_time(t3)) / e2e_steps
     F.check_errors(module, "affsig")
+
+    # the host link the e2e number is bound by: concurrent H2D + D2H of 256 MB chunks
+    # of the same pinned buffers (PCIe is full duplex)
+    pc = min(n, 64 << 20)
+    pcie_in, pcie_out = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(2):
+        sp, tp = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sp.record(stream)
+        pcie_in.wait_event(sp)
+        pcie_out.wait_event(sp)
+        with torch.cuda.stream(pcie_in):
+            for k in range(4):
+                dx_in.view(-1)[:pc].copy_(hx.view(-1)[:pc], non_blocking=True)
+        with torch.cuda.stream(pcie_out):
+            for k in range(4):
+                hy.view(-1)[:pc].copy_(y.view(-1)[:pc], non_blocking=True)
+        stream.wait_stream(pcie_in)
+        stream.wait_stream(pcie_out)
+        tp.record(stream)
+        torch.cuda.synchronize()
+    pcie_gbps = 4 * pc * 4 / (sp.elapsed_time(tp) * 1e-3) / 1e9  # per direction, both running
 
     peaks = load_peaks()
     grad_bytes = 12 * n
@@ -336,7 +380,9 @@ def broadcast_bench(args, world, rank, local, dist):
         "e2e": {"value": round(world * n * BYTES_PER_ELEM / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": f"fused_map + fused_map_grad public API on {nch} row chunks, pinned host buffers, "
-                        "H2D / kernels / D2H overlapped on three streams",
+                        "H2D / kernels / D2H overlapped on three streams (also across steps)",
+                "pcie_GBps_per_direction_measured": round(pcie_gbps, 1),
+                "pcie_bound_ms": round(max(h2d, d2h) / (pcie_gbps * 1e9) * 1e3, 2),
                 "serial_ms_per_step": round(e2e_serial_ms, 3),
                 "serial_value": round(world * n * BYTES_PER_ELEM / (e2e_serial_ms * 1e-3) / 1e9, 2)},
         "gpu_launches": 4 * args.steps,
