@@ -186,6 +186,21 @@ int broadcast_shape(int k, const sg_tensor* args, std::vector<long long>& out) {
 }
 
 // Collapse the broadcast to out[R][C] with one kind per operand.
+// A 1-D problem (every operand full-shaped or a single element) has no
+// preferred 2-D shape: fold it into rows of a wide power-of-two width so the
+// kernels get their usual long per-thread row walks (scalar cotangents then
+// accumulate in registers over many rows instead of one block reduction per
+// 1024 elements).
+void fold_rows(Shape2D& s) {
+  if (s.R != 1 || s.C < (1ll << 16)) return;
+  for (long long w = 4096; w >= 256; w >>= 1)
+    if (s.C % w == 0) {
+      s.R = s.C / w;
+      s.C = w;
+      return;
+    }
+}
+
 void canonicalise(int k, const sg_tensor* args, const std::vector<long long>& out, Shape2D& s) {
   const int n = (int)out.size();
   for (int i = 0; i < k; ++i) s.expand[i] = false;
@@ -231,6 +246,7 @@ void canonicalise(int k, const sg_tensor* args, const std::vector<long long>& ou
       else if (numel(args[i]) == 1) s.kinds[i] = SG_SPTR;
       else s.kinds[i] = SG_FULL;
     }
+    fold_rows(s);
     return;
   }
   if (groups.empty()) groups.push_back({0u, 1});
@@ -242,6 +258,7 @@ void canonicalise(int k, const sg_tensor* args, const std::vector<long long>& ou
       else if (groups[0].mask & (1u << i)) s.kinds[i] = SG_SPTR;
       else s.kinds[i] = SG_FULL;
     }
+    fold_rows(s);
     return;
   }
   s.R = groups[0].ext;
@@ -279,6 +296,7 @@ struct Launch {
   int vec, bdx, bdy;
   unsigned gx, gy;
   long long rpb;
+  int rowmode = 0;  // gradient kernel: one warp per row (COL operands, no ROW operands)
 };
 
 long long env_ll(const char* name, long long dflt) {
@@ -325,7 +343,7 @@ Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* arg
 
 std::string variant_key(int k, const int* kinds, const Launch& L) {
   std::ostringstream key;
-  key << "v" << L.vec << "x" << L.bdx << "y" << L.bdy << "k";
+  key << "v" << L.vec << "x" << L.bdx << "y" << L.bdy << (L.rowmode ? "r" : "") << "k";
   for (int i = 0; i < k; ++i) key << kinds[i];
   return key.str();
 }
@@ -341,6 +359,7 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   bool has_col = false;
   for (int i = 0; i < k; ++i) has_col |= kinds[i] == SG_COL;
   src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n";
+  src << "#define SG_ROWMODE " << L.rowmode << "\n";
   // tuning overrides, e.g. SGB200_EW_DEFINES="#define SG_UNROLL 8"
   if (const char* extra = std::getenv("SGB200_EW_DEFINES")) src << extra << "\n";
   src << "#define SG_KINDS {";
@@ -629,6 +648,24 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   for (int i = 0; i < k; ++i) extra.push_back(s.kinds[i] == SG_FULL ? argbars[i].ptr : nullptr);
   Launch L = plan(ctx, s, kern->dtype, args, k, extra.data(), (int)extra.size(),
                   env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", 8), env_ll("SGB200_EW_GRAD_BDX", 256));
+  // COL operands without ROW operands: warps own rows and walk the columns, so
+  // each row's cotangent is one register accumulation + one warp reduction
+  // (instead of a shuffle tree per 128 elements) and is written final.
+  bool has_col = false, has_row = false;
+  for (int i = 0; i < k; ++i) {
+    has_col |= s.kinds[i] == SG_COL;
+    has_row |= s.kinds[i] == SG_ROW;
+  }
+  if (has_col && !has_row && s.C >= 32ll * L.vec && env_ll("SGB200_EW_ROWMODE", 1)) {
+    L.rowmode = 1;
+    L.bdx = 256;
+    L.bdy = 1;
+    L.gx = 1;
+    const long long warps = (s.R + 7) / 8;
+    L.gy = (unsigned)std::max<long long>(1, std::min<long long>(
+        {warps, (long long)ctx->num_sms * env_ll("SGB200_EW_ROWMODE_BLOCKS_PER_SM", 8), 65535ll}));
+    L.rpb = 0;
+  }
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -638,7 +675,7 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   pr.p.out = y ? y->ptr : nullptr;
   long long total = s.R * s.C;
   const long long G_row = (long long)L.gy * L.bdy;
-  const long long G_col = (long long)L.gx * L.bdx / std::min(32, L.bdx);
+  const long long G_col = L.rowmode ? 1 : (long long)L.gx * L.bdx / std::min(32, L.bdx);
   const long long G_blk = (long long)L.gx * L.gy;
   std::vector<void*> parts;
   for (int i = 0; i < k; ++i) {

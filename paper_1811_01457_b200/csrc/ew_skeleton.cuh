@@ -276,9 +276,50 @@ sg_ew_grad(const SgEwParams p) {
     for (int j = 0; j < SG_VEC; ++j) acc.row[i][j] = 0.0;
   }
   T inv[SG_KT][SG_VEC];
-  if (active) sg_load_invariant(p, c, inv);
+  if (active || SG_ROWMODE) sg_load_invariant(p, SG_ROWMODE ? 0 : c, inv);  // row mode: scalars only
 
-#if !SG_HAS_COL
+#if SG_ROWMODE
+  // one warp per row, lanes walk the columns: COL cotangents accumulate in a
+  // register over the whole row, one warp reduction per row, written final
+  // (part[i][r], a single partial group).  ROW operands never take this path.
+  {
+    const int lane = tx % 32, wib = tx / 32;
+    const int warps = (SG_BDX * SG_BDY) / 32;
+    const long long rstride = (long long)gridDim.y * warps;
+    constexpr long long CSTEP = 32ll * SG_VEC;
+    for (long long r = (long long)blockIdx.y * warps + wib; r < p.R; r += rstride) {
+      double colsum[SG_KT];
+#pragma unroll
+      for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
+      long long c0 = (long long)lane * SG_VEC;
+      for (; c0 + (SG_GUNROLL - 1) * CSTEP < p.C; c0 += SG_GUNROLL * CSTEP) {
+        T xs[SG_GUNROLL][SG_KT][SG_VEC];
+        VT yb[SG_GUNROLL];
+#pragma unroll
+        for (int u = 0; u < SG_GUNROLL; ++u) {
+          sg_load_row(p, r, c0 + u * CSTEP, inv, xs[u]);
+          yb[u] = sg_ldv_stream(ybar + r * p.C + c0 + u * CSTEP);
+        }
+#pragma unroll
+        for (int u = 0; u < SG_GUNROLL; ++u) sg_grad_row(p, r, c0 + u * CSTEP, xs[u], yb[u], acc, colsum);
+      }
+      for (; c0 < p.C; c0 += CSTEP) {
+        T xs[SG_KT][SG_VEC];
+        sg_load_row(p, r, c0, inv, xs);
+        const VT yb = sg_ldv_stream(ybar + r * p.C + c0);
+        sg_grad_row(p, r, c0, xs, yb, acc, colsum);
+      }
+#pragma unroll
+      for (int i = 0; i < SG_K; ++i) {
+        if (sg_kinds[i] != SG_COL) continue;
+        double sum = colsum[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
+        if (lane == 0) p.part[i][r] = sum;
+      }
+    }
+  }
+#elif !SG_HAS_COL
   // no cross-thread work per row: full chunks with all loads issued first
   if (active) {
     const long long n = w.n;
@@ -311,27 +352,36 @@ sg_ew_grad(const SgEwParams p) {
   constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
   // the block-uniform trip count: the longest walk of any ty in the block
   const long long rows_span = sg_rows(p, 0).n;
-  for (long long it = 0; it < rows_span; ++it) {
-    const long long r = w.base + it * w.stride;
-    const bool live = active && it < w.n;
-    double colsum[SG_KT];
+  const long long gi = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
+  // SG_GUNROLL rows per trip: every row's loads are issued before the first
+  // row is computed (the trip count stays block-uniform for the shuffles)
+  for (long long it = 0; it < rows_span; it += SG_GUNROLL) {
+    T xs[SG_GUNROLL][SG_KT][SG_VEC];
+    VT yb[SG_GUNROLL];
 #pragma unroll
-    for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
-    if (live) {
-      T xs[SG_KT][SG_VEC];
-      sg_load_row(p, r, c, inv, xs);
-      VT yb = sg_ldv_stream(ybar + r * p.C + c);
-      sg_grad_row(p, r, c, xs, yb, acc, colsum);
+    for (int u = 0; u < SG_GUNROLL; ++u) {
+      const long long r = w.base + (it + u) * w.stride;
+      if (active && it + u < w.n) {
+        sg_load_row(p, r, c, inv, xs[u]);
+        yb[u] = sg_ldv_stream(ybar + r * p.C + c);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < SG_K; ++i) {
-      if (sg_kinds[i] != SG_COL) continue;
-      double s = colsum[i];
+    for (int u = 0; u < SG_GUNROLL; ++u) {
+      if (it + u >= rows_span) break;  // block-uniform
+      const long long r = w.base + (it + u) * w.stride;
+      const bool live = active && it + u < w.n;
+      double colsum[SG_KT];
 #pragma unroll
-      for (int off = kGroup / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, kGroup);
-      if (live && (tx % kGroup) == 0) {
-        const long long gi = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
-        p.part[i][gi * p.R + r] = s;
+      for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
+      if (live) sg_grad_row(p, r, c, xs[u], yb[u], acc, colsum);
+#pragma unroll
+      for (int i = 0; i < SG_K; ++i) {
+        if (sg_kinds[i] != SG_COL) continue;
+        double sum = colsum[i];
+#pragma unroll
+        for (int off = kGroup / 2; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off, kGroup);
+        if (live && (tx % kGroup) == 0) p.part[i][gi * p.R + r] = sum;
       }
     }
   }
@@ -350,7 +400,7 @@ sg_ew_grad(const SgEwParams p) {
 #pragma unroll
   for (int i = 0; i < SG_K; ++i) {
     if (sg_kinds[i] != SG_SPTR && sg_kinds[i] != SG_SVAL) continue;
-    red[tid] = active ? acc.s[i] : 0.0;
+    red[tid] = (active || SG_ROWMODE) ? acc.s[i] : 0.0;
     __syncthreads();
     for (int s = (SG_BDX * SG_BDY) / 2; s > 0; s >>= 1) {
       if (tid < s) red[tid] += red[tid + s];

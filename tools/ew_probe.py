@@ -60,3 +60,18 @@ f = timeit(lambda: torch.mul(x, 2.0, out=y))
 print(f"torch mul 1R1W {f:.4f} ms {8 * n / f / 1e6:.1f} GB/s")
 f = timeit(lambda: torch.mul(x, yb, out=y))
 print(f"torch mul 2R1W {f:.4f} ms {12 * n / f / 1e6:.1f} GB/s")
+
+# c2 variants of SURVEY §8(d): scalar a, b (full-reduction gradients) and (R,1) a, b (row reductions)
+ac = torch.rand((R, 1), generator=g, device="cuda") * 4 - 2
+bc = torch.rand((R, 1), generator=g, device="cuda") * 4 - 2
+abar_c, bbar_c = torch.empty_like(ac), torch.empty_like(bc)
+a1, b1 = torch.rand(1, generator=g, device="cuda") * 4 - 2, torch.rand(1, generator=g, device="cuda") * 4 - 2
+abar_1, bbar_1 = torch.empty_like(a1), torch.empty_like(b1)
+for label, args, outs in (("(R,1) a,b", [ac, x, bc], [abar_c, xbar, bbar_c]),
+                          ("1-elem a,b", [a1, x, b1], [abar_1, xbar, bbar_1])):
+    f = timeit(lambda: F.fused_map(m, "affsig", args, out=y, check=False))
+    gr = timeit(lambda: F.fused_map_grad(m, "affsig", args, yb, check=False, outs=outs))
+    print(f"{label:10s} K1 {f:.4f} ms {8 * n / f / 1e6:7.1f} GB/s | K2 {gr:.4f} ms {12 * n / gr / 1e6:7.1f} GB/s")
+f = timeit(lambda: F.fused_map(m, "affsig", [0.7, x, -0.3], out=y, check=False))
+gr = timeit(lambda: F.fused_map_grad(m, "affsig", [0.7, x, -0.3], yb, check=False))
+print(f"{'f64 a,b':10s} K1 {f:.4f} ms {8 * n / f / 1e6:7.1f} GB/s | K2 {gr:.4f} ms {12 * n / gr / 1e6:7.1f} GB/s")
