@@ -458,6 +458,58 @@ def _timed(fn, steps, warmup, dist, stream, per_step_events=None):
     return max_over_ranks(dist, s.elapsed_time(t)) / steps, evs
 
 
+def broadcast_variant_bench(args, dist, peaks, variant):
+    """SURVEY §8(d) c2 variants at the full 2^28 size: scalar a, b (f64 by value;
+    full-reduction cotangents) or (R,1) a, b (row reductions)."""
+    import statistics
+
+    import torch
+
+    from paper_1811_01457_b200 import fused as F
+    from paper_1811_01457_b200.irtext import parse_ir
+
+    module = parse_ir(AFFSIG)
+    R, C = args.rows, C_COLS
+    n = R * C
+    g = torch.Generator(device="cuda").manual_seed(4321)
+    x = torch.rand((R, C), generator=g, device="cuda") * 4 - 2
+    yb = torch.rand((R, C), generator=g, device="cuda") * 2 - 1
+    y, xbar = torch.empty_like(x), torch.empty_like(x)
+    if variant == "scalar":
+        a, b = 0.7, -0.3
+        abar, bbar = torch.empty(1, device="cuda"), torch.empty(1, device="cuda")
+        desc = "a, b f64 scalars (full-reduction cotangents)"
+    else:
+        a = torch.rand((R, 1), generator=g, device="cuda") * 4 - 2
+        b = torch.rand((R, 1), generator=g, device="cuda") * 4 - 2
+        abar, bbar = torch.empty_like(a), torch.empty_like(b)
+        desc = "a, b of shape (R,1) (row-reduction cotangents)"
+    stream = torch.cuda.current_stream()
+
+    def step(ev):
+        if ev: ev[0].record(stream)
+        F.fused_map(module, "affsig", [a, x, b], out=y, check=False)
+        if ev: ev[1].record(stream)
+        F.fused_map_grad(module, "affsig", [a, x, b], yb, check=False, outs=[abar, xbar, bbar])
+        if ev: ev[2].record(stream)
+
+    ms, evs = _timed(step, max(5, args.dense_steps), args.warmup, dist, stream, per_step_events=3)
+    F.check_errors(module, "affsig")
+    fwd = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    grad = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    return {
+        "workload": f"c2 variant: sigma.(a.*x.+b) + gradient, 2^28 fp32, {desc}",
+        "value": round(n * BYTES_PER_ELEM / (ms * 1e-3) / 1e9, 1), "unit": "GB/s", "ms_per_step": round(ms, 4),
+        "kernels_ms": {"fwd_K1": round(fwd, 4), "grad_K2_plus_finalize": round(grad, 4),
+                       "fwd_GBps": round(8 * n / (fwd * 1e-3) / 1e9, 1),
+                       "grad_GBps": round(12 * n / (grad * 1e-3) / 1e9, 1)},
+        "roofline": {"bound": "hbm", "kernel": "sg_ew_grad", "achieved": round(12 * n / (grad * 1e-3) / 1e9, 1),
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(12 * n / (grad * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
+        "gpu_launches_per_step": 3 if variant == "scalar" else 3,
+    }
+
+
 TF32_PEAK_TFLOPS = 1100.0  # B200_PROFILING.md dense TF32 figure (no measured TF32 peak in MEASURED_PEAKS.json)
 
 
@@ -576,6 +628,8 @@ def secondary_benches(args, world, rank, dist):
         try:
             if w == "c3" and world == 1:
                 out.append(dense_c3_bench(args, dist, peaks))
+            elif w in ("c2scalar", "c2col"):
+                out.append(broadcast_variant_bench(args, dist, peaks, "scalar" if w == "c2scalar" else "col"))
             elif w == "c3tf32" and world == 1:
                 out.append(dense_c3_bench(args, dist, peaks, precision="tf32"))
             elif w == "c4":
@@ -676,7 +730,7 @@ def main():
     ap.add_argument("--rows", type=int, default=R_ROWS)
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--secondary", default="c1,c3,c3tf32,c4,c5",
+    ap.add_argument("--secondary", default="c2scalar,c2col,c1,c3,c3tf32,c4,c5",
                     help="comma list of extra workloads measured in the same run (c1,c3,c4,c5)")
     ap.add_argument("--dense-steps", type=int, default=20)
     ap.add_argument("--mlp-steps", type=int, default=10)
