@@ -358,7 +358,9 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   src << "#define SG_VEC " << L.vec << "\n#define SG_BDX " << L.bdx << "\n#define SG_BDY " << L.bdy << "\n";
   bool has_col = false;
   for (int i = 0; i < k; ++i) has_col |= kinds[i] == SG_COL;
-  src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n";
+  bool has_row = false;
+  for (int i = 0; i < k; ++i) has_row |= kinds[i] == SG_ROW;
+  src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n#define SG_HAS_ROW " << (has_row ? 1 : 0) << "\n";
   src << "#define SG_ROWMODE " << L.rowmode << "\n";
   // tuning overrides, e.g. SGB200_EW_DEFINES="#define SG_UNROLL 8"
   if (const char* extra = std::getenv("SGB200_EW_DEFINES")) src << extra << "\n";

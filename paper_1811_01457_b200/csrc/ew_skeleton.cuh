@@ -25,7 +25,10 @@
 #define SG_UNROLL 4   // rows in flight per thread, forward
 #endif
 #ifndef SG_GUNROLL
-#define SG_GUNROLL 2  // rows in flight per thread, gradient (register budget)
+#define SG_GUNROLL 3  // rows in flight per thread, gradient (register budget)
+#endif
+#ifndef SG_RUNROLL
+#define SG_RUNROLL 2  // column chunks in flight per lane, gradient row mode
 #endif
 #ifndef SG_GRAD_MINB
 #define SG_GRAD_MINB 4
@@ -224,10 +227,30 @@ sg_ew_forward(const SgEwParams p) {
 //   SG_ROW:              part[(by*SG_BDY + ty) * C + c]      (G_row = gy*SG_BDY rows)
 //   SG_COL:              part[g * R + r], g = lane-group column id
 //   SG_SPTR / SG_SVAL:   part[by * gx + bx]                  (block partial)
+// SG_ROW_SMEM 1 (default): the per-column fp64 sums of ROW operands live in
+// shared memory (this thread's own slots) instead of registers -- frees 16
+// registers under the 64-register budget for a third row of loads in flight
+// (+2 % on c2, +9 % for cheaper sub-functions; tools/ew_sweep5.sh).
+#ifndef SG_ROW_SMEM
+#define SG_ROW_SMEM 1
+#endif
+#if !SG_HAS_ROW
+#undef SG_ROW_SMEM
+#define SG_ROW_SMEM 0
+#endif
 struct SgGradAcc {
+#if SG_ROW_SMEM
+  double* srow;               // srow[(i * SG_VEC + j) * SG_BDX * SG_BDY]
+#else
   double row[SG_KT][SG_VEC];  // ROW operands: per-column sums over my rows
+#endif
   double s[SG_KT];            // scalar operands
 };
+#if SG_ROW_SMEM
+#define SG_ACC_ROW(acc, i, j) (acc).srow[((i) * SG_VEC + (j)) * (SG_BDX * SG_BDY)]
+#else
+#define SG_ACC_ROW(acc, i, j) (acc).row[i][j]
+#endif
 
 // One row: duals, ybar contraction, xbar stores, accumulation.  Returns the
 // per-row sums for COL operands in colsum.
@@ -249,7 +272,7 @@ __device__ __forceinline__ void sg_grad_row(const SgEwParams& p, long long r, lo
       const T contrib = yb.v[j] * d[i];  // ybar .* partial_i (forward_ad.py:233)
       const int kind = sg_kinds[i];
       if (kind == SG_FULL) g[i].v[j] = contrib;
-      else if (kind == SG_ROW) acc.row[i][j] += (double)contrib;
+      else if (kind == SG_ROW) SG_ACC_ROW(acc, i, j) += (double)contrib;
       else if (kind == SG_COL) colsum[i] += (double)contrib;
       else acc.s[i] += (double)contrib;
     }
@@ -269,11 +292,15 @@ sg_ew_grad(const SgEwParams p) {
   const T* ybar = reinterpret_cast<const T*>(p.ybar);
 
   SgGradAcc acc;
+#if SG_ROW_SMEM
+  __shared__ double sg_srow[SG_KT * SG_VEC * SG_BDX * SG_BDY];
+  acc.srow = sg_srow + ty * SG_BDX + tx;
+#endif
 #pragma unroll
   for (int i = 0; i < SG_KT; ++i) {
     acc.s[i] = 0.0;
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) acc.row[i][j] = 0.0;
+    for (int j = 0; j < SG_VEC; ++j) SG_ACC_ROW(acc, i, j) = 0.0;
   }
   T inv[SG_KT][SG_VEC];
   if (active || SG_ROWMODE) sg_load_invariant(p, SG_ROWMODE ? 0 : c, inv);  // row mode: scalars only
@@ -292,16 +319,16 @@ sg_ew_grad(const SgEwParams p) {
 #pragma unroll
       for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
       long long c0 = (long long)lane * SG_VEC;
-      for (; c0 + (SG_GUNROLL - 1) * CSTEP < p.C; c0 += SG_GUNROLL * CSTEP) {
-        T xs[SG_GUNROLL][SG_KT][SG_VEC];
-        VT yb[SG_GUNROLL];
+      for (; c0 + (SG_RUNROLL - 1) * CSTEP < p.C; c0 += SG_RUNROLL * CSTEP) {
+        T xs[SG_RUNROLL][SG_KT][SG_VEC];
+        VT yb[SG_RUNROLL];
 #pragma unroll
-        for (int u = 0; u < SG_GUNROLL; ++u) {
+        for (int u = 0; u < SG_RUNROLL; ++u) {
           sg_load_row(p, r, c0 + u * CSTEP, inv, xs[u]);
           yb[u] = sg_ldv_stream(ybar + r * p.C + c0 + u * CSTEP);
         }
 #pragma unroll
-        for (int u = 0; u < SG_GUNROLL; ++u) sg_grad_row(p, r, c0 + u * CSTEP, xs[u], yb[u], acc, colsum);
+        for (int u = 0; u < SG_RUNROLL; ++u) sg_grad_row(p, r, c0 + u * CSTEP, xs[u], yb[u], acc, colsum);
       }
       for (; c0 < p.C; c0 += CSTEP) {
         T xs[SG_KT][SG_VEC];
@@ -392,7 +419,7 @@ sg_ew_grad(const SgEwParams p) {
     if (sg_kinds[i] != SG_ROW || !active) continue;
     const long long gi = (long long)blockIdx.y * SG_BDY + ty;
 #pragma unroll
-    for (int j = 0; j < SG_VEC; ++j) p.part[i][gi * p.C + c + j] = acc.row[i][j];
+    for (int j = 0; j < SG_VEC; ++j) p.part[i][gi * p.C + c + j] = SG_ACC_ROW(acc, i, j);
   }
   // scalar partials: block tree reduction in a fixed order
   __shared__ double red[SG_BDX * SG_BDY];
