@@ -104,6 +104,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// PDL (griddepcontrol): wait = the prerequisite grid has completed and its
+// memory is visible (a no-op without a programmatic dependency);
+// launch_dependents = the next kernel in the stream may start its prologue.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -450,6 +455,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the setup above (barriers, TMEM, descriptor
+  // prefetch) overlaps the previous kernel's tail; no global memory is touched
+  // before the previous grid has completed.
+  grid_dep_wait();
+  grid_dep_launch();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -726,6 +736,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   cluster_sync_all();  // barriers of both CTAs initialised before any remote traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  grid_dep_wait();  // see gemm_tc_kernel
+  grid_dep_launch();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -1004,6 +1016,28 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, in
   }
 }
 
+// Launch with a programmatic dependency on the previous kernel in the stream
+// (SGB200_GEMM_PDL=0 disables): the kernel's own griddepcontrol.wait orders
+// its memory accesses after the predecessor.
+template <class Kern, class... Args>
+cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("SGB200_GEMM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int launch_splitk_reduce(const float* part, int splits, const GemmArgs& g, long long ld_part,
                                 cudaStream_t st) {
   const unsigned gx = (unsigned)(((g.N + 3) / 4 + 255) / 256);
@@ -1063,7 +1097,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, maux, p);
+  SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
@@ -1120,7 +1154,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }
   const int work = tiles * splits;
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
-  kern<<<grid, tc::NUM_THREADS, SMEM, st>>>(ma, mb, mlp, mf32, maux, p);
+  SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
