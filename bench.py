@@ -163,6 +163,15 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- broadcast (c2)
+def c2_config(R, C, world):
+    """The headline workload's config, shared by both arms (the reference arm
+    measures the same workload on a bounded CPU sample, see cpu_baseline.sample)."""
+    return {"workload": "c2 fused broadcast sigma.(a.*x.+b) + gradient, 2^28 fp32 elements",
+            "shape": [R, C], "broadcast": "a,b of shape (4096,)",
+            "bytes_per_elem": BYTES_PER_ELEM, "l2": "inputs 1 GiB each > 126 MB L2, no flush",
+            "parallelism": f"replicas x{world}"}
+
+
 def broadcast_bench(args, world, rank, local, dist):
     import torch
 
@@ -364,10 +373,7 @@ def broadcast_bench(args, world, rank, local, dist):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded U[-2,2] inputs, U[-1,1] seed ybar)",
-        "config": {"workload": "c2 fused broadcast sigma.(a.*x.+b) + gradient, 2^28 fp32 elements",
-                   "shape": [R, C], "broadcast": "a,b of shape (4096,)",
-                   "bytes_per_elem": BYTES_PER_ELEM, "l2": "inputs 1 GiB each > 126 MB L2, no flush",
-                   "parallelism": f"replicas x{world}"},
+        "config": c2_config(R, C, world),
         "kernels_ms": {"fwd_K1": round(fwd_ms, 4), "grad_K2_plus_finalize": round(grad_ms, 4),
                        "fwd_GBps": round(8 * n / (fwd_ms * 1e-3) / 1e9, 1),
                        "grad_GBps": round(achieved, 1)},
@@ -708,7 +714,7 @@ def reference_arm(args, world, rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "c2 fused broadcast sigma.(a.*x.+b) + gradient (bounded CPU sample)"},
+        "config": c2_config(args.rows, C_COLS, world),
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "secondary": [
