@@ -14,7 +14,7 @@ $NCU --metrics gpu__time_duration.sum -c 60 --csv --log-file $O/launches_c2.csv 
   $B --steps 3 --warmup 3 --secondary none > /dev/null 2>&1
 $NCU --metrics gpu__time_duration.sum -k regex:'gemm|k_act|k_colsum|k_splitk' -c 40 --csv --log-file $O/launches_c3.csv \
   $B --steps 3 --warmup 3 --rows 1024 --secondary c3 > /dev/null 2>&1
-$NCU --metrics gpu__time_duration.sum -k regex:'gemm|k_act|k_colsum|k_splitk|k_mse|k_sgd|k_sum' -c 200 --csv \
+$NCU --metrics gpu__time_duration.sum -k regex:'gemm|k_act|k_colsum|k_splitk|k_mse|k_sgd|k_sum_loss' -c 300 --csv \
   --log-file $O/launches_c5.csv $B --steps 3 --warmup 3 --rows 1024 --secondary c5 > /dev/null 2>&1
 # full sections of the top kernels
 $NCU --set full --import-source on -k regex:'sg_ew_' -s 4 -c 2 -o $O/c2_ew -f \
