@@ -203,7 +203,7 @@ SG_API int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t l
  *                 p = sigmoid(z) clamped to [1e-7, 1-1e-7];
  *                 loss = -scale * sum y log p + (1-y) log(1-p);  dz = 0 where clamped
  * `loss` (device f64) receives the total; loss_part is scratch of n_part doubles
- * (>= ceil(N/32)*ceil(M/256) for MSE and BCE; ceil(M/32) for softmax).  Under data
+ * (>= ceil(N/32)*ceil(M/32) for MSE and BCE; ceil(M/32) for softmax).  Under data
  * parallelism scale = 1/global_batch so shard gradients sum to the full one. */
 SG_API int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_z, const void* y,
                    int64_t ld_y, int64_t M, int64_t N, double scale, double* loss, double* loss_part,

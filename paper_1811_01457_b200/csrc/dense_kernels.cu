@@ -111,40 +111,66 @@ __device__ __forceinline__ void st8(float* p, const V8& v) { st8_f32(p, v); }
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const V8& v) { st8_bf16(p, v); }
 
 // HT/DT: bf16 (BF16 tensor-core chain) or float (TF32 chain)
+// Block (64, 4): 512 columns (8 per thread) x one 32-row group, each ty a
+// quarter of the group's rows; the quarters' column sums are combined in
+// shared memory in a fixed order (one partial row per group).  Four times
+// the threads of a one-thread-per-32-rows layout: small batches still fill
+// the machine.
+__device__ __forceinline__ void quarter_colsum(float (&acc)[8], float* colsum, long long ldc, long long g,
+                                               long long c, bool ok) {
+  __shared__ float part[4][64][9];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[ty][tx][j] = acc[j];
+  __syncthreads();
+  if (ty == 0 && ok && colsum) {
+    V8 o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o.v[j] = ((part[0][tx][j] + part[1][tx][j]) + part[2][tx][j]) + part[3][tx][j];
+    st8_f32(colsum + g * ldc + c, o);
+  }
+}
+
 template <class HT, class DT>
 __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long long ldy, const HT* h,
                                                      long long ldh, long long M, long long N, int act,
                                                      DT* dz, long long lddz, float* colsum,
                                                      long long ldc) {
-  const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
-  if (c >= N) return;
-  const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
+  const long long c = (blockIdx.x * 64ll + threadIdx.x) * 8;
+  const bool ok = c < N;
+  const long long g = blockIdx.y, r0 = g * 32 + threadIdx.y * 8;
+  const long long r1 = r0 + 8 < M ? r0 + 8 : M;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ok) {
 #pragma unroll 4
-  for (long long r = r0; r < r1; ++r) {
-    const V8 yb = ld8_f32(ybar + r * ldy + c);
-    const V8 hv = ld8(h + r * ldh + c);
-    V8 o;
+    for (long long r = r0; r < r1; ++r) {
+      const V8 yb = ld8_f32(ybar + r * ldy + c);
+      const V8 hv = ld8(h + r * ldh + c);
+      V8 o;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      o.v[j] = yb.v[j] * act_grad_h(hv.v[j], act);
-      acc[j] += o.v[j];
+      for (int j = 0; j < 8; ++j) {
+        o.v[j] = yb.v[j] * act_grad_h(hv.v[j], act);
+        acc[j] += o.v[j];
+      }
+      st8(dz + r * lddz + c, o);
     }
-    st8(dz + r * lddz + c, o);
   }
-  if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
+  quarter_colsum(acc, colsum, ldc, g, c, ok);
 }
 
 template <class DT>
 __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, const float* y, long long ldy,
                                                 long long M, long long N, float scale, DT* dz,
                                                 long long lddz, float* colsum, long long ldc, double* loss_part) {
+  // block (64, 4) as k_act_grad_v8
   __shared__ double red[256];
-  const long long c = (blockIdx.x * 256ll + threadIdx.x) * 8;
-  const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
+  const long long c = (blockIdx.x * 64ll + threadIdx.x) * 8;
+  const bool ok = c < N;
+  const long long g = blockIdx.y, r0 = g * 32 + threadIdx.y * 8;
+  const long long r1 = r0 + 8 < M ? r0 + 8 : M;
   double lsum = 0.0;
-  if (c < N) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ok) {
 #pragma unroll 4
     for (long long r = r0; r < r1; ++r) {
       const V8 zv = ld8_f32(z + r * ldz + c);
@@ -161,15 +187,16 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
       lsum += (double)l;
       st8(dz + r * lddz + c, o);
     }
-    if (colsum) st8_f32(colsum + g * ldc + c, V8{{acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7]}});
   }
-  red[threadIdx.x] = lsum;
+  quarter_colsum(acc, colsum, ldc, g, c, ok);
+  const int tid = threadIdx.y * 64 + threadIdx.x;
+  red[tid] = lsum;
   __syncthreads();
   for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    if (tid < s) red[tid] += red[tid + s];
     __syncthreads();
   }
-  if (threadIdx.x == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+  if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
 }
 
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
@@ -549,13 +576,13 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
   if (ybar_dtype == SG_F32 && (h_dtype == SG_BF16 || h_dtype == SG_F32) && h_dtype == dz_dtype && !dz2 &&
       N % 8 == 0 && ld_y % 8 == 0 && ld_h % 8 == 0 && ld_dz % 8 == 0 && a16(ybar) && a16(h) && a16(dz) &&
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
-    dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
+    dim3 g8((unsigned)((N + 511) / 512), (unsigned)((M + 31) / 32));
     if (h_dtype == SG_BF16)
-      dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
+      dk::k_act_grad_v8<<<g8, dim3(64, 4), 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
                                                               ld_h, M, N, act, (__nv_bfloat16*)dz, ld_dz, colsum,
                                                               ld_colsum);
     else
-      dk::k_act_grad_v8<<<g8, 256, 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const float*)h, ld_h, M,
+      dk::k_act_grad_v8<<<g8, dim3(64, 4), 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const float*)h, ld_h, M,
                                                               N, act, (float*)dz, ld_dz, colsum, ld_colsum);
     SG_CUDA_TRY(cudaGetLastError());
     return SG_OK;
@@ -620,15 +647,15 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
       N % 8 == 0 && ld_z % 8 == 0 &&
       ld_y % 8 == 0 && ld_dz % 8 == 0 && a16(z) && a16(y) && a16(dz) &&
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
-    dim3 g8((unsigned)((N + 2047) / 2048), (unsigned)((M + 31) / 32));
+    dim3 g8((unsigned)((N + 511) / 512), (unsigned)((M + 31) / 32));
     blocks = (long long)g8.x * g8.y;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dz_dtype == SG_BF16)
-      dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+      dk::k_mse_v8<<<g8, dim3(64, 4), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
                                        (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part);
     else
-      dk::k_mse_v8<<<g8, 256, 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
-                                       (float*)dz, ld_dz, colsum, ld_colsum, loss_part);
+      dk::k_mse_v8<<<g8, dim3(64, 4), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                               (float*)dz, ld_dz, colsum, ld_colsum, loss_part);
   } else if (kind == SG_LOSS_MSE) {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
     if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
