@@ -609,6 +609,7 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
     steps = args.mlp_steps if name != "c1" else max(args.mlp_steps, 50)
     ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
     loss_v = float(tr.engine.loss.item())
+    replicas_ok = tr.replicas_identical() if world > 1 else True
     flops = tr.engine.flops_per_step() * world
     tflops = flops / (ms * 1e-3) / 1e12
     rec = {
@@ -621,6 +622,7 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
                      "frac": round(tflops / world / peaks["bf16_tflops_sustained"], 4),
                      "peak_kind": "sustained", "traffic": None},
         "cuda_graph": bool(tr.use_graph), "loss_last": loss_v, "n_gpus": world,
+        "replicas_identical": replicas_ok,
         "scaling": "strong (global batch fixed)",
     }
     return rec

@@ -202,6 +202,12 @@ class Trainer:
             self._eager_steps += 1
         return self.engine.loss
 
+    def replicas_identical(self) -> bool:
+        """Data parallel: the parameter replicas are bit-identical on all ranks."""
+        if self.dp is None:
+            return True
+        return replicas_identical(self.engine.P, self.dp.group)
+
     def gradient(self, X, Y):
         """Loss and parameter gradients without the update (the pullback API)."""
         e = self.engine
@@ -212,6 +218,25 @@ class Trainer:
         if self.dp is not None:
             self.dp.finish()
         return float(e.loss.item()), e.get_grads()
+
+
+def replicas_identical(t, group=None) -> bool:
+    """True when ``t`` is bit-identical on every rank of ``group`` (SURVEY
+    §8(e): every rank applies the same SGD to the same all-reduced gradient,
+    so the parameter replicas must never drift; checked, not assumed).
+    Compares an order-independent integer checksum of the raw bits plus the
+    element count, gathered over the group."""
+    import torch
+    import torch.distributed as dist
+
+    raw = t.detach().contiguous().view(-1)
+    bits = raw.view(torch.int32) if raw.element_size() == 4 else raw.view(torch.int64)
+    words = bits.to(torch.int64)
+    pos = torch.arange(words.numel(), device=words.device, dtype=torch.int64)
+    sig = torch.stack([words.sum(), (words * (pos % 65521 + 1)).sum(), torch.tensor(words.numel(), device=words.device)])
+    gathered = [torch.zeros_like(sig) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(gathered, sig, group=group)
+    return all(torch.equal(g, gathered[0]) for g in gathered)
 
 
 def shard_rows(X: np.ndarray, rank: int, world: int) -> np.ndarray:

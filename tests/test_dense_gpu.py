@@ -185,6 +185,7 @@ def test_data_parallel_trainer_over_nccl_world1():
                 assert isinstance(tr.dp, NcclDataParallel)
                 assert tr.use_graph == graph
             losses = [float(tr.step(X, Y).item()) for _ in range(3)]
+            assert tr.replicas_identical()
             if tr.dp is not None and hasattr(tr.dp, "close"):
                 torch.cuda.synchronize()
                 tr.dp.close()

@@ -152,3 +152,36 @@ def test_nccl_unique_id_rendezvous():
         assert p.exitcode == 0
     assert len(ids[0]) == 128 and any(ids[0])
     assert ids[0] == ids[1] == ids[2]
+
+
+def _replica_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_01457_b200.train import replicas_identical
+
+        p = torch.linspace(-1, 1, 1000, dtype=torch.float32)
+        same = replicas_identical(p)
+        if rank == 1:
+            p[17] = torch.nextafter(p[17], torch.tensor(2.0))  # one ulp on one rank
+        q.put((rank, same, replicas_identical(p)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replica_check_detects_one_ulp_drift():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = [q.get(timeout=10) for _ in range(world)]
+    for p in procs:
+        assert p.exitcode == 0
+    assert all(same for _, same, _ in res)
+    assert not any(drift for _, _, drift in res)
