@@ -155,6 +155,14 @@ def test_bf16_epilogues():
     torch.cuda.synchronize()
     want = (dy @ w) * hq * (1 - hq)
     assert np.abs(out.double().cpu().numpy() - want).max() <= 1e-4
+    # the same with the bias-gradient partial sums (per 32-row group) fused in
+    cs = torch.full(((M + 31) // 32, K), float("nan"), device="cuda")
+    lp = torch.empty((M, K), dtype=torch.bfloat16, device="cuda")
+    gemm(DY, W, b_mn=True, epilogue="act_grad", act="sigmoid", aux=H, out_lp=lp, colsum=cs)
+    torch.cuda.synchronize()
+    groups = want.reshape((M + 31) // 32, 32, K).sum(axis=1)
+    assert np.abs(cs.double().cpu().numpy() - groups).max() <= 1e-3 * max(1.0, np.abs(groups).max())
+    assert np.abs(lp.double().cpu().numpy() - want).max() <= 1e-2 * np.abs(want).max()
 
 
 @pytest.mark.parametrize("layout", ["kk", "k_mn", "mn_mn"])
