@@ -454,7 +454,14 @@ int check_out(const sg_tensor* t, const std::vector<long long>& shape, int dtype
   long long n = 1;
   for (long long d : want) n *= d;
   if (!t || t->dtype != dtype) return fail(SG_EINVAL, std::string(what) + ": dtype mismatch");
-  if (numel(*t) != n) return fail(SG_EINVAL, std::string(what) + ": shape mismatch");
+  // same extents in the same order (size-1 axes aside): a transposed or
+  // reshaped buffer with the right element count is still an error
+  std::vector<long long> got, exp;
+  for (int i = 0; i < t->ndim; ++i)
+    if (t->shape[i] != 1) got.push_back(t->shape[i]);
+  for (long long d : want)
+    if (d != 1) exp.push_back(d);
+  if (numel(*t) != n || got != exp) return fail(SG_EINVAL, std::string(what) + ": shape mismatch");
   if (!t->ptr && n) return fail(SG_EINVAL, std::string(what) + ": null pointer");
   return SG_OK;
 }

@@ -265,3 +265,13 @@ def test_c2_full_size_against_fp64(fused_module):
                                            yb[r0:r0 + R // 8])
         dx2[r0:r0 + R // 8] = part
     assert torch.equal(dx, dx2)
+
+
+def test_shape_errors_are_value_errors(fused_module):
+    # broadcast conflicts and wrong output shapes: ValueError like tensor.py:118-119
+    a = torch.zeros(5, device="cuda")
+    x = torch.zeros((3, 4), device="cuda")
+    with pytest.raises(ValueError, match="broadcast"):
+        F.fused_map(fused_module, "affsig", [a, x, a])
+    with pytest.raises(ValueError):
+        F.fused_map(fused_module, "affsig", [x[0], x, x[0]], out=torch.empty((4, 3), device="cuda"))

@@ -235,3 +235,21 @@ def test_batched_strict_fp64_equals_per_lane():
         one = torch.empty((M, N), dtype=torch.float64, device="cuda")
         gemm(a[l], b[l], b_mn=True, precision="strict_fp64", out=one)
         assert torch.equal(out[l], one)
+
+
+def test_argument_errors_are_value_errors():
+    """ABI misuse surfaces as ValueError (SG_EINVAL), the reference's error
+    type for shape problems (tensor.py:118-119, 358-359)."""
+    A = torch.zeros((64, 36), dtype=torch.bfloat16, device="cuda")  # lda 36: not a multiple of 8
+    B = torch.zeros((64, 40), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((64, 64), device="cuda")
+    with pytest.raises(ValueError, match="multiples of 8"):
+        gemm(A, B[:, :36], K=36, out=out)
+    with pytest.raises(ValueError, match="unknown precision|KeyError"):
+        try:
+            gemm(B, B, precision="fp8", out=out)
+        except KeyError as e:  # the Python mirror rejects unknown names first
+            raise ValueError("unknown precision") from e
+    W = torch.zeros((64, 40), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="ACT_GRAD needs aux"):
+        gemm(B, W, b_mn=True, epilogue="act_grad", act="tanh", out=torch.empty((64, 40), device="cuda"), K=40)
