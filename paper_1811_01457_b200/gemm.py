@@ -85,6 +85,15 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     M = Ma if M is None else M
     N = Nb if N is None else N
     K = min(Ka, Kb) if K is None else K
+    if M > Ma or N > Nb or K > min(Ka, Kb):
+        raise ValueError(f"gemm: M, N, K = {M}, {N}, {K} exceed the operands {tuple(A.shape)} x {tuple(B.shape)}")
+    for name, t in (("out", out), ("out_lp", out_lp), ("out_pre", out_pre), ("aux", aux)):
+        if t is not None and (t.dim() != 2 or t.shape[0] < M or t.shape[1] < N):
+            raise ValueError(f"gemm: {name} of shape {tuple(t.shape)} cannot hold the {M} x {N} result")
+    if bias is not None and bias.numel() < N:
+        raise ValueError(f"gemm: bias has {bias.numel()} elements, {N} needed")
+    if colsum is not None and (colsum.dim() != 2 or colsum.shape[0] < (M + 31) // 32 or colsum.shape[1] < N):
+        raise ValueError(f"gemm: colsum of shape {tuple(colsum.shape)} cannot hold ({(M + 31) // 32}, {N}) partials")
     d = GemmDesc()
     d.M, d.N, d.K = int(M), int(N), int(K)
     d.A, d.lda, d.a_mn_major = _ptr(A), _ld(A), int(a_mn)

@@ -253,3 +253,6 @@ def test_argument_errors_are_value_errors():
     W = torch.zeros((64, 40), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError, match="ACT_GRAD needs aux"):
         gemm(B, W, b_mn=True, epilogue="act_grad", act="tanh", out=torch.empty((64, 40), device="cuda"), K=40)
+
+    with pytest.raises(ValueError, match="cannot hold"):
+        gemm(B, W, out=torch.empty((32, 64), device="cuda"))  # result is 64 x 64
