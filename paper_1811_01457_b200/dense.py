@@ -164,8 +164,15 @@ def dense_desc(X, W, b, act: str, precision: str) -> DenseDesc:
     return d
 
 
+def _need(name, t, rows, cols):
+    if t is not None and (t.dim() != 2 or t.shape[0] < rows or t.shape[1] < cols):
+        raise ValueError(f"dense: {name} of shape {tuple(t.shape)} cannot hold {rows} x {cols}")
+
+
 def dense_forward(desc: DenseDesc, H=None, H_f32=None, Z=None, stream=None) -> None:
     """sg_dense_forward: H = act(X W^T + b) (nn_train.py:189-196) in one GEMM."""
+    for name, t in (("H", H), ("H_f32", H_f32), ("Z", Z)):
+        _need(name, t, desc.batch, desc.fan_out)
     rt.check(_lib().sg_dense_forward(rt.context(), ctypes.byref(desc), _p(H), _ldt(H), _p(H_f32), _ldt(H_f32),
                                      _p(Z), _ldt(Z), rt.stream_ptr(stream)), "sg_dense_forward")
 
@@ -174,6 +181,13 @@ def dense_backward(desc: DenseDesc, dZ, dW, db, dX=None, act_prev: str = "identi
                    colsum_out=None, stream=None) -> None:
     """sg_dense_backward: dW = dZ^T X, db = colsum(dZ), dX = dZ W [.* act_prev'(X)]
     (rules.py:45-46, 82-94, 113-124)."""
+    _need("dZ", dZ, desc.batch, desc.fan_out)
+    _need("dW", dW, desc.fan_out, desc.fan_in)
+    _need("dX", dX, desc.batch, desc.fan_in)
+    for name, t in (("colsum_in", colsum_in), ("colsum_out", colsum_out)):
+        _need(name, t, (desc.batch + 31) // 32, desc.fan_out if name == "colsum_in" else desc.fan_in)
+    if db is None or db.numel() < desc.fan_out:
+        raise ValueError(f"dense: db needs {desc.fan_out} elements")
     g = DenseGrad()
     g.dZ, g.ld_dz = _p(dZ), _ldt(dZ)
     g.colsum_in, g.ld_colsum_in = _p(colsum_in), _ldt(colsum_in)
