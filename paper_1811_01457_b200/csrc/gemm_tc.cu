@@ -248,6 +248,8 @@ struct KParams {
   int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
   int aux_stage;        // ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot
   int raster;           // CTA-pair kernel: M-tiles per raster group
+  int tail_split;       // CTA-pair kernel, > 0: tiles are taken row-major; the last tail_split tiles are
+  int tail_full;        //   computed as two K-halves each, reduce-added into the zeroed fp32 output
   int batch;            // independent GEMMs (bmm lanes), >= 1
   long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
 };
@@ -261,6 +263,13 @@ constexpr int STAGE_SLOT = 4096;
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// bulk tensor store with fp32 add into global memory (the split tail tiles)
+__device__ __forceinline__ void tma_store_add_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
@@ -292,7 +301,7 @@ __device__ __forceinline__ void stage_f32(uint8_t* slot, const float (&v)[32], i
 // warp-collective: stage one chunk and bulk-store it at (n0, row0)
 template <bool BF16>
 __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap* map, const float (&v)[32], int lane,
-                                               int n0, int row0, int bidx) {
+                                               int n0, int row0, int bidx, bool add = false) {
   if (lane == 0) bulk_wait_read0();  // the slot's previous store has been read out
   __syncwarp();
   if (BF16) stage_bf16(slot, v, lane);
@@ -300,7 +309,8 @@ __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap*
   fence_proxy_async();
   __syncwarp();
   if (lane == 0) {
-    tma_store_3d(map, slot, n0, row0, bidx);
+    if (add) tma_store_add_3d(map, slot, n0, row0, bidx);
+    else tma_store_3d(map, slot, n0, row0, bidx);
     bulk_commit();
   }
 }
@@ -333,7 +343,7 @@ __device__ __forceinline__ void aux_read(const uint8_t* slot, float (&h)[32], in
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
                                           bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
-                                          const float (&hs)[32], uint8_t* slot,
+                                          const float (&hs)[32], uint8_t* slot, bool radd,
                                           const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -377,8 +387,18 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   }
   const int row0 = m - lane;
   if (e.out_f32) {
-    if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx);
-    else if (row_ok) store_row_f32(e.out_f32 + bidx * p.so_f32 + (long long)m * e.ld_f32 + n0, v, nn);
+    if (radd) {  // split tail tile: add this K-half into the zeroed output (two terms: order-free)
+      if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx, true);
+      else if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nn) atomicAdd(e.out_f32 + (long long)m * e.ld_f32 + n0 + i, v[i]);
+      }
+    } else if (p.tma_f32) {
+      warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx);
+    } else if (row_ok) {
+      store_row_f32(e.out_f32 + bidx * p.so_f32 + (long long)m * e.ld_f32 + n0, v, nn);
+    }
   }
   if (e.out_bf16) {
     if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0, bidx);
@@ -574,7 +594,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
           if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
         }
         epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
-                  &tma_olp, &tma_of32);
+                  false, &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -687,15 +707,31 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   const int n_tiles = (p.N + BN - 1) / BN;
   const int tiles_pb = m_tiles * n_tiles;
   const int out_tiles = tiles_pb * p.batch;
-  const int tiles = out_tiles * p.splits;
+  // work units: split-K x batch x tiles, or (tail mode) the full tiles followed
+  // by two K-halves of each of the last tail_split tiles (row-major order)
+  const int tiles = p.tail_split > 0 ? p.tail_full + 2 * p.tail_split : out_tiles * p.splits;
   const int num_kb_total = (p.K + BK - 1) / BK;
+  const int kb_half = (num_kb_total + 1) / 2;
   const int pair = blockIdx.x / 2, pairs = gridDim.x / 2;
   auto kb_range = [&](int t, int& kb0, int& kb1) {
+    if (p.tail_split > 0) {
+      const bool half = t >= p.tail_full && ((t - p.tail_full) & 1);
+      kb0 = t < p.tail_full ? 0 : (half ? kb_half : 0);
+      kb1 = t < p.tail_full ? num_kb_total : min(num_kb_total, kb0 + kb_half);
+      return;
+    }
     const int s = t / out_tiles;
     kb0 = s * p.kb_per_split;
     kb1 = min(num_kb_total, kb0 + p.kb_per_split);
   };
   auto coord = [&](int t) {
+    TileCoord c;
+    if (p.tail_split > 0) {  // tail mode: row-major tiles
+      const int tile = t < p.tail_full ? t : p.tail_full + ((t - p.tail_full) >> 1);
+      c.m0 = (tile / n_tiles) * PM;
+      c.n0 = (tile % n_tiles) * BN;
+      return c;
+    }
     const int G = p.raster;  // grouped raster over 256-row pair tiles
     const int u = (t % out_tiles) % tiles_pb;
     const int per_group = G * n_tiles;
@@ -703,7 +739,6 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     const int first_m = group * G;
     const int gsize = min(m_tiles - first_m, G);
     const int in_group = u - group * per_group;
-    TileCoord c;
     c.m0 = (first_m + in_group % gsize) * PM;
     c.n0 = (in_group / gsize) * BN;
     return c;
@@ -853,7 +888,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
           if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
         }
         epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
-                  &tma_olp, &tma_of32);
+                  p.tail_split > 0 && t >= p.tail_full, &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -1084,7 +1119,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, g.batch, g.so_f32, g.so_lp};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, g.batch, g.so_f32, g.so_lp};
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
@@ -1141,7 +1176,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       splits = (num_kb + kb_per - 1) / kb_per;
     }
   }
-  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, g.batch, g.so_f32, g.so_lp};
+  tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, g.batch, g.so_f32, g.so_lp};
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
@@ -1152,7 +1187,27 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
     SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
     p.part = part;
   }
-  const int work = tiles * splits;
+  int work = tiles * splits;
+  // Split tail: when the last wave of pair tiles would run mostly empty (e.g. a
+  // 4096^2 dW: 256 tiles = 3 full waves of 74 pairs + 34 tiles), those last
+  // tiles are computed as two K-halves each and reduce-added (fp32; two terms,
+  // so the sum does not depend on their order) into the zeroed output: every
+  // pair then gets at most one half-length unit after its full tiles.
+  static const bool tail_ok = [] {
+    const char* e = std::getenv("SGB200_GEMM_TAIL");
+    return !(e && e[0] == '0');
+  }();
+  const int n_tiles = (g.N + 255) / 256;
+  const int rem = tiles % pairs_avail;
+  if (tail_ok && splits == 1 && g.batch == 1 && g.epi.mode == SG_EPI_STORE && g.epi.out_f32 && !g.epi.out_bf16 &&
+      !g.epi.colsum && !g.epi.out_pre && num_kb >= 8 && tiles > pairs_avail && rem > 0 && 2 * rem <= pairs_avail) {
+    p.tail_full = tiles - rem;
+    p.tail_split = rem;
+    const long long row0 = (long long)(p.tail_full / n_tiles) * 256;  // first row of the first split tile
+    SG_CUDA_TRY(cudaMemset2DAsync(g.epi.out_f32 + row0 * g.epi.ld_f32, (size_t)g.epi.ld_f32 * 4, 0,
+                                  (size_t)g.N * 4, (size_t)(g.M - row0), st));
+    work = p.tail_full + 2 * rem;
+  }
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
   SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());

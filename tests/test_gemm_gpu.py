@@ -256,3 +256,27 @@ def test_argument_errors_are_value_errors():
 
     with pytest.raises(ValueError, match="cannot hold"):
         gemm(B, W, out=torch.empty((32, 64), device="cuda"))  # result is 64 x 64
+
+
+@pytest.mark.parametrize("layout", ["kk", "mn_mn"])
+def test_split_tail_gemm(layout):
+    """256 pair tiles on 74 pairs: the last 34 tiles run as two K-halves each,
+    reduce-added into the zeroed fp32 output (two terms: order-free), so the
+    result is deterministic and within the bf16 GEMM tolerance."""
+    M = N = 4096
+    K = 512
+    rng = np.random.default_rng(11)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)).astype(np.float32))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)).astype(np.float32))
+    a_mn = b_mn = layout == "mn_mn"
+    A = torch.from_numpy(a.T.copy() if a_mn else a).to(torch.bfloat16).cuda()
+    B = torch.from_numpy(b.T.copy() if b_mn else b).to(torch.bfloat16).cuda()
+    outs = []
+    for _ in range(2):
+        out = torch.full((M, N), float("nan"), device="cuda")
+        gemm(A, B, a_mn=a_mn, b_mn=b_mn, out=out)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    got = outs[0].double().cpu().numpy()
+    check_close(got, a, b.T)
