@@ -321,3 +321,44 @@ def test_random_broadcast_patterns_vs_oracle(fused_module):
         for i, (shp, bar) in enumerate(zip(shapes, bars)):
             want = OS.reduce_to(np.broadcast_to(yb * parts[i], out), () if shp is None else shp)
             assert max_rel(bar, want) <= 1e-11, (case, i, out, shapes)
+
+
+def test_random_broadcast_patterns_f32(fused_module):
+    """The same random patterns in fp32 (vectorised and scalar access paths):
+    primal <= 1e-6 (reference rel metric), cotangents within 1e-6 * sum|terms|."""
+    rng = np.random.default_rng(7)
+    for case in range(16):
+        rank = int(rng.integers(1, 4))
+        out = tuple(int(v) for v in rng.integers(2, 9, rank))
+        if case % 4 == 0:
+            out = out[:-1] + (int(rng.choice([1024, 2048, 1000])),)  # wide rows: vector path
+        shapes = []
+        for _ in range(3):
+            if rng.random() < 0.2:
+                shapes.append(None)
+                continue
+            shp = [1 if rng.random() < 0.4 else d for d in out[int(rng.integers(0, rank)):]]
+            shapes.append(tuple(shp))
+        if all(s is None or np.prod(s) < np.prod(out) for s in shapes):
+            shapes[0] = out
+        args, host = [], []
+        for shp in shapes:
+            if shp is None:
+                v = float(np.float32(rng.uniform(-1.5, 1.5)))
+                args.append(v)
+                host.append(v)
+            else:
+                a = rng.uniform(-1.5, 1.5, shp).astype(np.float32)
+                args.append(torch.from_numpy(a).cuda())
+                host.append(a.astype(np.float64))
+        yb = rng.uniform(-1, 1, out).astype(np.float32)
+        y, bars = F.fused_map_grad(fused_module, "mixed", args, torch.from_numpy(yb).cuda(), want_primal=True)
+        p, parts = OS.vec_eval(fused_module, "mixed", host)
+        assert max_rel(y, p) <= 1e-6, (case, out, shapes)
+        for i, (shp, bar) in enumerate(zip(shapes, bars)):
+            terms = np.broadcast_to(yb.astype(np.float64) * parts[i], out)
+            tgt = () if shp is None else shp
+            want = OS.reduce_to(terms, tgt)
+            bound = OS.reduce_to(np.abs(terms), tgt)
+            err = np.abs(np.asarray(bar.double().cpu().numpy()).reshape(np.shape(want)) - want)
+            assert (err <= 1e-6 * np.maximum(1.0, bound) + 1e-7).all(), (case, i, out, shapes)
