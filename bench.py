@@ -587,6 +587,22 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
     }
 
 
+def count_launches(fn):
+    """Kernels launched by one call of fn (torch.profiler / CUPTI), or None."""
+    import torch
+
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        return sum(1 for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA)
+    except Exception:  # profiler unavailable: report nothing rather than a guess
+        return None
+
+
 def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, graph, lr=1e-4):
     """Dense-chain training step (fwd + loss + pullback + [allreduce] + SGD)."""
     import torch
@@ -610,6 +626,14 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
     ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
     loss_v = float(tr.engine.loss.item())
     replicas_ok = tr.replicas_identical() if world > 1 else True
+    launches = count_launches(lambda: tr._device_step())
+    no_graph_ms = None
+    if tr.use_graph:  # the same step without the graph (launch overhead exposed)
+        tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=False)
+        no_graph_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
+        if tr2.dp is not None and hasattr(tr2.dp, "close"):
+            torch.cuda.synchronize()
+            tr2.dp.close()
     flops = tr.engine.flops_per_step() * world
     tflops = flops / (ms * 1e-3) / 1e12
     rec = {
@@ -622,6 +646,8 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
                      "frac": round(tflops / world / peaks["bf16_tflops_sustained"], 4),
                      "peak_kind": "sustained", "traffic": None},
         "cuda_graph": bool(tr.use_graph), "loss_last": loss_v, "n_gpus": world,
+        "gpu_launches_per_step": launches,
+        "ms_per_step_without_graph": None if no_graph_ms is None else round(no_graph_ms, 4),
         "replicas_identical": replicas_ok,
         "scaling": "strong (global batch fixed)",
     }
