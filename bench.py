@@ -391,7 +391,7 @@ def broadcast_bench(args, world, rank, local, dist):
                 "pcie_bound_ms": round(max(h2d, d2h) / (pcie_gbps * 1e9) * 1e3, 2),
                 "serial_ms_per_step": round(e2e_serial_ms, 3),
                 "serial_value": round(world * n * BYTES_PER_ELEM / (e2e_serial_ms * 1e-3) / 1e9, 2)},
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": (count_launches(step) or 4) * args.steps,
         "clocks": clocks.summary(),
     }
     return rec
