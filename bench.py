@@ -569,19 +569,20 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
     gemm_ms = kms["fwd_gemm"] + kms["dX_gemm"] + kms["dW_gemm"]
     achieved = 3 * gf / (gemm_ms * 1e-3) / 1e12
     esz = 4 if tf32 else 2
-    cublas = None
-    if tf32:  # context for the TF32 line: cuBLAS TF32 on the same box, same forward GEMM shape
-        torch.backends.cuda.matmul.allow_tf32 = True
-        xa, wa = layer.X.contiguous(), layer.W.contiguous()
+    # context: cuBLAS on the same box and shapes (the library baseline; not on the product path)
+    torch.backends.cuda.matmul.allow_tf32 = True
+    xa, wa, dza = layer.X.contiguous(), Wop.contiguous(), layer.dZ.contiguous()
+    cublas = {}
+    for nm, fn in (("fwd_gemm", lambda: xa @ wa.T), ("dX_gemm", lambda: dza @ wa), ("dW_gemm", lambda: dza.T @ xa)):
         for _ in range(3):
-            xa @ wa.T
+            fn()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(10):
-            xa @ wa.T
+            fn()
         s1.record(stream)
         torch.cuda.synchronize()
-        cublas = round(gf / (s0.elapsed_time(s1) / 10 * 1e-3) / 1e12, 1)
+        cublas[nm] = round(gf / (s0.elapsed_time(s1) / 10 * 1e-3) / 1e12, 1)
     peak = TF32_PEAK_TFLOPS if tf32 else peaks["bf16_tflops"]
     return {
         "workload": f"c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, {precision} tcgen05",
@@ -596,7 +597,7 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
                      "traffic": None if tf32 else traffic_of("gemm_bf16_fwd_c3", True),
                      "traffic_algorithmic_bytes": esz * (M * D + D * D + M * D)},
         "gpu_launches_per_step": 5,
-        "cublas_tf32_fwd_TFLOPs": cublas,
+        "cublas_TFLOPs_same_shapes": cublas,
         "l2": f"working set ~{808 if tf32 else 544} MB per step > 126 MB L2",
     }
 
