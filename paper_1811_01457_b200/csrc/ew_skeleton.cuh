@@ -252,10 +252,15 @@ struct SgGradAcc {
 #define SG_ACC_ROW(acc, i, j) (acc).row[i][j]
 #endif
 
-// One row: duals, ybar contraction, xbar stores, accumulation.  Returns the
-// per-row sums for COL operands in colsum.
+// One row: duals, ybar contraction, xbar stores.  Contributions to ROW and
+// scalar operands are added into pre[i][j] (type T, registers) and flushed
+// into the fp64 sums by sg_flush_pre once per group of SG_GUNROLL rows: one
+// fp64 conversion + shared-memory update per group instead of per element.
+// (f32: the group sum adds at most (SG_GUNROLL-1) * 2^-24 * sum|terms| of
+// error, far inside the 1e-6 * sum|terms| tolerance.)  Returns the per-row
+// sums for COL operands in colsum.
 __device__ __forceinline__ void sg_grad_row(const SgEwParams& p, long long r, long long c,
-                                            const T (&x)[SG_KT][SG_VEC], const VT& yb, SgGradAcc& acc,
+                                            const T (&x)[SG_KT][SG_VEC], const VT& yb, T (&pre)[SG_KT][SG_VEC],
                                             double (&colsum)[SG_KT]) {
   VT y, g[SG_KT];
 #pragma unroll
@@ -272,15 +277,36 @@ __device__ __forceinline__ void sg_grad_row(const SgEwParams& p, long long r, lo
       const T contrib = yb.v[j] * d[i];  // ybar .* partial_i (forward_ad.py:233)
       const int kind = sg_kinds[i];
       if (kind == SG_FULL) g[i].v[j] = contrib;
-      else if (kind == SG_ROW) SG_ACC_ROW(acc, i, j) += (double)contrib;
       else if (kind == SG_COL) colsum[i] += (double)contrib;
-      else acc.s[i] += (double)contrib;
+      else pre[i][j] += contrib;
     }
   }
   if (p.out) sg_stv(reinterpret_cast<T*>(p.out) + r * p.C + c, y);
 #pragma unroll
   for (int i = 0; i < SG_K; ++i)
     if (sg_kinds[i] == SG_FULL) sg_stv(reinterpret_cast<T*>(p.xbar[i]) + r * p.C + c, g[i]);
+}
+
+__device__ __forceinline__ void sg_zero_pre(T (&pre)[SG_KT][SG_VEC]) {
+#pragma unroll
+  for (int i = 0; i < SG_KT; ++i)
+#pragma unroll
+    for (int j = 0; j < SG_VEC; ++j) pre[i][j] = (T)0;
+}
+
+__device__ __forceinline__ void sg_flush_pre(SgGradAcc& acc, T (&pre)[SG_KT][SG_VEC]) {
+#pragma unroll
+  for (int i = 0; i < SG_K; ++i) {
+    const int kind = sg_kinds[i];
+    if (kind == SG_ROW) {
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) SG_ACC_ROW(acc, i, j) += (double)pre[i][j];
+    } else if (kind == SG_SPTR || kind == SG_SVAL) {
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) acc.s[i] += (double)pre[i][j];
+    }
+  }
+  sg_zero_pre(pre);
 }
 
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_GRAD_MINB)
@@ -302,6 +328,8 @@ sg_ew_grad(const SgEwParams p) {
 #pragma unroll
     for (int j = 0; j < SG_VEC; ++j) SG_ACC_ROW(acc, i, j) = 0.0;
   }
+  T pre[SG_KT][SG_VEC];
+  sg_zero_pre(pre);
   T inv[SG_KT][SG_VEC];
   if (active || SG_ROWMODE) sg_load_invariant(p, SG_ROWMODE ? 0 : c, inv);  // row mode: scalars only
 
@@ -328,13 +356,15 @@ sg_ew_grad(const SgEwParams p) {
           yb[u] = sg_ldv_stream(ybar + r * p.C + c0 + u * CSTEP);
         }
 #pragma unroll
-        for (int u = 0; u < SG_RUNROLL; ++u) sg_grad_row(p, r, c0 + u * CSTEP, xs[u], yb[u], acc, colsum);
+        for (int u = 0; u < SG_RUNROLL; ++u) sg_grad_row(p, r, c0 + u * CSTEP, xs[u], yb[u], pre, colsum);
+        sg_flush_pre(acc, pre);
       }
       for (; c0 < p.C; c0 += CSTEP) {
         T xs[SG_KT][SG_VEC];
         sg_load_row(p, r, c0, inv, xs);
         const VT yb = sg_ldv_stream(ybar + r * p.C + c0);
-        sg_grad_row(p, r, c0, xs, yb, acc, colsum);
+        sg_grad_row(p, r, c0, xs, yb, pre, colsum);
+        sg_flush_pre(acc, pre);
       }
 #pragma unroll
       for (int i = 0; i < SG_K; ++i) {
@@ -363,15 +393,17 @@ sg_ew_grad(const SgEwParams p) {
       }
 #pragma unroll
       for (int u = 0; u < SG_GUNROLL; ++u)
-        sg_grad_row(p, w.base + (it + u) * w.stride, c, xs[u], yb[u], acc, colsum);
+        sg_grad_row(p, w.base + (it + u) * w.stride, c, xs[u], yb[u], pre, colsum);
+      sg_flush_pre(acc, pre);
     }
     for (; it < n; ++it) {
       const long long r = w.base + it * w.stride;
       T xs[SG_KT][SG_VEC];
       sg_load_row(p, r, c, inv, xs);
       VT yb = sg_ldv_stream(ybar + r * p.C + c);
-      sg_grad_row(p, r, c, xs, yb, acc, colsum);
+      sg_grad_row(p, r, c, xs, yb, pre, colsum);
     }
+    sg_flush_pre(acc, pre);
   }
 #else
   // COL operands reduce across the lanes sharing a row: every lane of a
@@ -401,7 +433,7 @@ sg_ew_grad(const SgEwParams p) {
       double colsum[SG_KT];
 #pragma unroll
       for (int i = 0; i < SG_KT; ++i) colsum[i] = 0.0;
-      if (live) sg_grad_row(p, r, c, xs[u], yb[u], acc, colsum);
+      if (live) sg_grad_row(p, r, c, xs[u], yb[u], pre, colsum);
 #pragma unroll
       for (int i = 0; i < SG_K; ++i) {
         if (sg_kinds[i] != SG_COL) continue;
@@ -411,6 +443,7 @@ sg_ew_grad(const SgEwParams p) {
         if (live && (tx % kGroup) == 0) p.part[i][gi * p.R + r] = sum;
       }
     }
+    sg_flush_pre(acc, pre);
   }
 #endif
   // ROW partials: one row of partials per row-thread
