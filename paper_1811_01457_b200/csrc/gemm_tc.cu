@@ -1228,6 +1228,13 @@ int run_bn(const GemmArgs& g, int num_sms, cudaStream_t st) {
 
 template <bool TF32>
 int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  static const int force_bn = [] {
+    const char* e = std::getenv("SGB200_GEMM_FORCE_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_bn == 64) return run_bn<TF32, 64>(g, num_sms, st);
+  if (force_bn == 128) return run_bn<TF32, 128>(g, num_sms, st);
+  if (force_bn == 256) return run_bn<TF32, 256>(g, num_sms, st);
   if (g.N <= 64) return run_bn<TF32, 64>(g, num_sms, st);
   if (g.N <= 128) return run_bn<TF32, 128>(g, num_sms, st);
   static const bool pair_ok = [] {
