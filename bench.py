@@ -641,9 +641,13 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
     ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
     loss_v = float(tr.engine.loss.item())
     replicas_ok = tr.replicas_identical() if world > 1 else True
-    launches = count_launches(lambda: tr._device_step())
-    no_graph_ms = None
-    if tr.use_graph:  # the same step without the graph (launch overhead exposed)
+    small = tr.engine.small is not None  # the whole step in one cooperative launch
+    launches = count_launches(lambda: tr.step(X, Y) if small else tr._device_step())
+    no_graph_ms = layer_ms = None
+    if small:  # beside it: the layer-by-layer tensor-core path in a CUDA graph
+        tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=True, small=False)
+        layer_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
+    elif tr.use_graph:  # the same step without the graph (launch overhead exposed)
         tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=False)
         no_graph_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
         if tr2.dp is not None and hasattr(tr2.dp, "close"):
@@ -651,18 +655,26 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
             tr2.dp.close()
     flops = tr.engine.flops_per_step() * world
     tflops = flops / (ms * 1e-3) / 1e12
+    if small:  # latency-bound: the roofline is the launch, not a pipe
+        roof = {"bound": "latency", "kernel": "k_mlp_small_step (one launch per step)",
+                "achieved_us_per_step": round(ms * 1e3, 2), "TFLOPs": round(tflops, 2)}
+    else:
+        roof = {"bound": "tensor", "kernel": "whole step (GEMM-dominated)", "achieved": round(tflops / world, 1),
+                "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                "frac": round(tflops / world / peaks["bf16_tflops_sustained"], 4),
+                "peak_kind": "sustained", "traffic": None}
     rec = {
         "workload": f"{name} MLP {'-'.join(map(str, sizes))} ({'/'.join(acts)}, {loss}) train step, "
-                    f"global batch {batch}, bf16 tcgen05" + (f", DP x{world} NCCL" if world > 1 else ""),
+                    f"global batch {batch}, "
+                    + ("fp32, whole step in one cooperative launch (sg_mlp_small_step)" if small else "bf16 tcgen05")
+                    + (f", DP x{world} NCCL" if world > 1 else ""),
         "value": round(batch / (ms * 1e-3), 1), "unit": "samples/s", "ms_per_step": round(ms, 4),
         "flops_per_step": flops, "TFLOPs": round(tflops, 1),
-        "roofline": {"bound": "tensor", "kernel": "whole step (GEMM-dominated)", "achieved": round(tflops / world, 1),
-                     "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": round(tflops / world / peaks["bf16_tflops_sustained"], 4),
-                     "peak_kind": "sustained", "traffic": None},
-        "cuda_graph": bool(tr.use_graph), "loss_last": loss_v, "n_gpus": world,
+        "roofline": roof,
+        "cuda_graph": bool(tr.use_graph) and not small, "loss_last": loss_v, "n_gpus": world,
         "gpu_launches_per_step": launches,
         "ms_per_step_without_graph": None if no_graph_ms is None else round(no_graph_ms, 4),
+        "layer_path_ms_per_step": None if layer_ms is None else round(layer_ms, 4),
         "replicas_identical": replicas_ok,
         "scaling": "strong (global batch fixed)",
     }

@@ -216,6 +216,35 @@ SG_API int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, i
 SG_API int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,
                    void* stream);
 
+/* ------------------------------------------------ small-chain training step
+ * The whole step of a small Dense chain -- forward (nn_train.py:189-210), loss
+ * + seed, pullback (rules.py:45-46, 82-94, 113-124) and SGD (nn_train.py:
+ * 365-372) -- in ONE cooperative launch, fp32 on the CUDA cores (c1: MLP
+ * 784-32-10 at batch 128 is latency-bound: 13 MFLOP per step).  Parameters use
+ * the flat [W0, b0, W1, b1, ...] layout of the Dense-chain engine: W_l at
+ * P + w_off[l], rows of ldw[l] >= fan_in, b_l at P + b_off[l]; G (same layout)
+ * receives the gradients, P is updated in place, and the optional bf16 shadow
+ * S mirrors the new P.  Losses: SG_LOSS_SOFTMAX_XENT, SG_LOSS_MSE (as sg_loss);
+ * `loss` (device f64) receives the total.  Limits: 1..4 layers, widths <= 1024,
+ * batch <= 512, batch x width working sets that fit in shared memory.
+ * `scratch` (device, >= sg_mlp_small_scratch_bytes) must be zeroed once
+ * before the first step (it holds the grid barrier). */
+#define SG_MLP_SMALL_MAXL 4
+typedef struct sg_mlp_small_desc {
+  int32_t L;                          /* layers */
+  int32_t sizes[SG_MLP_SMALL_MAXL + 1];
+  int32_t act[SG_MLP_SMALL_MAXL];     /* SG_ACT_* per layer */
+  int64_t w_off[SG_MLP_SMALL_MAXL], b_off[SG_MLP_SMALL_MAXL], ldw[SG_MLP_SMALL_MAXL];
+  int32_t loss;                       /* SG_LOSS_SOFTMAX_XENT or SG_LOSS_MSE */
+  int32_t B;                          /* minibatch rows */
+  double scale;                       /* loss scale (1/batch) */
+  double lr;
+} sg_mlp_small_desc;
+SG_API int sg_mlp_small_scratch_bytes(const sg_mlp_small_desc* d, int64_t* bytes);
+SG_API int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* G, void* S_bf16,
+                             const float* X, int64_t ldx, const float* Y, int64_t ldy, float* Z, int64_t ldz,
+                             double* loss, void* scratch, int64_t scratch_bytes, void* stream);
+
 /* ------------------------------------------------------ Dense layer
  * One Dense layer as the reference builds it (nn_train.py:189-210:
  * transpose(W) / matmul / add / activation) and its pullback (rules.py:45-46,

@@ -112,6 +112,15 @@ class DenseGrad(ctypes.Structure):  # sg_dense_grad
     ]
 
 
+class MlpSmallDesc(ctypes.Structure):  # sg_mlp_small_desc
+    MAXL = 4
+    _fields_ = [
+        ("L", ctypes.c_int32), ("sizes", ctypes.c_int32 * 5), ("act", ctypes.c_int32 * 4),
+        ("w_off", ctypes.c_int64 * 4), ("b_off", ctypes.c_int64 * 4), ("ldw", ctypes.c_int64 * 4),
+        ("loss", ctypes.c_int32), ("B", ctypes.c_int32), ("scale", ctypes.c_double), ("lr", ctypes.c_double),
+    ]
+
+
 _bound = False
 
 
@@ -127,6 +136,8 @@ def _lib():
         lib.sg_loss.argtypes = [P, I32, P, I32, I64, P, I64, I64, I64, D, P, P, I64, P, I32, I64, P, I32,
                                 I64, P, I64, P]
         lib.sg_sgd.argtypes = [P, P, P, I32, I64, D, P, P]
+        lib.sg_mlp_small_scratch_bytes.argtypes = [P, ctypes.POINTER(I64)]
+        lib.sg_mlp_small_step.argtypes = [P, P, P, P, P, P, I64, P, I64, P, I64, P, P, I64, P]
         lib.sg_cast.argtypes = [P, P, I32, P, I32, I64, P]
         lib.sg_dense_forward.argtypes = [P, ctypes.POINTER(DenseDesc), P, I64, P, I64, P, I64, P]
         lib.sg_dense_backward.argtypes = [P, ctypes.POINTER(DenseDesc), ctypes.POINTER(DenseGrad), P]
@@ -274,7 +285,7 @@ class ChainEngine:
     """Device state + kernels of a Dense chain's training step on one GPU."""
 
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", precision: str = "bf16",
-                 global_batch: int | None = None):
+                 global_batch: int | None = None, small: bool = True):
         import torch
 
         if loss not in LOSSES:
@@ -341,6 +352,7 @@ class ChainEngine:
                                  self.acts[l], precision) for l in range(self.L)]
         self.tape = Tape()
         self.grad_ready = None  # optional callback(layer_index) when layer l's gradients are written
+        self.small = self._plan_small() if small else None
         if chain.layers[0].W is not None:
             self.set_params([(l.W, l.b) for l in chain.layers])
 
@@ -431,6 +443,67 @@ class ChainEngine:
 
     def pullback(self):
         self.tape.pullback()
+
+    # ------------------------------------------------- one-launch small step
+    def _plan_small(self):
+        """Descriptor + scratch of the one-launch step (``sg_mlp_small_step``)
+        when this chain qualifies: tensor-core precision (the step then runs
+        in fp32, more accurate than requested), softmax-CE or MSE loss, <= 4
+        layers, widths <= 1024, batch <= 512 and a per-launch working set
+        that fits in shared memory; ``None`` otherwise (the layer-by-layer
+        path).  ``SGB200_MLP_SMALL=0`` disables it."""
+        import os
+
+        import torch
+
+        if os.environ.get("SGB200_MLP_SMALL", "1") == "0":
+            return None
+        if not self.tc or self.loss_kind not in ("softmax_xent", "mse") or self.L > MlpSmallDesc.MAXL:
+            return None
+        if self.B > 512 or max(self.sizes) > 1024 or self.scale != 1.0 / self.B:
+            return None
+        if self.flops_per_step() > 64e6:  # beyond latency-bound sizes the tensor-core chain wins
+            return None
+        d = MlpSmallDesc()
+        d.L, d.loss, d.B, d.scale = self.L, LOSSES[self.loss_kind], self.B, self.scale
+        for i, v in enumerate(self.sizes):
+            d.sizes[i] = v
+        for l, (wo, bo) in enumerate(self.seg):
+            d.act[l] = ACT[self.acts[l]]
+            d.w_off[l], d.b_off[l], d.ldw[l] = wo, bo, _ld(self.sizes[l])
+        lib = _lib()
+        n = ctypes.c_int64()
+        if lib.sg_mlp_small_scratch_bytes(ctypes.byref(d), ctypes.byref(n)) != 0:
+            return None  # outside the kernel's limits
+        dev = self.P.device
+        self.small_scratch = torch.zeros(n.value, dtype=torch.uint8, device=dev)
+        self.X32 = torch.zeros((self.B, self.sizes[0]), dtype=torch.float32, device=dev)
+        self.Y32 = torch.zeros((self.B, self.sizes[-1]), dtype=torch.float32, device=dev)
+        return d
+
+    def small_step(self, X, Y, lr: float):
+        """forward + loss + pullback + SGD of the loaded batch in ONE launch
+        (``sg_mlp_small_step``); X, Y fp32 rows are read in place when they
+        are row-contiguous, else copied first.  Returns the loss (device)."""
+        import torch
+
+        d = self.small
+        if tuple(X.shape) != (self.B, self.sizes[0]) or tuple(Y.shape) != (self.B, self.sizes[-1]):
+            raise ValueError(f"batch shapes {tuple(X.shape)}, {tuple(Y.shape)} do not match the engine")
+
+        def rows(t, buf):
+            if t.dtype == torch.float32 and t.is_cuda and t.stride(1) == 1 and t.data_ptr() % 16 == 0:
+                return t
+            buf.copy_(t, non_blocking=True)
+            return buf
+
+        X, Y = rows(X, self.X32), rows(Y, self.Y32)
+        d.lr = float(lr)
+        rt.check(_lib().sg_mlp_small_step(
+            rt.context(), ctypes.byref(d), _p(self.P), _p(self.G), _p(self.S), _p(X), X.stride(0), _p(Y),
+            Y.stride(0), _p(self.Zt), self.Zt.stride(0), _p(self.loss), _p(self.small_scratch),
+            self.small_scratch.numel(), rt.stream_ptr()), "sg_mlp_small_step")
+        return self.loss
 
     # ---------------------------------------------------------------- SGD
     def sgd(self, lr: float):

@@ -151,7 +151,7 @@ class Trainer:
 
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", lr: float = 0.05,
                  precision: str = "bf16", dp: bool = False, group=None, graph: bool = False,
-                 dp_backend: str | None = None):
+                 dp_backend: str | None = None, small: bool = True):
         self.lr = float(lr)
         self.world = 1
         if dp:
@@ -161,7 +161,9 @@ class Trainer:
         if batch % self.world:
             raise ValueError(f"global batch {batch} not divisible by {self.world} ranks")
         self.local_batch = batch // self.world
-        self.engine = ChainEngine(chain, self.local_batch, loss, precision, global_batch=batch)
+        # small chains on one GPU: the whole step is one launch (sg_mlp_small_step)
+        self.engine = ChainEngine(chain, self.local_batch, loss, precision, global_batch=batch,
+                                  small=small and not dp)
         self.dp = None
         if dp:
             backend = dp_backend or _default_dp_backend(group)
@@ -190,6 +192,8 @@ class Trainer:
 
     def step(self, X, Y):
         """One training step on (X, Y) already on the device; returns the loss (device)."""
+        if self.engine.small is not None:  # one launch: nothing for a graph to save
+            return self.engine.small_step(X, Y, self.lr)
         self.engine.load_batch(X, Y)
         if self.use_graph and self._eager_steps > 0:
             # the first step ran eagerly (one-time kernel attribute setup);

@@ -133,3 +133,33 @@ def test_lowering_accepts_reference_module_objects():
     rm = ref.parse_ir(FUSED_SRC)
     lo = lower(rm, "affsig")
     assert _compile(lo, rt.SG_F32, [1, 0, 1], 4) > 0
+
+
+def test_small_step_planner_limits():
+    """sg_mlp_small_scratch_bytes (host-only planning of the one-launch step):
+    accepts the c1 chain, rejects what the kernel cannot hold."""
+    from paper_1811_01457_b200.dense import MlpSmallDesc, _lib
+
+    lib = _lib()
+
+    def plan(sizes, B, loss=0):
+        d = MlpSmallDesc()
+        d.L, d.B, d.loss, d.scale, d.lr = len(sizes) - 1, B, loss, 1.0 / B, 0.05
+        for i, v in enumerate(sizes[:5]):
+            d.sizes[i] = v
+        off = 0
+        for l in range(min(d.L, 4)):
+            d.w_off[l], d.ldw[l] = off, (sizes[l] + 7) // 8 * 8
+            off += sizes[l + 1] * d.ldw[l]
+            d.b_off[l] = off
+            off += sizes[l + 1]
+        n = ctypes.c_int64()
+        return lib.sg_mlp_small_scratch_bytes(ctypes.byref(d), ctypes.byref(n)), n.value
+
+    rc, n = plan((784, 32, 10), 128)
+    assert rc == 0 and n >= 256 + 128 * 8 + 128 * 32 * 4 + 128 * 42 * 4
+    assert plan((784, 32, 10), 128, loss=2)[0] != 0         # BCE: layer path
+    assert plan((784, 32, 10), 1024)[0] != 0                # batch beyond 512
+    assert plan((2048, 32, 10), 128)[0] != 0                # width beyond 1024
+    assert plan((8,) * 6, 64)[0] != 0                       # 5 layers
+    assert plan((1024, 1024, 1024), 512)[0] != 0            # working set beyond shared memory

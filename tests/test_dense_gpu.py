@@ -286,3 +286,73 @@ def test_dense_layer_c3_full_size(precision):
     assert nrel_t(dX, dz @ w64) <= tol
     assert nrel_t(dW, dz.T @ x64) <= tol
     assert nrel_t(db, dz.sum(0)) <= tol
+
+
+@pytest.mark.parametrize("sizes,acts,loss,B", [
+    ((784, 32, 10), ("sigmoid", "identity"), "softmax_xent", 128),   # c1 at full size
+    ((784, 32, 10), ("sigmoid", "identity"), "softmax_xent", 129),   # last CTA holds one row
+    ((64, 48, 40, 24, 8), ("tanh", "relu", "sigmoid", "identity"), "mse", 200),
+    ((100, 30, 5), ("tanh", "sigmoid"), "mse", 7),                   # activated top layer, tiny batch
+])
+def test_small_chain_one_launch_step_matches_oracle(sizes, acts, loss, B):
+    """sg_mlp_small_step (the whole step in one cooperative launch, fp32):
+    loss, gradients and the SGD update against the fp64 oracle, and bit-identical
+    to itself across runs (fixed-order reductions)."""
+    rng = np.random.default_rng(B)
+    X = rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)
+    if loss == "softmax_xent":
+        Y = np.zeros((B, sizes[-1]), np.float32)
+        Y[np.arange(B), rng.integers(0, sizes[-1], B)] = 1
+    else:
+        Y = rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)
+
+    def run():
+        chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(len(acts))]).init_params(
+            np.random.default_rng(3))
+        for l in chain.layers:
+            l.b = np.random.default_rng(4).uniform(-0.1, 0.1, l.fan_out).astype(np.float32)
+        tr = Trainer(chain, B, loss=loss, lr=0.05, precision="bf16")
+        assert tr.engine.small is not None
+        lv = float(tr.step(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()).item())
+        return chain, lv, tr.engine.get_grads(), tr.engine.get_params(), tr.engine.P.clone()
+
+    chain, lv, grads, new, P1 = run()
+    _, lv2, _, _, P2 = run()
+    assert lv == lv2 and torch.equal(P1, P2)
+    params = [(l.W.astype(np.float64), l.b.astype(np.float64)) for l in chain.layers]
+    lo, go, no = OD.mlp_step(params, X.astype(np.float64), Y.astype(np.float64), acts, loss, lr=0.05,
+                             mode="blas")
+    tol = 2e-5  # fp32 end to end
+    assert abs(lv - lo) <= tol * max(1.0, abs(lo))
+    for (gW, gb), (oW, ob) in zip(grads, go):
+        assert nrel(gW, oW) <= tol
+        assert nrel(gb, ob) <= tol
+    for (W, b), (Wn, bn), (W0, b0) in zip(new, no, params):
+        assert nrel(W - W0, Wn - W0) <= tol
+        assert nrel(b - b0, bn - b0) <= tol
+
+
+def test_small_chain_step_equals_layer_path_and_trains():
+    """The one-launch step and the layer-by-layer tensor-core path (SGB200
+    small path off) train the c1 model to the same losses (within bf16), and
+    the one-launch step keeps the bf16 shadow in sync with P."""
+    rng = np.random.default_rng(0)
+    sizes, acts, B = (784, 32, 10), ("sigmoid", "identity"), 128
+    X = torch.from_numpy(rng.uniform(0, 1, (B, 784)).astype(np.float32)).cuda()
+    Y = torch.zeros((B, 10), device="cuda")
+    Y[torch.arange(B), torch.from_numpy(rng.integers(0, 10, B)).cuda()] = 1
+
+    def run(small):
+        chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(2)]).init_params(
+            np.random.default_rng(1))
+        tr = Trainer(chain, B, loss="softmax_xent", lr=0.5, precision="bf16", small=small, graph=not small)
+        assert (tr.engine.small is not None) == small
+        return [float(tr.step(X, Y).item()) for _ in range(20)], tr
+
+    ls, trs = run(True)
+    ll, _ = run(False)
+    assert ls[-1] < ls[0] - 0.1
+    for a, b in zip(ls, ll):
+        assert abs(a - b) <= 1e-2 * max(1.0, abs(b))
+    e = trs.engine
+    assert torch.equal(e.S, e.P.to(torch.bfloat16))

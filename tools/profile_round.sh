@@ -10,7 +10,7 @@ B="timeout -s KILL 600 python bench.py --no-cpu-baseline"
 $B --steps 10 --warmup 3 --secondary c3,c5 > $O/bench.log 2>&1 || { echo "bench failed"; tail -20 $O/bench.log; exit 1; }
 tail -c 600 $O/bench.log
 # launch lists (per-launch durations, cold cache, serialised)
-$NCU --metrics gpu__time_duration.sum -c 60 --csv --log-file $O/launches_c2.csv \
+$NCU --metrics gpu__time_duration.sum -k regex:'sg_ew_|k_sum' -c 24 --csv --log-file $O/launches_c2.csv \
   $B --steps 3 --warmup 3 --secondary none > /dev/null 2>&1
 $NCU --metrics gpu__time_duration.sum -k regex:'gemm|k_act|k_colsum|k_splitk' -c 40 --csv --log-file $O/launches_c3.csv \
   $B --steps 3 --warmup 3 --rows 1024 --secondary c3 > /dev/null 2>&1
