@@ -68,7 +68,10 @@ struct Params {
   float* dzg;          // dZ_l, l = 0..L-1: dzg + dz_off[l] + r * d[l+1]
   long long h_off[MAXL + 1], dz_off[MAXL];
   int chunks;          // phase 2 work items: sum over layers of ceil((d[l] + 1) / KW)
-  int dbg;             // timing experiments (SGB200_MLP_SMALL_DBG): 1 empty, 2 phase 1 only, 4 no barrier
+  int wstage;          // 1: every W_l is staged in shared memory by bulk copies (TMA) at launch
+  long long ws_base;   // float offset of the staged weights in shared memory (128-byte aligned)
+  long long ws_off[MAXL];
+  int k4[MAXL];        // staged row stride (fan_in rounded up to 4 floats = 16 bytes)
 };
 
 __device__ __forceinline__ float act_f(float z, int a) {
@@ -100,6 +103,23 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar))
+                 : "memory");
+  } while (!done);
+}
+
 // Sense-reversal grid barrier (the launch is cooperative: all CTAs resident).
 // The counter is back at 0 after every use, the generation only grows.
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
@@ -125,7 +145,6 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   const int L = p.L;
-  if (p.dbg & 1) return;
 
   // ------------------------------------------------------------ phase 1
   {
@@ -144,13 +163,37 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
     float* dz_a = hs(L + 1 - 1) + p.R * p.d[L];
     float* dz_b = dz_a + p.R * dmax;
 
+    // weights: one bulk copy per W row into shared memory, all on one
+    // mbarrier, in flight while the input rows load (one L2 round trip)
+    __shared__ uint64_t wbar;
+    float* ws = sm + p.ws_base;
+    if (p.wstage) {
+      if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+      if (warp == 0) {
+        if (lane == 0) {
+          uint32_t total = 0;
+          for (int l = 0; l < L; ++l) total += (uint32_t)p.d[l + 1] * p.k4[l] * 4u;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&wbar)), "r"(total)
+                       : "memory");
+        }
+        __syncwarp();
+        for (int l = 0; l < L; ++l)
+          for (int j = lane; j < p.d[l + 1]; j += 32)
+            bulk_g2s(ws + p.ws_off[l] + (long long)j * p.k4[l], p.P + p.w_off[l] + (long long)j * p.ldw[l],
+                     (uint32_t)p.k4[l] * 4u, &wbar);
+      }
+    }
     // input rows (fp32)
     for (int i = tid; i < nr * p.d[0]; i += NT) {
       const int r = i / p.d[0], k = i - r * p.d[0];
       hs(0)[i] = p.X[(long long)(r0 + r) * p.ldx + k];
     }
     __syncthreads();
-    if (p.dbg & 8) return;
+    if (p.wstage) mbar_wait0(&wbar);
 
     // forward: warp per output column j, lanes split K (coalesced W rows).
     // The step is latency-bound, so every W row is fetched with all of its
@@ -159,6 +202,32 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
       const int K = p.d[l], N = p.d[l + 1];
       const float* W = p.P + p.w_off[l];
       const float* bias = p.P + p.b_off[l];
+      if (p.wstage) {  // weights in shared memory: warp per column, lanes split K
+        const float* wl = ws + p.ws_off[l];
+        const float* h0 = hs(l);
+        for (int j = warp; j < N; j += NW) {
+          const float* w = wl + (long long)j * p.k4[l];
+          float acc[MAXR];
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+          for (int k = lane; k < K; k += 32) {
+            const float wv = w[k];
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(h0[min(r, nr - 1) * K + k], wv, acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) acc[r] = warp_sum(acc[r]);
+          if (lane < nr) {
+            float z = 0.0f;
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r)
+              if (r == lane) z = acc[r];
+            hs(l + 1)[lane * N + j] = act_f(z + __ldg(bias + j), p.act[l]);
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       const int rot = (blockIdx.x * NW) % N;  // CTAs start on different W rows (spreads L2 slices)
       for (int jj = warp; jj < N; jj += NW) {
         const int j = jj + rot < N ? jj + rot : jj + rot - N;
@@ -196,7 +265,6 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
       __syncthreads();
     }
 
-    if (p.dbg & 16) return;
     // loss + seed: warp per row (top layer output h_L, width N <= MAXD)
     {
       const int N = p.d[L];
@@ -244,7 +312,6 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
       __syncthreads();
     }
 
-    if (p.dbg & 32) return;
     // pullback: dZ_{l-1} = (dZ_l W_l) .* act'_{l-1}(h_l), thread per input column k
     float* cur = dz_a;
     float* nxt = dz_b;
@@ -256,6 +323,27 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
         for (int i = tid; i < nr * K; i += NT) p.hg[p.h_off[l] + (long long)r0 * K + i] = hs(l)[i];
       if (l == 0) break;  // dX of the first layer is not needed
       const float* W = p.P + p.w_off[l];
+      if (p.wstage) {
+        const float* wl = ws + p.ws_off[l];
+        for (int k = tid; k < K; k += NT) {
+          float acc[MAXR];
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+          for (int j = 0; j < N; ++j) {
+            const float wv = wl[(long long)j * p.k4[l] + k];
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(cur[min(r, nr - 1) * N + j], wv, acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r)
+            if (r < nr) nxt[r * K + k] = acc[r] * act_grad_f(hs(l)[r * K + k], p.act[l - 1]);
+        }
+        __syncthreads();
+        float* t = cur;
+        cur = nxt;
+        nxt = t;
+        continue;
+      }
       for (int k = tid; k < K; k += NT) {
         float acc[MAXR];
 #pragma unroll
@@ -286,43 +374,87 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
     }
   }
 
-  if (p.dbg & 2) return;
-  if (!(p.dbg & 4)) grid_barrier(p.bar);
 
-  // ------------------------------------------------------------ phase 2
-  // chunk = (layer l, columns k0..k0+KW) of [W_l | b_l]^T; column K is the bias.
-  for (int c = blockIdx.x; c < p.chunks; c += gridDim.x) {
-    int l = 0, k0 = c;
-    while ((p.d[l] + KW) / KW <= k0) {  // ceil((d[l] + 1) / KW) chunks in layer l
+  // chunk -> (layer, first column): ceil((d[l] + 1) / KW) chunks per layer
+  auto chunk_of = [&](int c, int& l, int& k0) {
+    l = 0;
+    k0 = c;
+    while ((p.d[l] + KW) / KW <= k0) {
       k0 -= (p.d[l] + KW) / KW;
       ++l;
     }
     k0 *= KW;
+  };
+  // What this CTA's first chunk needs that no other CTA writes -- the X
+  // columns of a layer-0 chunk (cp.async into shared memory) and the P values
+  // it will update (registers) -- goes in flight before the grid barrier.
+  __syncthreads();  // phase-1 shared-memory traffic is over
+  float pv[2] = {0.0f, 0.0f};
+  const bool first = blockIdx.x < p.chunks;
+  if (first) {
+    int l, k0;
+    chunk_of(blockIdx.x, l, k0);
+    const int K = p.d[l], N = p.d[l + 1], B = p.B;
+    const int kw = min(KW, K + 1 - k0);
+    if (l == 0) {
+      float* hcs = sm + (long long)B * N;
+      for (int i = tid; i < B * KW; i += NT) {
+        const int r = i / KW, kk = i - r * KW, k = k0 + kk;
+        if (kk < kw && k < K)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(hcs + i)),
+                       "l"(p.X + (long long)r * p.ldx + k)
+                       : "memory");
+        else
+          hcs[i] = kk < kw ? 1.0f : 0.0f;  // bias column / past the chunk
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int o = tid + q * NT, j = o / KW, kk = o - j * KW, k = k0 + kk;
+      if (o < N * KW && kk < kw)
+        pv[q] = p.P[k == K ? p.b_off[l] + j : p.w_off[l] + (long long)j * p.ldw[l] + k];
+    }
+  }
+  grid_barrier(p.bar);
+
+  // ------------------------------------------------------------ phase 2
+  // chunk = (layer l, columns k0..k0+KW) of [W_l | b_l]^T; column K is the bias.
+  for (int c = blockIdx.x; c < p.chunks; c += gridDim.x) {
+    int l, k0;
+    chunk_of(c, l, k0);
+    const bool pre = c == (int)blockIdx.x;  // prefetched above
     const int K = p.d[l], N = p.d[l + 1], B = p.B;
     const int kw = min(KW, K + 1 - k0);
     float* dzs = sm;                  // [B][N]
     float* hcs = sm + (long long)B * N;  // [B][KW]
     const float* dzl = p.dzg + p.dz_off[l];
     for (int i = tid; i < B * N; i += NT) dzs[i] = __ldcg(dzl + i);
-    for (int i = tid; i < B * KW; i += NT) {
-      const int r = i / KW, kk = i - r * KW, k = k0 + kk;
-      float v = 0.0f;
-      if (kk < kw) {
-        if (k == K) v = 1.0f;
-        else if (l == 0) v = p.X[(long long)r * p.ldx + k];
-        else v = __ldcg(p.hg + p.h_off[l] + (long long)r * K + k);
+    if (pre && l == 0) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else {
+      for (int i = tid; i < B * KW; i += NT) {
+        const int r = i / KW, kk = i - r * KW, k = k0 + kk;
+        float v = 0.0f;
+        if (kk < kw) {
+          if (k == K) v = 1.0f;
+          else if (l == 0) v = p.X[(long long)r * p.ldx + k];
+          else v = __ldcg(p.hg + p.h_off[l] + (long long)r * K + k);
+        }
+        hcs[i] = v;
       }
-      hcs[i] = v;
     }
     __syncthreads();
-    for (int o = tid; o < N * KW; o += NT) {
+    int q = 0;
+    for (int o = tid; o < N * KW; o += NT, ++q) {
       const int j = o / KW, kk = o - j * KW, k = k0 + kk;
       if (kk >= kw) continue;
       float g = 0.0f;
       for (int r = 0; r < B; ++r) g = fmaf(dzs[r * N + j], hcs[r * KW + kk], g);  // ascending rows
       const long long idx = k == K ? p.b_off[l] + j : p.w_off[l] + (long long)j * p.ldw[l] + k;
       p.G[idx] = g;
-      const float v = p.P[idx] - p.lr * g;  // nn_train.py:365-372
+      const float old = pre && q < 2 ? (q == 0 ? pv[0] : pv[1]) : p.P[idx];
+      const float v = old - p.lr * g;  // nn_train.py:365-372
       p.P[idx] = v;
       if (p.S) p.S[idx] = __float2bfloat16_rn(v);
     }
@@ -386,6 +518,25 @@ int plan(const sg_mlp_small_desc* d, ms::Params& p, size_t& smem, size_t& scratc
   if (p.R > ms::MAXR) return fail(SG_EINVAL, "mlp_small: batch too large");
   // phase 1: h_0..h_L + two dZ buffers; phase 2: dZ_l [B][N] + h columns [B][KW]
   size_t s1 = ((size_t)p.R * hsum + 2ull * p.R * dmax) * sizeof(float);
+  // stage every W_l in shared memory when it fits (rows of fan_in rounded to 16 B)
+  {
+    long long base = ((long long)p.R * hsum + 2ll * p.R * dmax + 31) / 32 * 32;
+    long long off = 0;
+    for (int l = 0; l < d->L; ++l) {
+      p.k4[l] = (d->sizes[l] + 3) / 4 * 4;
+      p.ws_off[l] = off;
+      off += (long long)d->sizes[l + 1] * p.k4[l];
+    }
+    const size_t sw = (size_t)(base + off) * sizeof(float);
+    const char* e = std::getenv("SGB200_MLP_SMALL_WSTAGE");
+    bool aligned = true;  // bulk copies: 16-byte aligned rows
+    for (int l = 0; l < d->L; ++l) aligned = aligned && d->w_off[l] % 4 == 0 && d->ldw[l] % 4 == 0;
+    if (aligned && sw <= 160 * 1024 && !(e && e[0] == '0')) {
+      p.wstage = 1;
+      p.ws_base = base;
+      s1 = sw;
+    }
+  }
   size_t s2 = 0;
   for (int l = 0; l < d->L; ++l)
     s2 = std::max(s2, ((size_t)d->B * d->sizes[l + 1] + (size_t)d->B * ms::KW) * sizeof(float));
@@ -435,6 +586,7 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   if (ldx < d->sizes[0] || ldy < d->sizes[d->L] || (Z && ldz < d->sizes[d->L]))
     return fail(SG_EINVAL, "mlp_small: leading dimension smaller than the row");
   if (int rc = ctx_activate(ctx)) return rc;
+  if (reinterpret_cast<uintptr_t>(P) % 16) p.wstage = 0;  // (shared memory stays sized for it)
   p.P = P;
   p.G = G;
   p.S = static_cast<__nv_bfloat16*>(S_bf16);
@@ -445,7 +597,6 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   p.Z = Z;
   p.ldz = ldz;
   p.loss_out = loss;
-  if (const char* e = std::getenv("SGB200_MLP_SMALL_DBG")) p.dbg = std::atoi(e);
   char* s = static_cast<char*>(scratch);
   p.bar = reinterpret_cast<unsigned*>(s);
   p.loss_part = reinterpret_cast<double*>(s + 256);
@@ -459,8 +610,13 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
     SG_CUDA_TRY(cudaFuncSetAttribute(ms::k_mlp_small_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  int per_sm = 0;
-  SG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ms::k_mlp_small_step, ms::NT, smem));
+  static size_t occ_smem = ~size_t(0);  // occupancy query cached per shared-memory size (host cost per step)
+  static int occ_per_sm = 0;
+  if (occ_smem != smem) {
+    SG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_per_sm, ms::k_mlp_small_step, ms::NT, smem));
+    occ_smem = smem;
+  }
+  const int per_sm = occ_per_sm;
   if ((long long)per_sm * ctx_num_sms(ctx) < ctas) return fail(SG_EINVAL, "mlp_small: grid cannot be co-resident");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
