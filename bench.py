@@ -466,7 +466,9 @@ def _timed(fn, steps, warmup, dist, stream, per_step_events=None):
 
 def broadcast_variant_bench(args, dist, peaks, variant):
     """SURVEY §8(d) c2 variants at the full 2^28 size: scalar a, b (f64 by value;
-    full-reduction cotangents) or (R,1) a, b (row reductions)."""
+    full-reduction cotangents), (R,1) a, b (row reductions), or the main
+    (C,) a, b case in f64 -- the reference's own dtype, where + - * / round
+    exactly like the reference's Python floats (only libm ulps differ)."""
     import statistics
 
     import torch
@@ -478,10 +480,17 @@ def broadcast_variant_bench(args, dist, peaks, variant):
     R, C = args.rows, C_COLS
     n = R * C
     g = torch.Generator(device="cuda").manual_seed(4321)
-    x = torch.rand((R, C), generator=g, device="cuda") * 4 - 2
-    yb = torch.rand((R, C), generator=g, device="cuda") * 2 - 1
+    dt = torch.float64 if variant == "f64" else torch.float32
+    esz = 8 if variant == "f64" else 4
+    x = torch.rand((R, C), generator=g, device="cuda", dtype=dt) * 4 - 2
+    yb = torch.rand((R, C), generator=g, device="cuda", dtype=dt) * 2 - 1
     y, xbar = torch.empty_like(x), torch.empty_like(x)
-    if variant == "scalar":
+    if variant == "f64":
+        a = torch.rand(C, generator=g, device="cuda", dtype=dt) * 4 - 2
+        b = torch.rand(C, generator=g, device="cuda", dtype=dt) * 4 - 2
+        abar, bbar = torch.empty_like(a), torch.empty_like(b)
+        desc = "f64 (the reference's dtype), a, b of shape (C,)"
+    elif variant == "scalar":
         a, b = 0.7, -0.3
         abar, bbar = torch.empty(1, device="cuda"), torch.empty(1, device="cuda")
         desc = "a, b f64 scalars (full-reduction cotangents)"
@@ -503,15 +512,17 @@ def broadcast_variant_bench(args, dist, peaks, variant):
     F.check_errors(module, "affsig")
     fwd = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     grad = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    bpe = BYTES_PER_ELEM * esz // 4  # 20 B/elem in fp32, 40 in f64
     return {
-        "workload": f"c2 variant: sigma.(a.*x.+b) + gradient, 2^28 fp32, {desc}",
-        "value": round(n * BYTES_PER_ELEM / (ms * 1e-3) / 1e9, 1), "unit": "GB/s", "ms_per_step": round(ms, 4),
+        "workload": f"c2 variant: sigma.(a.*x.+b) + gradient, 2^28 {'f64' if esz == 8 else 'fp32'}, {desc}",
+        "value": round(n * bpe / (ms * 1e-3) / 1e9, 1), "unit": "GB/s", "ms_per_step": round(ms, 4),
+        "bytes_per_elem": bpe,
         "kernels_ms": {"fwd_K1": round(fwd, 4), "grad_K2_plus_finalize": round(grad, 4),
-                       "fwd_GBps": round(8 * n / (fwd * 1e-3) / 1e9, 1),
-                       "grad_GBps": round(12 * n / (grad * 1e-3) / 1e9, 1)},
-        "roofline": {"bound": "hbm", "kernel": "sg_ew_grad", "achieved": round(12 * n / (grad * 1e-3) / 1e9, 1),
+                       "fwd_GBps": round(2 * esz * n / (fwd * 1e-3) / 1e9, 1),
+                       "grad_GBps": round(3 * esz * n / (grad * 1e-3) / 1e9, 1)},
+        "roofline": {"bound": "hbm", "kernel": "sg_ew_grad", "achieved": round(3 * esz * n / (grad * 1e-3) / 1e9, 1),
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(12 * n / (grad * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
+                     "frac": round(3 * esz * n / (grad * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
         "gpu_launches_per_step": 3 if variant == "scalar" else 3,
     }
 
@@ -689,8 +700,9 @@ def secondary_benches(args, world, rank, dist):
         try:
             if w == "c3" and world == 1:
                 out.append(dense_c3_bench(args, dist, peaks))
-            elif w in ("c2scalar", "c2col"):
-                out.append(broadcast_variant_bench(args, dist, peaks, "scalar" if w == "c2scalar" else "col"))
+            elif w in ("c2scalar", "c2col", "c2f64"):
+                out.append(broadcast_variant_bench(args, dist, peaks, {"c2scalar": "scalar", "c2col": "col",
+                                                                      "c2f64": "f64"}[w]))
             elif w == "c3tf32" and world == 1:
                 out.append(dense_c3_bench(args, dist, peaks, precision="tf32"))
             elif w == "c4":
@@ -791,7 +803,7 @@ def main():
     ap.add_argument("--rows", type=int, default=R_ROWS)
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--secondary", default="c2scalar,c2col,c1,c3,c3tf32,c4,c5",
+    ap.add_argument("--secondary", default="c2scalar,c2col,c2f64,c1,c3,c3tf32,c4,c5",
                     help="comma list of extra workloads measured in the same run (c1,c3,c4,c5)")
     ap.add_argument("--dense-steps", type=int, default=20)
     ap.add_argument("--mlp-steps", type=int, default=10)
