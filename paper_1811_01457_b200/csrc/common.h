@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
 #include <string>
 
 #include "../../include/sgb200.h"
@@ -34,6 +36,16 @@ inline int cu_fail(CUresult r, const char* what) {
   const char* s = nullptr;
   if (const Driver* d = driver()) d->getErrorString(r, &s);
   return fail(SG_ECUDA, std::string(what) + ": " + (s ? s : "unknown driver error"));
+}
+
+// Function attributes (cudaFuncSetAttribute) are per device: `mask` keeps one
+// bit per device on which the caller already set them.  True the first time
+// on the current device.
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const uint64_t bit = 1ull << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
 }
 
 inline size_t dtype_size(int dt) { return dt == SG_F64 ? 8 : (dt == SG_F32 ? 4 : 2); }

@@ -1100,11 +1100,9 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, BN, TF32, false, g.batch, g.sb);
   if (rc) return rc;
   auto kern = tc::gemm_tc_kernel<TF32, BN, STAGES, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};  // per device
+  if (first_on_device(attr_set))
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr_set = true;
-  }
   const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int num_kb = (g.K + BK - 1) / BK;
   // split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
@@ -1158,11 +1156,9 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false, g.batch, g.sb);
   if (rc) return rc;
   auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};  // per device
+  if (first_on_device(attr_set))
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr_set = true;
-  }
   const int pairs_avail = num_sms / 2;
   const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256) * g.batch;
   const int num_kb = (g.K + BK - 1) / BK;

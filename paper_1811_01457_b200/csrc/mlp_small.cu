@@ -605,15 +605,18 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   for (int l = 1; l < d->L; ++l) hf += (long long)d->B * d->sizes[l];
   p.dzg = p.hg + hf;
   const int ctas = (d->B + p.R - 1) / p.R;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // per device
+  if (first_on_device(attr))
     SG_CUDA_TRY(cudaFuncSetAttribute(ms::k_mlp_small_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  static size_t occ_smem = ~size_t(0);  // occupancy query cached per shared-memory size (host cost per step)
-  static int occ_per_sm = 0;
-  if (occ_smem != smem) {
+  // occupancy query cached per (device, shared-memory size): it costs host time every step
+  thread_local int occ_dev = -1;
+  thread_local size_t occ_smem = 0;
+  thread_local int occ_per_sm = 0;
+  int dev = 0;
+  SG_CUDA_TRY(cudaGetDevice(&dev));
+  if (occ_dev != dev || occ_smem != smem) {
     SG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_per_sm, ms::k_mlp_small_step, ms::NT, smem));
+    occ_dev = dev;
     occ_smem = smem;
   }
   const int per_sm = occ_per_sm;
