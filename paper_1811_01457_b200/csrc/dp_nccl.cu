@@ -17,6 +17,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -24,6 +26,7 @@
 
 namespace sg {
 int ctx_activate(sg_ctx* ctx);
+void ctx_add_sm_reserve(sg_ctx* ctx, int delta);
 }  // namespace sg
 
 using namespace sg;
@@ -34,6 +37,8 @@ struct sg_dp {
   cudaEvent_t fork = nullptr;     // compute -> comm
   cudaEvent_t join = nullptr;     // comm -> compute
   int rank = 0, world = 1, device = 0;
+  sg_ctx* ctx = nullptr;
+  int sm_reserve = 0;  // SMs this communicator keeps free of the persistent GEMMs
 };
 
 namespace {
@@ -126,6 +131,14 @@ int sg_dp_init(sg_ctx* ctx, const uint8_t* unique_id, size_t n, int rank, int wo
     sg_dp_finalize(dp);
     return cuda_fail(e, "dp: stream/event creation");
   }
+  // world > 1: keep SGB200_DP_SM_RESERVE (default 8) SMs free of the
+  // persistent GEMMs so the bucketed all-reduces overlap the backward pass
+  if (world > 1) {
+    const char* e = std::getenv("SGB200_DP_SM_RESERVE");
+    dp->sm_reserve = e ? std::max(0, std::atoi(e)) : 8;
+    dp->ctx = ctx;
+    ctx_add_sm_reserve(ctx, dp->sm_reserve);
+  }
   *out = dp;
   return SG_OK;
 }
@@ -161,6 +174,7 @@ int sg_dp_finalize(sg_dp* dp) {
   if (dp->fork) cudaEventDestroy(dp->fork);
   if (dp->join) cudaEventDestroy(dp->join);
   if (dp->stream) cudaStreamDestroy(dp->stream);
+  if (dp->ctx && dp->sm_reserve) ctx_add_sm_reserve(dp->ctx, -dp->sm_reserve);
   delete dp;
   return rc;
 }

@@ -17,6 +17,7 @@
 #include <fstream>
 #include <functional>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -72,6 +73,7 @@ using namespace sg;
 struct sg_ctx {
   int device = 0;
   int num_sms = 148;
+  std::atomic<int> sm_reserve{0};  // SMs left to concurrent collectives (data parallel, sg_dp_init)
   unsigned long long* d_err = nullptr;
   long long step_limit = 2000000;  // interp.py:23 DEFAULT_STEP_LIMIT
   std::mutex mu;
@@ -155,6 +157,15 @@ int ensure_context(sg_ctx* ctx) {
 
 namespace sg {
 int ctx_num_sms(sg_ctx* ctx) { return ctx->num_sms; }
+// SMs the persistent GEMMs may occupy: all of them, minus what an active
+// data-parallel communicator reserves so its all-reduce kernels can run
+// beside the backward GEMMs (a 1-CTA/SM persistent GEMM with ~227 KB of
+// shared memory leaves no room for an NCCL CTA on the SMs it holds).
+int ctx_compute_sms(sg_ctx* ctx) {
+  const int n = ctx->num_sms - ctx->sm_reserve.load();
+  return n < 2 ? 2 : (n & ~1);
+}
+void ctx_add_sm_reserve(sg_ctx* ctx, int delta) { ctx->sm_reserve += delta; }
 int ctx_activate(sg_ctx* ctx) { return ensure_context(ctx); }
 }  // namespace sg
 

@@ -6,6 +6,7 @@
 
 namespace sg {
 int ctx_num_sms(sg_ctx* ctx);
+int ctx_compute_sms(sg_ctx* ctx);
 int ctx_activate(sg_ctx* ctx);
 }  // namespace sg
 
@@ -60,7 +61,7 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     g.sb = d->stride_b;
     g.so_f32 = d->stride_out;
     g.so_lp = d->stride_lp;
-    return launch_gemm_tc(g, tf32, ctx_num_sms(ctx), st);
+    return launch_gemm_tc(g, tf32, ctx_compute_sms(ctx), st);
   }
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
     if (d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
