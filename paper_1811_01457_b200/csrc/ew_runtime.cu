@@ -308,6 +308,7 @@ struct Launch {
   unsigned gx, gy;
   long long rpb;
   int rowmode = 0;  // gradient kernel: one warp per row (COL operands, no ROW operands)
+  int flat = 0;     // forward kernel: flat address-order walk (SG_FLAT)
 };
 
 long long env_ll(const char* name, long long dflt) {
@@ -354,7 +355,7 @@ Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* arg
 
 std::string variant_key(int k, const int* kinds, const Launch& L) {
   std::ostringstream key;
-  key << "v" << L.vec << "x" << L.bdx << "y" << L.bdy << (L.rowmode ? "r" : "") << "k";
+  key << "v" << L.vec << "x" << L.bdx << "y" << L.bdy << (L.rowmode ? "r" : "") << (L.flat ? "f" : "") << "k";
   for (int i = 0; i < k; ++i) key << kinds[i];
   return key.str();
 }
@@ -373,6 +374,7 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   for (int i = 0; i < k; ++i) has_row |= kinds[i] == SG_ROW;
   src << "#define SG_HAS_COL " << (has_col ? 1 : 0) << "\n#define SG_HAS_ROW " << (has_row ? 1 : 0) << "\n";
   src << "#define SG_ROWMODE " << L.rowmode << "\n";
+  src << "#define SG_FLAT " << L.flat << "\n";
   // tuning overrides, e.g. SGB200_EW_DEFINES="#define SG_UNROLL 8"
   if (const char* extra = std::getenv("SGB200_EW_DEFINES")) src << extra << "\n";
   src << "#define SG_KINDS {";
@@ -502,6 +504,10 @@ int prepare(sg_kernel* kern, int k, const sg_tensor* args, const std::vector<lon
   }
   pr.p.R = s.R;
   pr.p.C = s.C;
+  pr.p.c_log2 = -1;
+  if (s.C > 0 && (s.C & (s.C - 1)) == 0)
+    for (int b = 0; b < 63; ++b)
+      if ((1ll << b) == s.C) pr.p.c_log2 = b;
   pr.p.err = kern->ctx->d_err;
   pr.p.step_limit = kern->ctx->step_limit;
   return SG_OK;
@@ -619,6 +625,16 @@ int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg
   const void* extra[] = {y->ptr};
   Launch L = plan(ctx, s, kern->dtype, args, k, extra, 1, env_ll("SGB200_EW_FWD_BLOCKS_PER_SM", 64),
                   env_ll("SGB200_EW_FWD_BDX", 256));
+  if (env_ll("SGB200_EW_FLAT", 0)) {  // flat address-order walk
+    const long long nvec = s.R * s.C / L.vec;
+    const long long per_block = 256ll * 4;  // 256 threads x SG_UNROLL (4) vectors
+    L.flat = 1;
+    L.bdx = 256;
+    L.bdy = 1;
+    L.gx = (unsigned)((nvec + per_block - 1) / per_block);
+    L.gy = 1;
+    L.rpb = 0;
+  }
   Variant* v = nullptr;
   if ((rc = compile_variant(kern, s, L, &v))) return rc;
   cudaStream_t st = (cudaStream_t)stream;

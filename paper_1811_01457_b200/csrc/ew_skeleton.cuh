@@ -195,6 +195,48 @@ __device__ __forceinline__ void sg_primal_row(const SgEwParams& p, long long r, 
 }
 
 // --------------------------------------------------------------- K1: forward
+#ifndef SG_FLAT
+#define SG_FLAT 0
+#endif
+#if SG_FLAT
+// Flat walk (torch-like): each block covers 256 * SG_UNROLL consecutive
+// vectors of the output, so the whole grid sweeps memory in address order;
+// broadcast operands are re-read per vector (L1 hits).
+__device__ __forceinline__ void sg_load_elem(const SgEwParams& p, long long r, long long c, T (&x)[SG_KT][SG_VEC]) {
+#pragma unroll
+  for (int i = 0; i < SG_K; ++i) {
+    const int kind = sg_kinds[i];
+    const T* base = reinterpret_cast<const T*>(p.in[i]);
+    if (kind == SG_FULL || kind == SG_ROW) {
+      const VT v = kind == SG_FULL ? sg_ldv_stream(base + r * p.C + c) : sg_ldv(base + c);
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) x[i][j] = v.v[j];
+    } else {
+      const T s = kind == SG_COL ? __ldg(base + r) : (kind == SG_SPTR ? base[0] : (T)p.sval[i]);
+#pragma unroll
+      for (int j = 0; j < SG_VEC; ++j) x[i][j] = s;
+    }
+  }
+}
+extern "C" __global__ void __launch_bounds__(256)
+sg_ew_forward(const SgEwParams p) {
+  const long long nvec = p.R * p.C / SG_VEC;
+  const long long v0 = (long long)blockIdx.x * (256 * SG_UNROLL) + threadIdx.x;
+  T* out = reinterpret_cast<T*>(p.out);
+  T xs[SG_UNROLL][SG_KT][SG_VEC];
+  long long rr[SG_UNROLL], cc[SG_UNROLL];
+#pragma unroll
+  for (int u = 0; u < SG_UNROLL; ++u) {
+    const long long e = (v0 + u * 256) * SG_VEC;
+    rr[u] = p.c_log2 >= 0 ? e >> p.c_log2 : e / p.C;
+    cc[u] = e - rr[u] * p.C;
+    if (v0 + u * 256 < nvec) sg_load_elem(p, rr[u], cc[u], xs[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < SG_UNROLL; ++u)
+    if (v0 + u * 256 < nvec) sg_primal_row(p, rr[u], cc[u], xs[u], out);
+}
+#else
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
 sg_ew_forward(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -220,6 +262,8 @@ sg_ew_forward(const SgEwParams p) {
     sg_primal_row(p, r, c, xs, out);
   }
 }
+
+#endif
 
 // ------------------------------------------------------ K2: fused gradient
 // Recomputes the duals from the inputs, writes xbar for full operands and

@@ -37,6 +37,7 @@ typedef struct SgEwParams {
   long long rows_per_block;    /* rows handled by one blockIdx.y                     */
   unsigned long long* err;     /* (element << 24 | site), atomicMin; ~0 = no error   */
   long long step_limit;        /* per-element budget for functions with loops        */
+  int c_log2;                  /* log2(C) when C is a power of two, else -1 (flat K1) */
 } SgEwParams;
 
 #endif
