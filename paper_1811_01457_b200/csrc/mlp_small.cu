@@ -140,6 +140,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
 }
 
+// MR: rows per CTA (compile time, >= p.R) -- no FMAs on duplicated rows
+template <int MR>
 __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant__ Params p) {
   extern __shared__ float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -207,20 +209,21 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
         const float* h0 = hs(l);
         for (int j = warp; j < N; j += NW) {
           const float* w = wl + (long long)j * p.k4[l];
-          float acc[MAXR];
+          float acc[MR];
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+          for (int r = 0; r < MR; ++r) acc[r] = 0.0f;
+#pragma unroll 8
           for (int k = lane; k < K; k += 32) {
             const float wv = w[k];
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(h0[min(r, nr - 1) * K + k], wv, acc[r]);
+            for (int r = 0; r < MR; ++r) acc[r] = fmaf(h0[min(r, nr - 1) * K + k], wv, acc[r]);
           }
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r) acc[r] = warp_sum(acc[r]);
+          for (int r = 0; r < MR; ++r) acc[r] = warp_sum(acc[r]);
           if (lane < nr) {
             float z = 0.0f;
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r)
+            for (int r = 0; r < MR; ++r)
               if (r == lane) z = acc[r];
             hs(l + 1)[lane * N + j] = act_f(z + __ldg(bias + j), p.act[l]);
           }
@@ -242,22 +245,22 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
         // branch-free (clamped indices, zero weights past K, rows past nr
         // duplicate the last one): a guarded FMA lets the compiler sink each
         // load into its branch and serialise the L2 round trips
-        float acc[MAXR];
+        float acc[MR];
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+        for (int r = 0; r < MR; ++r) acc[r] = 0.0f;
         const float* h0 = hs(l);
 #pragma unroll
         for (int i = 0; i < MAXD / 32; ++i) {
           const int k = min(lane + 32 * i, K - 1);
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(h0[min(r, nr - 1) * K + k], wv[i], acc[r]);
+          for (int r = 0; r < MR; ++r) acc[r] = fmaf(h0[min(r, nr - 1) * K + k], wv[i], acc[r]);
         }
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r) acc[r] = warp_sum(acc[r]);
+        for (int r = 0; r < MR; ++r) acc[r] = warp_sum(acc[r]);
         if (lane < nr) {
           float z = 0.0f;
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r)
+          for (int r = 0; r < MR; ++r)
             if (r == lane) z = acc[r];
           hs(l + 1)[lane * N + j] = act_f(z + bj, p.act[l]);
         }
@@ -326,16 +329,17 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
       if (p.wstage) {
         const float* wl = ws + p.ws_off[l];
         for (int k = tid; k < K; k += NT) {
-          float acc[MAXR];
+          float acc[MR];
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+          for (int r = 0; r < MR; ++r) acc[r] = 0.0f;
+#pragma unroll 8
           for (int j = 0; j < N; ++j) {
             const float wv = wl[(long long)j * p.k4[l] + k];
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(cur[min(r, nr - 1) * N + j], wv, acc[r]);
+            for (int r = 0; r < MR; ++r) acc[r] = fmaf(cur[min(r, nr - 1) * N + j], wv, acc[r]);
           }
 #pragma unroll
-          for (int r = 0; r < MAXR; ++r)
+          for (int r = 0; r < MR; ++r)
             if (r < nr) nxt[r * K + k] = acc[r] * act_grad_f(hs(l)[r * K + k], p.act[l - 1]);
         }
         __syncthreads();
@@ -345,9 +349,9 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
         continue;
       }
       for (int k = tid; k < K; k += NT) {
-        float acc[MAXR];
+        float acc[MR];
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r) acc[r] = 0.0f;
+        for (int r = 0; r < MR; ++r) acc[r] = 0.0f;
         constexpr int JC = 16;  // W column values fetched 16 at a time, all in flight
         for (int j0 = 0; j0 < N; j0 += JC) {
           float wv[JC];
@@ -360,11 +364,11 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
           for (int i = 0; i < JC; ++i) {
             const int j = min(j0 + i, N - 1);  // wv = 0 past N (branch-free, as above)
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) acc[r] = fmaf(cur[min(r, nr - 1) * N + j], wv[i], acc[r]);
+            for (int r = 0; r < MR; ++r) acc[r] = fmaf(cur[min(r, nr - 1) * N + j], wv[i], acc[r]);
           }
         }
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r)
+        for (int r = 0; r < MR; ++r)
           if (r < nr) nxt[r * K + k] = acc[r] * act_grad_f(hs(l)[r * K + k], p.act[l - 1]);
       }
       __syncthreads();
@@ -605,19 +609,22 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   for (int l = 1; l < d->L; ++l) hf += (long long)d->B * d->sizes[l];
   p.dzg = p.hg + hf;
   const int ctas = (d->B + p.R - 1) / p.R;
-  static std::atomic<uint64_t> attr{0};  // per device
+  auto kern = p.R == 1 ? ms::k_mlp_small_step<1> : (p.R == 2 ? ms::k_mlp_small_step<2> : ms::k_mlp_small_step<4>);
+  static std::atomic<uint64_t> attr{0};  // per device (all instantiations)
   if (first_on_device(attr))
-    SG_CUDA_TRY(cudaFuncSetAttribute(ms::k_mlp_small_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  // occupancy query cached per (device, shared-memory size): it costs host time every step
-  thread_local int occ_dev = -1;
+    for (auto f : {ms::k_mlp_small_step<1>, ms::k_mlp_small_step<2>, ms::k_mlp_small_step<4>})
+      SG_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  // occupancy query cached per (device, rows, shared-memory size): it costs host time every step
+  thread_local int occ_dev = -1, occ_r = 0;
   thread_local size_t occ_smem = 0;
   thread_local int occ_per_sm = 0;
   int dev = 0;
   SG_CUDA_TRY(cudaGetDevice(&dev));
-  if (occ_dev != dev || occ_smem != smem) {
-    SG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_per_sm, ms::k_mlp_small_step, ms::NT, smem));
+  if (occ_dev != dev || occ_smem != smem || occ_r != p.R) {
+    SG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_per_sm, kern, ms::NT, smem));
     occ_dev = dev;
     occ_smem = smem;
+    occ_r = p.R;
   }
   const int per_sm = occ_per_sm;
   if ((long long)per_sm * ctx_num_sms(ctx) < ctas) return fail(SG_EINVAL, "mlp_small: grid cannot be co-resident");
@@ -631,7 +638,7 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SG_CUDA_TRY(cudaLaunchKernelEx(&cfg, ms::k_mlp_small_step, p));
+  SG_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
