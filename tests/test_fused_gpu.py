@@ -267,6 +267,31 @@ def test_c2_full_size_against_fp64(fused_module):
     assert torch.equal(dx, dx2)
 
 
+def test_c2_f64_at_scale_matches_fp64_arithmetic(fused_module):
+    """c2's sub-function in f64 -- the reference's own dtype -- at 2^26
+    elements: the device path does + - * / in IEEE f64 exactly as the
+    reference's Python floats (--fmad=false), so against the same arithmetic
+    in torch f64 (test-side) y and xbar agree to libm ulps (1e-14, reference
+    rel metric) and the 16384-term column sums to 1e-12 * sum|terms|
+    (summation order only)."""
+    R, C = 1 << 14, 1 << 12
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand((R, C), generator=g, device="cuda", dtype=torch.float64) * 4 - 2
+    yb = torch.rand((R, C), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
+    a = torch.rand(C, generator=g, device="cuda", dtype=torch.float64) * 4 - 2
+    b = torch.rand(C, generator=g, device="cuda", dtype=torch.float64) * 4 - 2
+    y, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", [a, x, b], yb, want_primal=True)
+    z = a * x + b                         # mul then add: two roundings, like the IR
+    s = 1.0 / (1.0 + torch.exp(-z))       # tensor.py:214-215
+    ds = s * (1.0 - s)                    # forward_ad.py sigmoid rule y(1-y)
+    want_x = yb * (ds * a)
+    assert max_rel(y, s) <= 1e-14
+    assert max_rel(dx, want_x) <= 1e-14
+    ta, tb = yb * (ds * x), yb * ds
+    for got, t in ((da, ta), (db, tb)):
+        assert bool(((got - t.sum(0)).abs() <= 1e-12 * t.abs().sum(0).clamp_min(1.0)).all())
+
+
 def test_shape_errors_are_value_errors(fused_module):
     # broadcast conflicts and wrong output shapes: ValueError like tensor.py:118-119
     a = torch.zeros(5, device="cuda")
