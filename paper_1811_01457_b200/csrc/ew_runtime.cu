@@ -320,7 +320,7 @@ long long env_ll(const char* name, long long dflt) {
 // thread-row).  Tuned on B200 (tools/ew_sweep*.sh, c2 shape): the forward
 // kernel streams best with many short-lived blocks (64/SM: ~27 rows each);
 // the gradient kernel amortises its fp64 partial-sum rows over long spans
-// (8/SM, 64-register budget, SG_GRAD_MINB 4).
+// (6/SM, 85-register budget, SG_GRAD_MINB 3, up to 4 rows in flight).
 Launch plan(const sg_ctx* ctx, const Shape2D& s, int dtype, const sg_tensor* args, int k,
             const void* const* extra_ptrs, int n_extra, long long per_sm = 8, long long max_bdx = 256) {
   Launch L;
@@ -377,6 +377,18 @@ std::string build_source(const std::string& user, const std::string& tag, int k,
   src << "#define SG_FLAT " << L.flat << "\n";
   // tuning overrides, e.g. SGB200_EW_DEFINES="#define SG_UNROLL 8"
   if (const char* extra = std::getenv("SGB200_EW_DEFINES")) src << extra << "\n";
+  // gradient kernel: 3 blocks per SM (85-register budget) and as many rows in
+  // flight as x/ybar-style row loads fit: 32 registers of row data per
+  // thread (c2: x + ybar, float4 -> 4 rows; measured on B200, tools/ew_sweep8.sh)
+  {
+    int nfull = 0;
+    for (int i = 0; i < k; ++i) nfull += kinds[i] == SG_FULL;
+    const int words = (nfull + 1) * L.vec * (dtype == SG_F64 ? 2 : 1);  // 32-bit registers per row
+    const bool f64 = dtype == SG_F64;  // f64 measured best at the earlier 4 blocks/SM, 3 rows
+    const int rows = f64 ? 3 : std::max(1, std::min(4, 32 / std::max(1, words)));
+    src << "#ifndef SG_GRAD_MINB\n#define SG_GRAD_MINB " << (f64 ? 4 : 3) << "\n#endif\n";
+    src << "#ifndef SG_GUNROLL\n#define SG_GUNROLL " << rows << "\n#endif\n";
+  }
   src << "#define SG_KINDS {";
   for (int i = 0; i < std::max(1, k); ++i) src << (i ? "," : "") << (i < k ? kinds[i] : 0);
   src << "}\n";
@@ -683,7 +695,8 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   std::vector<const void*> extra = {ybar->ptr, y ? y->ptr : nullptr};
   for (int i = 0; i < k; ++i) extra.push_back(s.kinds[i] == SG_FULL ? argbars[i].ptr : nullptr);
   Launch L = plan(ctx, s, kern->dtype, args, k, extra.data(), (int)extra.size(),
-                  env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", 8), env_ll("SGB200_EW_GRAD_BDX", 256));
+                  env_ll("SGB200_EW_GRAD_BLOCKS_PER_SM", kern->dtype == SG_F64 ? 8 : 6),
+                  env_ll("SGB200_EW_GRAD_BDX", 256));
   // COL operands without ROW operands: warps own rows and walk the columns, so
   // each row's cotangent is one register accumulation + one warp reduction
   // (instead of a shuffle tree per 128 elements) and is written final.

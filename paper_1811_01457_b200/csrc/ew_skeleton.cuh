@@ -25,13 +25,13 @@
 #define SG_UNROLL 4   // rows in flight per thread, forward
 #endif
 #ifndef SG_GUNROLL
-#define SG_GUNROLL 3  // rows in flight per thread, gradient (register budget)
+#define SG_GUNROLL 3  // rows in flight per thread, gradient (the runtime sets it from the operand kinds)
 #endif
 #ifndef SG_RUNROLL
 #define SG_RUNROLL 2  // column chunks in flight per lane, gradient row mode
 #endif
 #ifndef SG_GRAD_MINB
-#define SG_GRAD_MINB 4
+#define SG_GRAD_MINB 3  // blocks per SM the gradient kernel's register budget is sized for
 #endif
 
 struct D { T p; T t[SG_KT]; };
