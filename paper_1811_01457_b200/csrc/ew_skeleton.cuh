@@ -237,7 +237,10 @@ sg_ew_forward(const SgEwParams p) {
     if (v0 + u * 256 < nvec) sg_primal_row(p, rr[u], cc[u], xs[u], out);
 }
 #else
-extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+#ifndef SG_FWD_MINB
+#define SG_FWD_MINB 1  // blocks per SM the forward kernel's register budget is sized for
+#endif
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_FWD_MINB)
 sg_ew_forward(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
