@@ -237,10 +237,13 @@ sg_ew_forward(const SgEwParams p) {
     if (v0 + u * 256 < nvec) sg_primal_row(p, rr[u], cc[u], xs[u], out);
 }
 #else
-#ifndef SG_FWD_MINB
-#define SG_FWD_MINB 1  // blocks per SM the forward kernel's register budget is sized for
-#endif
+// SG_FWD_MINB: optional blocks-per-SM register budget (default: none, the
+// compiler's choice -- an explicit 1 relaxes it to more registers)
+#ifdef SG_FWD_MINB
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_FWD_MINB)
+#else
+extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
+#endif
 sg_ew_forward(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
