@@ -145,11 +145,11 @@ __device__ __forceinline__ void sg_load_row(const SgEwParams& p, long long r, lo
   }
 }
 
-__device__ __forceinline__ long long sg_row_begin(const SgEwParams& p) {
-  return (long long)blockIdx.y * p.rows_per_block;
+__device__ __forceinline__ long long sg_row_begin(const SgEwParams& p, long long by) {
+  return by * p.rows_per_block;
 }
-__device__ __forceinline__ long long sg_row_end(const SgEwParams& p) {
-  long long e = ((long long)blockIdx.y + 1) * p.rows_per_block;
+__device__ __forceinline__ long long sg_row_end(const SgEwParams& p, long long by) {
+  long long e = (by + 1) * p.rows_per_block;
   return e < p.R ? e : p.R;
 }
 // Row walk of thread (by, ty): r = base + it * stride, it in [0, n).
@@ -163,19 +163,29 @@ __device__ __forceinline__ long long sg_row_end(const SgEwParams& p) {
 struct SgRows {
   long long base, stride, n;
 };
-__device__ __forceinline__ SgRows sg_rows(const SgEwParams& p, int ty) {
+__device__ __forceinline__ SgRows sg_rows(const SgEwParams& p, int ty, long long by) {
   SgRows w;
 #if SG_ROW_IL
-  w.base = (long long)blockIdx.y * SG_BDY + ty;
+  w.base = by * SG_BDY + ty;
   w.stride = (long long)gridDim.y * SG_BDY;
   w.n = p.R > w.base ? (p.R - w.base + w.stride - 1) / w.stride : 0;
 #else
-  const long long r0 = sg_row_begin(p), r1 = sg_row_end(p);
+  const long long r0 = sg_row_begin(p, by), r1 = sg_row_end(p, by);
   w.base = r0 + ty;
   w.stride = SG_BDY;
   w.n = r1 > w.base ? (r1 - w.base + SG_BDY - 1) / SG_BDY : 0;
 #endif
   return w;
+}
+// SG_GRAD_REV 1: the gradient kernel walks the row spans last-to-first, to
+// start on the rows the forward kernel finished with (still in L2).  Measured
+// 1.5 % SLOWER in the c2 step on B200 (tools/c2_ab.sh; the forward's dirty
+// output lines are written back under it), so off by default.
+#ifndef SG_GRAD_REV
+#define SG_GRAD_REV 0
+#endif
+__device__ __forceinline__ long long sg_grad_span() {
+  return SG_GRAD_REV ? (long long)(gridDim.y - 1 - blockIdx.y) : (long long)blockIdx.y;
 }
 
 __device__ __forceinline__ void sg_primal_row(const SgEwParams& p, long long r, long long c,
@@ -248,7 +258,7 @@ sg_ew_forward(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
-  const SgRows w = sg_rows(p, ty);
+  const SgRows w = sg_rows(p, ty, blockIdx.y);
   const long long n = w.n;
   T* out = reinterpret_cast<T*>(p.out);
   T inv[SG_KT][SG_VEC];
@@ -364,7 +374,7 @@ sg_ew_grad(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   const bool active = c < p.C;
-  const SgRows w = sg_rows(p, ty);
+  const SgRows w = sg_rows(p, ty, sg_grad_span());
   const T* ybar = reinterpret_cast<const T*>(p.ybar);
 
   SgGradAcc acc;
@@ -460,7 +470,7 @@ sg_ew_grad(const SgEwParams p) {
   // group must take the same trip count, so walk the block's row span
   constexpr int kGroup = SG_BDX >= 32 ? 32 : SG_BDX;
   // the block-uniform trip count: the longest walk of any ty in the block
-  const long long rows_span = sg_rows(p, 0).n;
+  const long long rows_span = sg_rows(p, 0, sg_grad_span()).n;
   const long long gi = ((long long)blockIdx.x * SG_BDX + tx) / kGroup;
   // SG_GUNROLL rows per trip: every row's loads are issued before the first
   // row is computed (the trip count stays block-uniform for the shuffles)
@@ -528,7 +538,7 @@ sg_ew_pack(const SgEwParams p) {
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
-  const SgRows w = sg_rows(p, ty);
+  const SgRows w = sg_rows(p, ty, blockIdx.y);
   const long long plane = p.R * p.C;
   T* pk = reinterpret_cast<T*>(p.pack);
   T inv[SG_KT][SG_VEC];
