@@ -131,6 +131,7 @@ __device__ __forceinline__ void quarter_colsum(float (&acc)[8], float* colsum, l
   }
 }
 
+// 8 rows per thread, all loads in flight (#pragma unroll 8: c3 48.5 us vs 51.5 with 4)
 template <class HT, class DT>
 __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long long ldy, const HT* h,
                                                      long long ldh, long long M, long long N, int act,
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long lon
   const long long r1 = r0 + 8 < M ? r0 + 8 : M;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (ok) {
-#pragma unroll 4
+#pragma unroll 8
     for (long long r = r0; r < r1; ++r) {
       const V8 yb = ld8_f32(ybar + r * ldy + c);
       const V8 hv = ld8(h + r * ldh + c);
