@@ -351,7 +351,8 @@ class ChainEngine:
         self.descs = [dense_desc(self.H[l], self.Ws[l] if precision == "bf16" else self.W[l], self.b[l],
                                  self.acts[l], precision) for l in range(self.L)]
         self.tape = Tape()
-        self.grad_ready = None  # optional callback(layer_index) when layer l's gradients are written
+        self.grad_ready = None  # optional callback(bucket_index) when a bucket's gradients are written
+        self.l0_slices = 1      # data parallel: layer 0's dW in row slices (enable_first_layer_slices)
         self.small = self._plan_small() if small else None
         if chain.layers[0].W is not None:
             self.set_params([(l.W, l.b) for l in chain.layers])
@@ -398,9 +399,37 @@ class ChainEngine:
 
     def _ready(self, l):
         def cb(_entry):
-            if self.grad_ready is not None:
+            if self.grad_ready is None:
+                return
+            if self.l0_slices > 1:
+                if l > 0:  # layer 0's slices already readied their own buckets
+                    self.grad_ready(l + self.l0_slices - 1)
+            else:
                 self.grad_ready(l)
         return cb
+
+    def enable_first_layer_slices(self, slices: int = 4, min_params: int = 8 << 20) -> bool:
+        """Data parallel: split layer 0's dW into `slices` row blocks, each
+        all-reduced as soon as it is written.  Layer 0's bucket is the last
+        one the pullback produces and nothing is left to overlap it, so its
+        exposed collective shrinks to one slice.  The buckets become
+        [W0 rows 0, ..., W0 rows S-1 (+ b0), layer 1, layer 2, ...].  Each
+        slice is the same GEMM restricted to its rows, so gradients are
+        bit-identical to the unsliced step.  Returns whether slicing is on."""
+        F = self.sizes[1]
+        rows = F // max(1, slices)
+        # worth it only for a large last bucket (c4: 16.8 M parameters, 67 MB; the
+        # 1 M of c5 would pay ~50 us of smaller GEMMs to hide ~10 us of collective)
+        if slices < 2 or F % slices or rows % 64 or self.sizes[0] * F < min_params:
+            return False
+        self.l0_slices = slices
+        wo, _ = self.seg[0]
+        ldi = _ld(self.sizes[0])
+        end0 = self.bucket_bounds[0][1]
+        sub = [(wo + k * rows * ldi, wo + (k + 1) * rows * ldi) for k in range(slices - 1)]
+        sub.append((wo + (slices - 1) * rows * ldi, end0))
+        self.bucket_bounds = sub + self.bucket_bounds[1:]
+        return True
 
     # --------------------------------------------------------------- loss
     def loss_and_seed(self):
@@ -433,6 +462,18 @@ class ChainEngine:
             d_out, d_in = self.sizes[l + 1], self.sizes[l]
             dz = self.dZ[l % 2][:, :d_out]
             cs = self.colsum if self.tc else None
+            if l == 0 and self.l0_slices > 1:
+                S = self.l0_slices
+                rows = d_out // S
+                Wop = self.Ws[0] if self.precision == "bf16" else self.W[0]
+                for k in range(S):
+                    r = slice(k * rows, (k + 1) * rows)
+                    desc = dense_desc(self.H[0], Wop[r], self.b[0][r], self.acts[0], self.precision)
+                    dense_backward(desc, dz[:, r], self.gW[0][r], self.gb[0][r],
+                                   colsum_in=None if cs is None else cs[:, r])
+                    if self.grad_ready is not None:
+                        self.grad_ready(k)
+                return
             # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
             # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below
             dense_backward(self.descs[l], dz, self.gW[l], self.gb[l],

@@ -170,6 +170,11 @@ class Trainer:
             if backend not in ("sg", "torch"):
                 raise ValueError(f"unknown dp backend {backend!r}")
             cls = NcclDataParallel if backend == "sg" else DataParallel
+            import os
+
+            slices = int(os.environ.get("SGB200_DP_L0_SLICES", "4"))
+            min_params = int(os.environ.get("SGB200_DP_L0_SLICE_MIN", str(8 << 20)))
+            self.engine.enable_first_layer_slices(slices, min_params)  # before the bucket list is handed over
             self.dp = cls(self.engine.G, self.engine.bucket_bounds, group)
             self.engine.grad_ready = self.dp.ready
             self.dp.broadcast_params(self.engine.P)

@@ -184,6 +184,9 @@ def test_data_parallel_trainer_over_nccl_world1():
             if backend == "sg":
                 assert isinstance(tr.dp, NcclDataParallel)
                 assert tr.use_graph == graph
+            if dp:  # 2 layers: 2 buckets, or 5 with layer 0 in 4 slices
+                sliced = os.environ.get("SGB200_DP_L0_SLICE_MIN") == "0"
+                assert len(tr.engine.bucket_bounds) == (5 if sliced else 2)
             losses = [float(tr.step(X, Y).item()) for _ in range(3)]
             assert tr.replicas_identical()
             if tr.dp is not None and hasattr(tr.dp, "close"):
@@ -196,6 +199,16 @@ def test_data_parallel_trainer_over_nccl_world1():
             l1, p1 = run(True, backend, graph)
             assert l0 == l1, backend
             assert torch.equal(p0, p1), backend
+        # layer 0's dW in 4 row slices, each its own bucket (forced on at this
+        # small size): still bit-identical to the single-GPU step
+        os.environ["SGB200_DP_L0_SLICE_MIN"] = "0"
+        try:
+            for backend, graph in (("torch", False), ("sg", True)):
+                l1, p1 = run(True, backend, graph)
+                assert l0 == l1, backend
+                assert torch.equal(p0, p1), backend
+        finally:
+            del os.environ["SGB200_DP_L0_SLICE_MIN"]
     finally:
         dist.destroy_process_group()
 
