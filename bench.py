@@ -804,7 +804,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--secondary", default="c2scalar,c2col,c2f64,c1,c3,c3tf32,c4,c5",
-                    help="comma list of extra workloads measured in the same run (c1,c3,c4,c5)")
+                    help="comma list of extra workloads measured in the same run (c2scalar,c2col,c2f64,c1,c3,c3tf32,c4,c5)")
     ap.add_argument("--dense-steps", type=int, default=20)
     ap.add_argument("--mlp-steps", type=int, default=10)
     args = ap.parse_args()
