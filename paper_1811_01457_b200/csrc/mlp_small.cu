@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
         const float* h0 = hs(l);
         for (int j = warp; j < N; j += NW) {
           const float* w = wl + (long long)j * p.k4[l];
+          const float bj = __ldg(bias + j);  // issued before the dot product, not after it
           float acc[MR];
 #pragma unroll
           for (int r = 0; r < MR; ++r) acc[r] = 0.0f;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
 #pragma unroll
             for (int r = 0; r < MR; ++r)
               if (r == lane) z = acc[r];
-            hs(l + 1)[lane * N + j] = act_f(z + __ldg(bias + j), p.act[l]);
+            hs(l + 1)[lane * N + j] = act_f(z + bj, p.act[l]);
           }
         }
         __syncthreads();
