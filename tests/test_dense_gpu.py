@@ -370,6 +370,12 @@ def test_small_chain_step_equals_layer_path_and_trains():
 
     ls, trs = run(True)
     ll, _ = run(False)
+    # the same one-launch steps replayed from a CUDA graph: bit-identical
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(2)]).init_params(np.random.default_rng(1))
+    trg = Trainer(chain, B, loss="softmax_xent", lr=0.5, precision="bf16", small=True, graph=True)
+    lg = [float(trg.step(X, Y).item()) for _ in range(20)]
+    assert trg._small_graph is not None
+    assert lg == ls and torch.equal(trg.engine.P, trs.engine.P)
     assert ls[-1] < ls[0] - 0.1
     for a, b in zip(ls, ll):
         assert abs(a - b) <= 1e-2 * max(1.0, abs(b))
