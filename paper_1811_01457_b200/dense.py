@@ -281,6 +281,21 @@ class DenseLayer:
         return 2.0 * self.M * self.K * self.N * (3 if need_dx else 2)
 
 
+def slice_first_layer_buckets(buckets, w_off0: int, fan_in: int, fan_out: int, slices: int):
+    """Bucket list with layer 0's bucket split into `slices` row blocks of W0
+    (the last one running on through b0 to the end of the layer's bucket), or
+    None when fan_out does not split into 64-row multiples.  Host-only (the
+    data-parallel bucket layout; ChainEngine.enable_first_layer_slices)."""
+    rows = fan_out // max(1, slices)
+    if slices < 2 or fan_out % slices or rows % 64:
+        return None
+    ldi = _ld(fan_in)
+    end0 = buckets[0][1]
+    sub = [(w_off0 + k * rows * ldi, w_off0 + (k + 1) * rows * ldi) for k in range(slices - 1)]
+    sub.append((w_off0 + (slices - 1) * rows * ldi, end0))
+    return sub + list(buckets[1:])
+
+
 class ChainEngine:
     """Device state + kernels of a Dense chain's training step on one GPU."""
 
@@ -416,19 +431,15 @@ class ChainEngine:
         [W0 rows 0, ..., W0 rows S-1 (+ b0), layer 1, layer 2, ...].  Each
         slice is the same GEMM restricted to its rows, so gradients are
         bit-identical to the unsliced step.  Returns whether slicing is on."""
-        F = self.sizes[1]
-        rows = F // max(1, slices)
         # worth it only for a large last bucket (c4: 16.8 M parameters, 67 MB; the
         # 1 M of c5 would pay ~50 us of smaller GEMMs to hide ~10 us of collective)
-        if slices < 2 or F % slices or rows % 64 or self.sizes[0] * F < min_params:
+        if self.sizes[0] * self.sizes[1] < min_params:
+            return False
+        b = slice_first_layer_buckets(self.bucket_bounds, self.seg[0][0], self.sizes[0], self.sizes[1], slices)
+        if b is None:
             return False
         self.l0_slices = slices
-        wo, _ = self.seg[0]
-        ldi = _ld(self.sizes[0])
-        end0 = self.bucket_bounds[0][1]
-        sub = [(wo + k * rows * ldi, wo + (k + 1) * rows * ldi) for k in range(slices - 1)]
-        sub.append((wo + (slices - 1) * rows * ldi, end0))
-        self.bucket_bounds = sub + self.bucket_bounds[1:]
+        self.bucket_bounds = b
         return True
 
     # --------------------------------------------------------------- loss

@@ -61,15 +61,16 @@ def _shard_grads(params, X, Y, acts, loss, B_global):
     return lv * f, [(dW * f, db * f) for dW, db in grads]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, sliced=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_1811_01457_b200.dense import slice_first_layer_buckets
         from paper_1811_01457_b200.train import DataParallel, shard_rows
 
         rng = np.random.default_rng(0)  # same data and params on every rank
-        sizes, acts = (20, 13, 7), ("tanh", "identity")
+        sizes, acts = ((20, 256, 7) if sliced else (20, 13, 7)), ("tanh", "identity")
         B = 16
         params = [(rng.uniform(-0.5, 0.5, (sizes[i + 1], sizes[i])), rng.uniform(-0.1, 0.1, sizes[i + 1]))
                   for i in range(2)]
@@ -77,6 +78,13 @@ def _worker(rank, world, port, q):
         Y = rng.uniform(-1, 1, (B, sizes[-1]))
         lv, grads = _shard_grads(params, shard_rows(X, rank, world), shard_rows(Y, rank, world), acts, "mse", B)
         flat, buckets = _pack(grads, sizes)
+        if sliced:  # layer 0's bucket as 4 row slices of W0 (the last through b0), ChainEngine's rule
+            _, segs = _layout(sizes)
+            whole = buckets
+            buckets = slice_first_layer_buckets(buckets, segs[0][0], sizes[0], sizes[1], 4)
+            assert len(buckets) == len(whole) + 3
+            assert buckets[0][0] == whole[0][0] and buckets[3][1] == whole[0][1]
+            assert all(a[1] == b[0] for a, b in zip(buckets[:3], buckets[1:4]))  # contiguous, no overlap
         G = torch.from_numpy(flat)
         dp = DataParallel(G, buckets)
         for i in reversed(range(len(buckets))):  # pullback order: top layer first
@@ -92,12 +100,15 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_bucketed_allreduce_reproduces_full_batch_gradient(world):
+@pytest.mark.parametrize("world,sliced", [(2, False), (4, False), (2, True)])
+def test_bucketed_allreduce_reproduces_full_batch_gradient(world, sliced):
+    """Bucketed all-reduce of shard gradients == full-batch gradient; with
+    `sliced`, layer 0's bucket is split into W0 row slices as data-parallel
+    ChainEngines do for large first layers (readied last, in pullback order)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, sliced)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
