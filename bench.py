@@ -653,18 +653,20 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
     loss_v = float(tr.engine.loss.item())
     replicas_ok = tr.replicas_identical() if world > 1 else True
     small = tr.engine.small is not None  # the whole step in one cooperative launch
-    launches = count_launches(lambda: tr.step(X, Y) if small else tr._device_step())
+    # the whole step as issued eagerly: minibatch load (sg_cast_2d), forward,
+    # loss, pullback, [all-reduce], SGD -- the graph replays exactly these
+    launches = count_launches(lambda: tr.step(X, Y) if small else (tr.engine.load_batch(X, Y), tr._device_step()))
     no_graph_ms = layer_ms = None
     if small:  # beside it: the layer-by-layer tensor-core path in a CUDA graph
         tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=True, small=False)
         layer_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
+        tr2.close()
     elif tr.use_graph:  # the same step without the graph (launch overhead exposed)
         tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=False)
         no_graph_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
-        if tr2.dp is not None and hasattr(tr2.dp, "close"):
-            torch.cuda.synchronize()
-            tr2.dp.close()
+        tr2.close()
     flops = tr.engine.flops_per_step() * world
+    tr.close()
     tflops = flops / (ms * 1e-3) / 1e12
     if small:  # latency-bound: the roofline is the launch, not a pipe
         roof = {"bound": "latency", "kernel": "k_mlp_small_step (one launch per step)",

@@ -215,6 +215,31 @@ SG_API int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, i
                   void* shadow_bf16, void* stream);
 SG_API int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,
                    void* stream);
+/* 2-D cast / copy of a [rows][cols] block between row-strided buffers (the
+ * minibatch load of a training step: fp32 host-layout rows -> the bf16
+ * activation rows the first GEMM reads through TMA). */
+SG_API int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, void* dst, int32_t dst_dtype,
+                      int64_t ld_dst, int64_t rows, int64_t cols, void* stream);
+
+/* ------------------------------------------------ Dense-path domain errors
+ * The reference raises where its float64 ops are undefined: math.exp
+ * overflow (an uncaught OverflowError from scalar_sigmoid / exp,
+ * tensor.py:214-215, 245-250), division by zero (DomainError, tensor.py:
+ * 197-205) and log of p <= 0 (DomainError, tensor.py:230-233), the latter two
+ * wrapped into EvalError by run_blocks (interp.py:117-119).  The Dense-path
+ * kernels compute numerically stable values (max-subtracted log-sum-exp) and,
+ * beside them, evaluate the reference's conditions on the float64 widening of
+ * the same values, OR-ing these bits into a per-context device word:
+ *   sigmoid activation / BCE head:  z < -709.782712893384   -> EXP_OVERFLOW
+ *   softmax cross-entropy:          z >  709.782712893384   -> EXP_OVERFLOW
+ *                                   row sum of exp(z) == 0  -> DIV_ZERO
+ *                                   exp(z_j) / sum == 0     -> LOG_NONPOS
+ * sg_domain_check synchronises `stream`, returns the bits in *flags (and
+ * clears them); SG_EDOMAIN when any is set. */
+#define SG_DOM_EXP_OVERFLOW 1
+#define SG_DOM_DIV_ZERO 2
+#define SG_DOM_LOG_NONPOS 4
+SG_API int sg_domain_check(sg_ctx* ctx, void* stream, int32_t* flags);
 
 /* ------------------------------------------------ small-chain training step
  * The whole step of a small Dense chain -- forward (nn_train.py:189-210), loss

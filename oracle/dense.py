@@ -24,6 +24,7 @@ Two arithmetic modes:
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -182,6 +183,49 @@ def bce(z: np.ndarray, Y: np.ndarray):
 
 
 LOSS_FNS = {"softmax_xent": softmax_xent, "mse": mse, "bce": bce}
+
+
+class DomainError(ValueError):
+    """The reference's DomainError (tensor.py:25-26)."""
+
+
+def _exp_checked(x: float) -> float:
+    return math.exp(x)  # OverflowError("math range error") exactly as the reference's unary_math
+
+
+def check_domain(params, X, Y, acts, loss="softmax_xent"):
+    """Restates where the reference's float64 evaluation of a Dense chain's
+    loss IR raises (the conditions the device kernels flag, SG_DOM_*):
+
+    * ``sigmoid`` activations / the BCE head: ``scalar_sigmoid`` calls
+      ``math.exp(-z)`` per element (tensor.py:214-215, 245-250) ->
+      OverflowError, uncaught by run_blocks;
+    * softmax cross-entropy (the c1 loss IR): ``exp`` per element
+      (OverflowError), ``div`` by a zero row sum (tensor.py:197-205) and
+      ``log`` of p <= 0 (tensor.py:230-233) -> DomainError, in that op order.
+
+    Raises what the reference raises (DomainError here; run_blocks wraps it
+    into EvalError, interp.py:117-119); returns None otherwise."""
+    h = np.asarray(X, dtype=np.float64)
+    for (W, b), act in zip(params, acts):
+        zb = h @ np.asarray(W, dtype=np.float64).T + np.asarray(b, dtype=np.float64)
+        if act == "sigmoid":
+            for v in zb.reshape(-1):
+                _exp_checked(-float(v))
+        h = act_fwd(zb, act)
+    if loss == "bce":
+        for v in h.reshape(-1):
+            _exp_checked(-float(v))
+    elif loss == "softmax_xent":
+        e = np.array([[_exp_checked(float(v)) for v in row] for row in h])
+        s = np.cumsum(e, axis=1)[:, -1:]
+        if bool((s == 0.0).any()):
+            raise DomainError("division by zero")
+        with np.errstate(over="ignore", divide="ignore", invalid="ignore"):
+            p = e / s
+        for v in p.reshape(-1):
+            if v <= 0.0:
+                raise DomainError(f"log of non-positive value {float(v)!r}")
 
 
 def mlp_step(params, X, Y, acts, loss="softmax_xent", lr=0.05, mode="blas"):

@@ -48,6 +48,14 @@ inline bool first_on_device(std::atomic<uint64_t>& mask) {
   return !(mask.fetch_or(bit) & bit);
 }
 
+// Device word of the Dense-path domain flags (SG_DOM_*, sg_domain_check).
+unsigned* ctx_domain_word(sg_ctx* ctx);
+// The reference's float64 thresholds (CPython math.exp / glibc): exp(x) is
+// finite for x <= EXP_MAX_ARG and raises OverflowError above it.
+constexpr double EXP_MAX_ARG = 709.782712893384;
+// fp32 form of "(double)z < -EXP_MAX_ARG": the largest float below -EXP_MAX_ARG
+constexpr float SIGMOID_OVF_F32 = -709.78271484375f;
+
 inline size_t dtype_size(int dt) { return dt == SG_F64 ? 8 : (dt == SG_F32 ? 4 : 2); }
 
 inline long long numel(const sg_tensor& t) {

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "common.h"
@@ -293,18 +294,20 @@ template <class T>
 __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T* y, long long ldy, long long M,
                                              long long N, T scale, void* dz, int dzd, long long lddz, void* dz2,
                                              int dz2d, long long lddz2, float* colsum, long long ldc,
-                                             double* loss_part) {
+                                             double* loss_part, unsigned* dom) {
   __shared__ double red[256];
   const long long c = blockIdx.x * 32ll + threadIdx.x;
   const long long g = blockIdx.y * 8ll + threadIdx.y;
   const long long r0 = g * 32;
   const double lo = 1e-7, hi = 1.0 - 1e-7, one = 1.0;
+  bool ovf = false;
   double lsum = 0.0;
   if (r0 < M && c < N) {
     double acc = 0.0;
     const long long r1 = r0 + 32 < M ? r0 + 32 : M;
     for (long long r = r0; r < r1; ++r) {
       const double zz = (double)z[r * ldz + c], yy = (double)y[r * ldy + c];
+      ovf |= zz < -EXP_MAX_ARG;  // scalar_sigmoid: math.exp(-z) overflows (tensor.py:214-215)
       const double p = one / (one + exp(-zz));
       const bool under = p < lo;
       const double p1 = under ? lo : p;
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T*
     }
     if (colsum) colsum[g * ldc + c] = (float)acc;
   }
+  if (ovf && dom) atomicOr(dom, (unsigned)SG_DOM_EXP_OVERFLOW);
   const int tid = threadIdx.y * 32 + threadIdx.x;
   red[tid] = lsum;
   __syncthreads();
@@ -331,6 +335,43 @@ __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T*
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * -(double)scale;
 }
 
+// The c1 loss IR's float64 domain conditions for one softmax row, checked
+// beside the stable evaluation (see SG_DOM_* in include/sgb200.h):
+// exp(z) overflow (OverflowError), row sum == 0 (div: DomainError) and
+// exp(z_j)/sum == 0 (log: DomainError), evaluated exactly only for rows
+// with an extreme logit (|z| > 700); warp-collective, lanes own columns
+// lane + 32t of the row.
+template <class T, int MAXT>
+__device__ __forceinline__ void softmax_row_domain(const T (&zc)[MAXT], int nt, long long N, int lane, T mx,
+                                                   unsigned* dom) {
+  T mn = (T)INFINITY;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+    if (t < nt && lane + 32 * t < N) mn = min(mn, zc[t]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (!dom || ((double)mx <= 700.0 && (double)mn >= -700.0)) return;  // warp-uniform
+  if ((double)mx > EXP_MAX_ARG) {
+    if (lane == 0) atomicOr(dom, (unsigned)SG_DOM_EXP_OVERFLOW);
+    return;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+    if (t < nt && lane + 32 * t < N) s += exp((double)zc[t]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (s == 0.0) {
+    if (lane == 0) atomicOr(dom, (unsigned)SG_DOM_DIV_ZERO);
+    return;
+  }
+  bool zero = false;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+    if (t < nt && lane + 32 * t < N) zero |= !(exp((double)zc[t]) / s > 0.0) && !isnan((double)zc[t]);
+  if (__any_sync(0xffffffffu, zero) && lane == 0) atomicOr(dom, (unsigned)SG_DOM_LOG_NONPOS);
+}
+
 // softmax cross-entropy for narrow heads (N <= 128): one warp per row, a
 // 32-warp block per 32-row group, so every row's dependent chain (max ->
 // exp-sum -> log -> probabilities) runs concurrently; the group's column sums
@@ -339,7 +380,8 @@ template <class T>
 __global__ void __launch_bounds__(1024) k_softmax_xent_rows(const T* z, long long ldz, const T* y, long long ldy,
                                                             long long M, long long N, T scale, void* dz, int dzd,
                                                             long long lddz, void* dz2, int dz2d, long long lddz2,
-                                                            float* colsum, long long ldc, double* loss_part) {
+                                                            float* colsum, long long ldc, double* loss_part,
+                                                            unsigned* dom) {
   __shared__ float cs[32][129];
   __shared__ double red[32];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
@@ -375,6 +417,7 @@ __global__ void __launch_bounds__(1024) k_softmax_xent_rows(const T* z, long lon
       sy += __shfl_xor_sync(0xffffffffu, sy, o);
       syz += __shfl_xor_sync(0xffffffffu, syz, o);
     }
+    softmax_row_domain<T, 4>(zc, nt, N, lane, mx, dom);
     const T lse = log(se);
     l = (double)(sy * lse - syz);  // -sum y (z - mx - lse)
 #pragma unroll
@@ -416,7 +459,8 @@ template <class T>
 __global__ void __launch_bounds__(256) k_softmax_xent(const T* z, long long ldz, const T* y, long long ldy,
                                                       long long M, long long N, T scale, void* dz, int dzd,
                                                       long long lddz, void* dz2, int dz2d, long long lddz2,
-                                                      float* colsum, long long ldc, double* loss_part) {
+                                                      float* colsum, long long ldc, double* loss_part,
+                                                      unsigned* dom) {
   __shared__ double red[8];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const long long g = blockIdx.x * 8ll + w;  // 32-row group
@@ -453,6 +497,15 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const T* z, long long ldz,
         se += __shfl_xor_sync(0xffffffffu, se, o);
         sy += __shfl_xor_sync(0xffffffffu, sy, o);
         syz += __shfl_xor_sync(0xffffffffu, syz, o);
+      }
+      {
+        T zr[MAXT];
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          const long long c = lane + 32ll * t;
+          zr[t] = (t < nt && c < N) ? z[r * ldz + c] : (T)0;
+        }
+        softmax_row_domain<T, MAXT>(zr, nt, N, lane, mx, dom);
       }
       const T lse = log(se);
       if (lane == 0) lsum += (double)(sy * lse - syz);  // -sum y (z - mx - lse)
@@ -526,6 +579,30 @@ __global__ void k_sgd_vec(float4* p, const float4* g, long long n4, float lr, ui
 __global__ void k_cast(const void* src, int sd, void* dst, int dd, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     st_as(dst, dd, i, ld_as<double>(src, sd, i));
+}
+
+// 2-D cast of a row-strided block; fp32 -> bf16 (the minibatch load) with
+// 8-element vectors: two streaming float4 loads -> one 16-byte store.
+// Blocks walk rows (grid-stride), threads the 8-column vectors of a row.
+__global__ void k_cast2d_f32_bf16(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
+                                  long long ldd, long long rows, long long vecs) {
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + r * lds);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + r * ldd);
+    for (long long v = threadIdx.x; v < vecs; v += blockDim.x) {
+      const float4 a = __ldcs(s4 + 2 * v), b = __ldcs(s4 + 2 * v + 1);
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+      d4[v] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                         *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+    }
+  }
+}
+__global__ void k_cast2d(const void* src, int sd, long long lds, void* dst, int dd, long long ldd, long long rows,
+                         long long cols) {
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x)
+    for (long long c = threadIdx.x; c < cols; c += blockDim.x)
+      st_as(dst, dd, r * ldd + c, ld_as<double>(src, sd, r * lds + c));
 }
 
 }  // namespace dk
@@ -642,6 +719,7 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
   int rc = ctx_activate(ctx);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  unsigned* dom = ctx_domain_word(ctx);
   long long blocks = 0;
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (kind == SG_LOSS_MSE && dtype == SG_F32 && (dz_dtype == SG_BF16 || dz_dtype == SG_F32) && !dz2 &&
@@ -678,22 +756,22 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
     if (dtype == SG_F64)
       dk::k_bce<double><<<grid, dim3(32, 8), 0, st>>>((const double*)z, ld_z, (const double*)y, ld_y, M, N,
                                                        scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
-                                                       ld_colsum, loss_part);
+                                                       ld_colsum, loss_part, dom);
     else
       dk::k_bce<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
                                                       (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-                                                      colsum, ld_colsum, loss_part);
+                                                      colsum, ld_colsum, loss_part, dom);
   } else if (kind == SG_LOSS_SOFTMAX_XENT && N <= 128) {
     blocks = (M + 31) / 32;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dtype == SG_F64)
       dk::k_softmax_xent_rows<double><<<(unsigned)blocks, 1024, 0, st>>>(
           (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-          colsum, ld_colsum, loss_part);
+          colsum, ld_colsum, loss_part, dom);
     else
       dk::k_softmax_xent_rows<float><<<(unsigned)blocks, 1024, 0, st>>>(
           (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
-          ld_dz2, colsum, ld_colsum, loss_part);
+          ld_dz2, colsum, ld_colsum, loss_part, dom);
   } else if (kind == SG_LOSS_SOFTMAX_XENT) {
     if (N > 1024) return fail(SG_EINVAL, "softmax_xent: at most 1024 classes");
     blocks = (M + 255) / 256;
@@ -701,11 +779,11 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
     if (dtype == SG_F64)
       dk::k_softmax_xent<double><<<(unsigned)blocks, 256, 0, st>>>(
           (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-          colsum, ld_colsum, loss_part);
+          colsum, ld_colsum, loss_part, dom);
     else
       dk::k_softmax_xent<float><<<(unsigned)blocks, 256, 0, st>>>(
           (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
-          ld_dz2, colsum, ld_colsum, loss_part);
+          ld_dz2, colsum, ld_colsum, loss_part, dom);
   } else {
     return fail(SG_EINVAL, "loss: unknown kind");
   }
@@ -746,6 +824,32 @@ int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t 
   if (rc) return rc;
   dk::k_cast<<<cap_grid(n, 256, (long long)ctx_num_sms(ctx) * 16), 256, 0, (cudaStream_t)stream>>>(
       src, src_dtype, dst, dst_dtype, n);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, void* dst, int32_t dst_dtype,
+               int64_t ld_dst, int64_t rows, int64_t cols, void* stream) {
+  if (!ctx || !src || !dst) return fail(SG_EINVAL, "null argument");
+  if (rows <= 0 || cols <= 0) return SG_OK;
+  if (ld_src < cols || ld_dst < cols) return fail(SG_EINVAL, "cast_2d: leading dimension smaller than the row");
+  if (src_dtype < SG_F32 || src_dtype > SG_BF16 || dst_dtype < SG_F32 || dst_dtype > SG_BF16)
+    return fail(SG_EINVAL, "cast_2d: dtypes are f32 / f64 / bf16");
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::min<long long>(rows, (long long)ctx_num_sms(ctx) * 16);
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (src_dtype == SG_F32 && dst_dtype == SG_BF16 && cols % 8 == 0 && ld_src % 4 == 0 && ld_dst % 8 == 0 &&
+      a16(src) && a16(dst)) {
+    const long long vecs = cols / 8;
+    const int block = vecs >= 256 ? 256 : (int)((vecs + 31) / 32 * 32);
+    dk::k_cast2d_f32_bf16<<<grid, block, 0, st>>>((const float*)src, ld_src, (__nv_bfloat16*)dst, ld_dst, rows,
+                                                   vecs);
+  } else {
+    const int block = cols >= 256 ? 256 : (int)((cols + 31) / 32 * 32);
+    dk::k_cast2d<<<grid, block, 0, st>>>(src, src_dtype, ld_src, dst, dst_dtype, ld_dst, rows, cols);
+  }
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }

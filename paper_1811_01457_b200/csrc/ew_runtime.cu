@@ -73,8 +73,10 @@ using namespace sg;
 struct sg_ctx {
   int device = 0;
   int num_sms = 148;
-  std::atomic<int> sm_reserve{0};  // SMs left to concurrent collectives (data parallel, sg_dp_init)
+  std::atomic<int> sm_reserve{0};  // SMs left to concurrent collectives: max over live communicators
+  std::vector<int> reserves;       // one entry per live communicator (sg_dp_init / sg_dp_finalize)
   unsigned long long* d_err = nullptr;
+  unsigned* d_dom = nullptr;       // Dense-path domain flags (SG_DOM_*)
   long long step_limit = 2000000;  // interp.py:23 DEFAULT_STEP_LIMIT
   std::mutex mu;
 };
@@ -165,8 +167,25 @@ int ctx_compute_sms(sg_ctx* ctx) {
   const int n = ctx->num_sms - ctx->sm_reserve.load();
   return n < 2 ? 2 : (n & ~1);
 }
-void ctx_add_sm_reserve(sg_ctx* ctx, int delta) { ctx->sm_reserve += delta; }
+// A communicator adds its reserve on init (delta > 0) and removes it on
+// finalize (delta < 0).  The effective reserve is the MAX over the live
+// communicators, not their sum: several trainers in one process share the
+// same free SMs for their collectives, so a leaked or concurrent
+// communicator never shrinks the GEMM grids further.
+void ctx_add_sm_reserve(sg_ctx* ctx, int delta) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (delta > 0) {
+    ctx->reserves.push_back(delta);
+  } else if (delta < 0) {
+    auto it = std::find(ctx->reserves.begin(), ctx->reserves.end(), -delta);
+    if (it != ctx->reserves.end()) ctx->reserves.erase(it);
+  }
+  int m = 0;
+  for (int r : ctx->reserves) m = std::max(m, r);
+  ctx->sm_reserve = m;
+}
 int ctx_activate(sg_ctx* ctx) { return ensure_context(ctx); }
+unsigned* ctx_domain_word(sg_ctx* ctx) { return ctx->d_dom; }
 }  // namespace sg
 
 namespace {
@@ -492,14 +511,25 @@ int check_out(const sg_tensor* t, const std::vector<long long>& shape, int dtype
 }
 
 // Operands that do not fit the 2-D pattern are materialised into temporaries.
+// Temporaries (expanded operands, partial sums) are stream-ordered
+// allocations owned here: freed on every path out of a call, the early
+// error returns included.
 struct Prepared {
   SgEwParams p;
   std::vector<void*> temps;
+  cudaStream_t st = nullptr;
+  Prepared() = default;
+  Prepared(const Prepared&) = delete;
+  Prepared& operator=(const Prepared&) = delete;
+  ~Prepared() {
+    for (void* t : temps) cudaFreeAsync(t, st);
+  }
 };
 
 int prepare(sg_kernel* kern, int k, const sg_tensor* args, const std::vector<long long>& out,
             const Shape2D& s, cudaStream_t st, Prepared& pr) {
   std::memset(&pr.p, 0, sizeof pr.p);
+  pr.st = st;
   long long total = 1;
   for (long long d : out) total *= d;
   for (int i = 0; i < k; ++i) {
@@ -567,6 +597,12 @@ int sg_create(int device, sg_ctx** out) {
     return fail(SG_ECUDA, "cudaMalloc(error word) failed");
   }
   cudaMemset(ctx->d_err, 0xff, sizeof(unsigned long long));
+  if (cudaMalloc(&ctx->d_dom, sizeof(unsigned)) != cudaSuccess) {
+    cudaFree(ctx->d_err);
+    delete ctx;
+    return fail(SG_ECUDA, "cudaMalloc(domain word) failed");
+  }
+  cudaMemset(ctx->d_dom, 0, sizeof(unsigned));
   // keep stream-ordered temporaries cached in the pool between calls
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -581,6 +617,7 @@ int sg_create(int device, sg_ctx** out) {
 int sg_destroy(sg_ctx* ctx) {
   if (!ctx) return SG_OK;
   if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->d_dom) cudaFree(ctx->d_dom);
   delete ctx;
   return SG_OK;
 }
@@ -726,7 +763,6 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   const long long G_row = (long long)L.gy * L.bdy;
   const long long G_col = L.rowmode ? 1 : (long long)L.gx * L.bdx / std::min(32, L.bdx);
   const long long G_blk = (long long)L.gx * L.gy;
-  std::vector<void*> parts;
   for (int i = 0; i < k; ++i) {
     const int kind = s.kinds[i];
     if (kind == SG_FULL) {
@@ -744,7 +780,7 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
     long long n = kind == SG_ROW ? G_row * s.C : kind == SG_COL ? G_col * s.R : G_blk;
     double* pp = nullptr;
     SG_CUDA_TRY(cudaMallocAsync((void**)&pp, (size_t)n * sizeof(double), st));
-    parts.push_back(pp);
+    pr.temps.push_back(pp);
     pr.p.part[i] = pp;
   }
   if ((rc = launch(v->grad, L, pr.p, st))) return rc;
@@ -785,7 +821,6 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
     long long N = kind == SG_ROW ? s.C : kind == SG_COL ? s.R : 1;
     if ((rc = launch_sum_partials(pr.p.part[i], G, N, argbars[i].ptr, kern->dtype, st))) return rc;
   }
-  for (void* pp : parts) SG_CUDA_TRY(cudaFreeAsync(pp, st));
   return release(pr, st);
 }
 
@@ -801,6 +836,21 @@ int sg_ew_check(sg_ctx* ctx, void* stream, int64_t* element, int32_t* site) {
   if (site) *site = (int32_t)(w & 0xffffff);
   return fail(SG_EDOMAIN, "element " + std::to_string((long long)(w >> 24)) + " failed at site " +
                               std::to_string((long long)(w & 0xffffff)));
+}
+
+int sg_domain_check(sg_ctx* ctx, void* stream, int32_t* flags) {
+  if (!ctx) return fail(SG_EINVAL, "null ctx");
+  if (int rc = ensure_context(ctx)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  SG_CUDA_TRY(cudaStreamSynchronize(st));
+  unsigned w = 0;
+  SG_CUDA_TRY(cudaMemcpy(&w, ctx->d_dom, sizeof w, cudaMemcpyDeviceToHost));
+  if (flags) *flags = (int32_t)w;
+  if (!w) return SG_OK;
+  SG_CUDA_TRY(cudaMemset(ctx->d_dom, 0, sizeof(unsigned)));
+  if (w & SG_DOM_EXP_OVERFLOW) return fail(SG_EDOMAIN, "math range error");
+  if (w & SG_DOM_DIV_ZERO) return fail(SG_EDOMAIN, "division by zero");
+  return fail(SG_EDOMAIN, "log of non-positive value 0.0");
 }
 
 int sg_reduce_to(sg_ctx* ctx, const sg_tensor* a, const sg_tensor* b, sg_tensor* out, void* stream) {

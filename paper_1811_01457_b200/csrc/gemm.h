@@ -24,6 +24,7 @@ struct GemmEpilogue {
   long long ld_bf16;
   float* colsum;               // optional column sums of the result per 32-row group:
   long long ld_colsum;         //   colsum[(m / 32)][n], [ceil(M/32)][ld_colsum]
+  unsigned* dom = nullptr;     // domain flags (SG_DOM_*): sigmoid pre-activations that overflow the reference
 };
 
 // Column sums of a 32x32 block held one row per lane (v[i] = column i):
@@ -69,6 +70,7 @@ struct StrictArgs {
   long long ldb;
   bool b_mn;
   int mode, act;
+  unsigned* dom;
   const void* bias;
   const void* aux;
   long long ld_aux;

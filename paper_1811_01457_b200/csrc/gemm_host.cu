@@ -56,6 +56,7 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     g.epi.ld_bf16 = d->ld_lp;
     g.epi.colsum = d->colsum;
     g.epi.ld_colsum = d->ld_colsum;
+    g.epi.dom = ctx_domain_word(ctx);
     g.batch = (int)batch;
     g.sa = d->stride_a;
     g.sb = d->stride_b;
@@ -66,7 +67,7 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
     if (d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
     strict::StrictArgs g{(int)d->M, (int)d->N, (int)d->K, d->A, d->lda, d->a_mn_major != 0,
-                         d->B, d->ldb, d->b_mn_major != 0, d->epilogue, d->act, d->bias, d->aux,
+                         d->B, d->ldb, d->b_mn_major != 0, d->epilogue, d->act, ctx_domain_word(ctx), d->bias, d->aux,
                          d->ld_aux, d->out_pre, d->ld_pre, d->out, d->ld_out, (int)batch, d->stride_a,
                          d->stride_b, d->stride_out};
     return launch_gemm_strict(g, d->precision == SG_PREC_STRICT_FP64, st);

@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(256) strict_gemm_kernel(const StrictArgs g) {
       if (g.mode == SG_EPI_BIAS_ACT) {
         if (bias) v = add_rn(v, bias[n]);  // add(z, b): tensor.py:179-182
         if (pre) pre[(long long)m * g.ld_pre + n] = v;
+        // scalar_sigmoid's math.exp(-z) raises OverflowError (tensor.py:214-215)
+        if (g.act == SG_ACT_SIGMOID && (double)v < -EXP_MAX_ARG && g.dom)
+          atomicOr(g.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
         v = act_fwd(v, g.act);
       } else if (g.mode == SG_EPI_ACT_GRAD) {
         v = mul_rn(v, act_grad(aux[(long long)m * g.ld_aux + n], g.act));

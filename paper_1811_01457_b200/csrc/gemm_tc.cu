@@ -374,6 +374,14 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       for (int i = 0; i < 32; ++i) v[i] += bv[i];
     }
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
+    if (e.act == SG_ACT_SIGMOID) {
+      // the reference's scalar_sigmoid computes math.exp(-z): OverflowError for
+      // z < -709.78 (tensor.py:214-215); flagged, the value below is still 0
+      bool ovf = false;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ovf |= v[i] <= SIGMOID_OVF_F32;
+      if (__any_sync(0xffffffffu, ovf) && lane == 0 && e.dom) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
+    }
     act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
     if (hstaged) {

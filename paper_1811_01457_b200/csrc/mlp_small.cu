@@ -61,6 +61,7 @@ struct Params {
   float* Z;  // optional top-layer output [B][ldz]
   long long ldz;
   double* loss_out;
+  unsigned* dom;       // domain flags (SG_DOM_*, sg_domain_check)
   // scratch
   unsigned* bar;       // {arrivals, generation}
   double* loss_part;   // [B]
@@ -74,6 +75,38 @@ struct Params {
   int k4[MAXL];        // staged row stride (fan_in rounded up to 4 floats = 16 bytes)
 };
 
+__device__ __forceinline__ float act_f(float z, int a);
+// act_f plus the reference's overflow condition: scalar_sigmoid's math.exp(-z)
+// raises OverflowError for z < -709.78 (tensor.py:214-215)
+__device__ __forceinline__ float act_dom(float z, int a, unsigned* dom) {
+  if (a == SG_ACT_SIGMOID && z <= SIGMOID_OVF_F32 && dom) atomicOr(dom, (unsigned)SG_DOM_EXP_OVERFLOW);
+  return act_f(z, a);
+}
+// The c1 loss IR's float64 domain conditions for one softmax row z[0..N)
+// (exp overflow, row sum == 0, exp(z_j)/sum == 0; see include/sgb200.h),
+// evaluated exactly only when the row holds an extreme logit.  Warp-collective.
+__device__ __forceinline__ void softmax_row_domain(const float* z, int N, int lane, float mx, unsigned* dom) {
+  float mn = INFINITY;
+  for (int c = lane; c < N; c += 32) mn = fminf(mn, z[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (!dom || ((double)mx <= 700.0 && (double)mn >= -700.0)) return;
+  if ((double)mx > EXP_MAX_ARG) {
+    if (lane == 0) atomicOr(dom, (unsigned)SG_DOM_EXP_OVERFLOW);
+    return;
+  }
+  double se = 0.0;
+  for (int c = lane; c < N; c += 32) se += exp((double)z[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (se == 0.0) {
+    if (lane == 0) atomicOr(dom, (unsigned)SG_DOM_DIV_ZERO);
+    return;
+  }
+  bool zero = false;
+  for (int c = lane; c < N; c += 32) zero |= !(exp((double)z[c]) / se > 0.0) && !isnan(z[c]);
+  if (__any_sync(0xffffffffu, zero) && lane == 0) atomicOr(dom, (unsigned)SG_DOM_LOG_NONPOS);
+}
 __device__ __forceinline__ float act_f(float z, int a) {
   switch (a) {
     case SG_ACT_SIGMOID: return 1.0f / (1.0f + expf(-z));  // tensor.py:214-215
@@ -226,7 +259,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
 #pragma unroll
             for (int r = 0; r < MR; ++r)
               if (r == lane) z = acc[r];
-            hs(l + 1)[lane * N + j] = act_f(z + bj, p.act[l]);
+            hs(l + 1)[lane * N + j] = act_dom(z + bj, p.act[l], p.dom);
           }
         }
         __syncthreads();
@@ -263,7 +296,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
 #pragma unroll
           for (int r = 0; r < MR; ++r)
             if (r == lane) z = acc[r];
-          hs(l + 1)[lane * N + j] = act_f(z + bj, p.act[l]);
+          hs(l + 1)[lane * N + j] = act_dom(z + bj, p.act[l], p.dom);
         }
       }
       __syncthreads();
@@ -282,6 +315,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_small_step(const __grid_constant_
           float mx = -INFINITY;
           for (int c = lane; c < N; c += 32) mx = fmaxf(mx, z[c]);
           mx = warp_max(mx);
+          softmax_row_domain(z, N, lane, mx, p.dom);
           float se = 0.0f, sy = 0.0f, syz = 0.0f;
           for (int c = lane; c < N; c += 32) {
             const float d = z[c] - mx, yc = y[c];
@@ -602,6 +636,7 @@ int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* 
   p.Z = Z;
   p.ldz = ldz;
   p.loss_out = loss;
+  p.dom = ctx_domain_word(ctx);
   char* s = static_cast<char*>(scratch);
   p.bar = reinterpret_cast<unsigned*>(s);
   p.loss_part = reinterpret_cast<double*>(s + 256);

@@ -139,9 +139,10 @@ def _lib():
         lib.sg_mlp_small_scratch_bytes.argtypes = [P, ctypes.POINTER(I64)]
         lib.sg_mlp_small_step.argtypes = [P, P, P, P, P, P, I64, P, I64, P, I64, P, P, I64, P]
         lib.sg_cast.argtypes = [P, P, I32, P, I32, I64, P]
+        lib.sg_cast_2d.argtypes = [P, P, I32, I64, P, I32, I64, I64, I64, P]
         lib.sg_dense_forward.argtypes = [P, ctypes.POINTER(DenseDesc), P, I64, P, I64, P, I64, P]
         lib.sg_dense_backward.argtypes = [P, ctypes.POINTER(DenseDesc), ctypes.POINTER(DenseGrad), P]
-        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast",
+        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d",
                   "sg_dense_forward", "sg_dense_backward"):
             getattr(lib, n).restype = ctypes.c_int
         _bound = True
@@ -160,14 +161,32 @@ def _ldt(t):
     return 0 if t is None else t.stride(0)
 
 
+def cast_rows(src, dst, stream=None) -> None:
+    """dst[:, :] = src (cast to dst's dtype) with the library's 2-D cast kernel
+    (``sg_cast_2d``): rows may be padded (row strides), columns unit-stride."""
+    if src.dim() != 2 or dst.dim() != 2 or tuple(src.shape) != tuple(dst.shape):
+        raise ValueError(f"cast_rows: shapes {tuple(src.shape)} -> {tuple(dst.shape)}")
+    if src.stride(1) != 1 or dst.stride(1) != 1:
+        raise ValueError("cast_rows: rows must be unit-stride")
+    if not src.is_cuda:
+        raise ValueError("cast_rows: the source must be a device tensor (copy host batches in first)")
+    rt.check(_lib().sg_cast_2d(rt.context(), _p(src), _dt(src), src.stride(0), _p(dst), _dt(dst), dst.stride(0),
+                               src.shape[0], src.shape[1], rt.stream_ptr(stream)), "sg_cast_2d")
+
+
 def dense_desc(X, W, b, act: str, precision: str) -> DenseDesc:
     """sg_dense_desc of one layer: X [batch][fan_in], W [fan_out][fan_in] (the
     precision's operand dtype), b [fan_out]."""
     from .gemm import PREC
 
+    from .gemm import check_dtypes
+
+    check_dtypes(precision, operands=(("X", X), ("W", W)), fp32=(("b", b),))
     d = DenseDesc()
     d.batch, d.fan_in = X.shape
     d.fan_out = W.shape[0]
+    if W.shape[1] != d.fan_in:
+        raise ValueError(f"dense: W of shape {tuple(W.shape)} does not take {d.fan_in} inputs")
     d.precision, d.act = PREC[precision], ACT[act]
     d.X, d.ldx = _p(X), _ldt(X)
     d.W, d.ldw = _p(W), _ldt(W)
@@ -180,10 +199,23 @@ def _need(name, t, rows, cols):
         raise ValueError(f"dense: {name} of shape {tuple(t.shape)} cannot hold {rows} x {cols}")
 
 
+def _prec(desc: DenseDesc) -> str:
+    from .gemm import PREC
+
+    return {v: k for k, v in PREC.items()}[desc.precision]
+
+
 def dense_forward(desc: DenseDesc, H=None, H_f32=None, Z=None, stream=None) -> None:
     """sg_dense_forward: H = act(X W^T + b) (nn_train.py:189-196) in one GEMM."""
+    from .gemm import check_dtypes
+
     for name, t in (("H", H), ("H_f32", H_f32), ("Z", Z)):
         _need(name, t, desc.batch, desc.fan_out)
+    prec = _prec(desc)
+    if prec == "bf16":
+        check_dtypes(prec, fp32=(("H_f32", H_f32), ("Z", Z)), lp=(("H", H),))
+    else:
+        check_dtypes(prec, fp32=(("H", H), ("Z", Z)), lp=(("H_f32", H_f32),))
     rt.check(_lib().sg_dense_forward(rt.context(), ctypes.byref(desc), _p(H), _ldt(H), _p(H_f32), _ldt(H_f32),
                                      _p(Z), _ldt(Z), rt.stream_ptr(stream)), "sg_dense_forward")
 
@@ -199,6 +231,18 @@ def dense_backward(desc: DenseDesc, dZ, dW, db, dX=None, act_prev: str = "identi
         _need(name, t, (desc.batch + 31) // 32, desc.fan_out if name == "colsum_in" else desc.fan_in)
     if db is None or db.numel() < desc.fan_out:
         raise ValueError(f"dense: db needs {desc.fan_out} elements")
+    from .gemm import check_dtypes
+
+    prec = _prec(desc)
+    check_dtypes(prec, operands=(("dZ", dZ),), fp32=(("dW", dW), ("db", db)))
+    check_dtypes(prec, colsum=colsum_in)
+    check_dtypes(prec, colsum=colsum_out)
+    if dX is not None:
+        import torch
+
+        ok = (torch.bfloat16, torch.float32) if prec == "bf16" else (dZ.dtype,)
+        if dX.dtype not in ok:
+            raise ValueError(f"dense: dX must be one of {ok} for precision {prec!r}, not {dX.dtype}")
     g = DenseGrad()
     g.dZ, g.ld_dz = _p(dZ), _ldt(dZ)
     g.colsum_in, g.ld_colsum_in = _p(colsum_in), _ldt(colsum_in)
@@ -259,7 +303,7 @@ class DenseLayer:
 
     def forward(self, X=None):
         if X is not None:
-            self.X.copy_(X, non_blocking=True)
+            cast_rows(X, self.X)
         dense_forward(self.desc(), H=self.H)
         return self.H
 
@@ -294,6 +338,23 @@ def slice_first_layer_buckets(buckets, w_off0: int, fan_in: int, fan_out: int, s
     sub = [(w_off0 + k * rows * ldi, w_off0 + (k + 1) * rows * ldi) for k in range(slices - 1)]
     sub.append((w_off0 + (slices - 1) * rows * ldi, end0))
     return sub + list(buckets[1:])
+
+
+def bucket_of_layer(layer: int, l0_slices: int = 1, slice_k: int = 0) -> int:
+    """Index of the gradient bucket that holds `layer` (and, for layer 0 in
+    `l0_slices` > 1 row slices, its slice `slice_k`) in the bucket list of
+    slice_first_layer_buckets: [W0 slice 0..S-1 (+ b0), layer 1, layer 2, ...]."""
+    if l0_slices <= 1:
+        return layer
+    return slice_k if layer == 0 else layer + l0_slices - 1
+
+
+def pullback_ready_order(n_layers: int, l0_slices: int = 1) -> list:
+    """Bucket indices in the order the pullback readies them: the top layer
+    first, down to layer 1, then layer 0's slices in ascending row order
+    (ChainEngine._make_backward / _ready).  Host-only; the gloo tests replay it."""
+    order = [bucket_of_layer(l, l0_slices) for l in range(n_layers - 1, 0, -1)]
+    return order + [bucket_of_layer(0, l0_slices, k) for k in range(max(1, l0_slices))]
 
 
 class ChainEngine:
@@ -390,12 +451,21 @@ class ChainEngine:
 
     # ------------------------------------------------------------- inputs
     def load_batch(self, X, Y) -> None:
-        """Copy one minibatch into the engine's input/target buffers."""
+        """Load one minibatch (device tensors) with the library's kernels: X is
+        cast into the first layer's activation rows (the operand dtype of the
+        first GEMM) by ``sg_cast_2d``; Y is read IN PLACE by the loss kernel
+        when it already has the master dtype and unit-stride rows (else it is
+        cast into the engine's own target buffer).  No torch kernels: this
+        runs inside the captured training step."""
         d0 = self.sizes[0]
         if tuple(X.shape) != (self.B, d0) or tuple(Y.shape) != (self.B, self.sizes[-1]):
             raise ValueError(f"batch shapes {tuple(X.shape)}, {tuple(Y.shape)} do not match the engine")
-        self.H[0].copy_(X, non_blocking=True)
-        self.Y.copy_(Y, non_blocking=True)
+        cast_rows(X, self.H[0])
+        if Y.dtype == self.mdt and Y.is_cuda and Y.stride(1) == 1:
+            self.Yin = Y
+        else:
+            cast_rows(Y, self.Y)
+            self.Yin = self.Y
 
     # ------------------------------------------------------------ forward
     def forward(self):
@@ -416,11 +486,8 @@ class ChainEngine:
         def cb(_entry):
             if self.grad_ready is None:
                 return
-            if self.l0_slices > 1:
-                if l > 0:  # layer 0's slices already readied their own buckets
-                    self.grad_ready(l + self.l0_slices - 1)
-            else:
-                self.grad_ready(l)
+            if l > 0 or self.l0_slices <= 1:  # layer 0's slices ready their own buckets
+                self.grad_ready(bucket_of_layer(l, self.l0_slices))
         return cb
 
     def enable_first_layer_slices(self, slices: int = 4, min_params: int = 8 << 20) -> bool:
@@ -453,8 +520,10 @@ class ChainEngine:
         ident = self.acts[top] == "identity"
         strict = not self.tc
         target = dz if ident else self.dH
+        Y = getattr(self, "Yin", None)
+        Y = self.Y if Y is None else Y
         rt.check(lib.sg_loss(ctx, LOSSES[self.loss_kind], _p(self.Zt), _dt(self.Zt), self.Zt.stride(0),
-                             _p(self.Y), self.Y.stride(0), self.B, dL, self.scale, _p(self.loss),
+                             _p(Y), Y.stride(0), self.B, dL, self.scale, _p(self.loss),
                              _p(self.loss_part), self.loss_part.numel(), _p(target), _dt(target),
                              target.stride(0), None, 0, 0,
                              None if (strict or not ident) else _p(self.colsum), self.colsum.stride(0), st),
@@ -483,7 +552,7 @@ class ChainEngine:
                     dense_backward(desc, dz[:, r], self.gW[0][r], self.gb[0][r],
                                    colsum_in=None if cs is None else cs[:, r])
                     if self.grad_ready is not None:
-                        self.grad_ready(k)
+                        self.grad_ready(bucket_of_layer(0, S, k))
                 return
             # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
             # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below

@@ -66,6 +66,43 @@ def _ld(t):
     return t.stride(0)
 
 
+def _want_dtypes(precision: str):
+    """(operand, fp32-side, bf16-side) torch dtypes of a precision: operands
+    A/B/aux, the fp32 outputs out/out_pre/bias/colsum, and out_lp."""
+    import torch
+
+    if precision not in PREC:
+        raise ValueError(f"gemm: unknown precision {precision!r}")
+    if precision == "bf16":
+        return torch.bfloat16, torch.float32, torch.bfloat16
+    if precision == "strict_fp64":
+        return torch.float64, torch.float64, None
+    return torch.float32, torch.float32, None
+
+
+def check_dtypes(precision: str, operands=(), fp32=(), lp=(), colsum=None) -> None:
+    """Reject tensors whose dtype the kernel would misread: the C descriptors
+    carry no dtype, so a wrong one would be read as garbage or written past
+    its allocation (an fp32 epilogue into a bf16 buffer writes twice its
+    size).  ``operands``/``fp32``/``lp`` are (name, tensor-or-None) pairs."""
+    op, wide, narrow = _want_dtypes(precision)
+    import torch
+
+    def need(name, t, dt):
+        if t is not None and t.dtype != dt:
+            raise ValueError(f"{name} must be {dt} for precision {precision!r}, not {t.dtype}")
+
+    for name, t in operands:
+        need(name, t, op)
+    for name, t in fp32:
+        need(name, t, wide)
+    for name, t in lp:
+        if t is not None and narrow is None:
+            raise ValueError(f"{name} is a bf16-precision output (precision {precision!r})")
+        need(name, t, narrow)
+    need("colsum", colsum, torch.float32)
+
+
 def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
          epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
          out_pre=None, colsum=None, stream=None):
@@ -82,9 +119,11 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
         Kb, Nb = B.shape
     else:
         Nb, Kb = B.shape
+    if K is None and Ka != Kb:
+        raise ValueError(f"gemm: inner dimensions differ ({Ka} vs {Kb}); pass K to use a prefix")
     M = Ma if M is None else M
     N = Nb if N is None else N
-    K = min(Ka, Kb) if K is None else K
+    K = Ka if K is None else K
     if M > Ma or N > Nb or K > min(Ka, Kb):
         raise ValueError(f"gemm: M, N, K = {M}, {N}, {K} exceed the operands {tuple(A.shape)} x {tuple(B.shape)}")
     for name, t in (("out", out), ("out_lp", out_lp), ("out_pre", out_pre), ("aux", aux)):
@@ -92,6 +131,11 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
             raise ValueError(f"gemm: {name} of shape {tuple(t.shape)} cannot hold the {M} x {N} result")
     if bias is not None and bias.numel() < N:
         raise ValueError(f"gemm: bias has {bias.numel()} elements, {N} needed")
+    if epilogue == "act_grad" and aux is None:
+        raise ValueError("gemm: the act_grad epilogue needs aux (the saved activation)")
+    check_dtypes(precision, operands=(("A", A), ("B", B), ("aux", aux)),
+                 fp32=(("out", out), ("out_pre", out_pre), ("bias", bias)), lp=(("out_lp", out_lp),),
+                 colsum=colsum)
     if colsum is not None and (colsum.dim() != 2 or colsum.shape[0] < (M + 31) // 32 or colsum.shape[1] < N):
         raise ValueError(f"gemm: colsum of shape {tuple(colsum.shape)} cannot hold ({(M + 31) // 32}, {N}) partials")
     d = GemmDesc()
@@ -131,6 +175,13 @@ def bmm(A, B, out=None, *, a_mn=False, b_mn=False, precision="bf16", epilogue="s
     Kb, Nb = (B.shape[1], B.shape[2]) if b_mn else (B.shape[2], B.shape[1])
     if Ka != Kb:
         raise ValueError(f"bmm shapes {tuple(A.shape)} x {tuple(B.shape)}")
+    for name, t in (("out", out), ("out_lp", out_lp)):
+        if t is not None and (t.dim() != 3 or t.shape[0] != L or t.shape[1] < Ma or t.shape[2] < Nb):
+            raise ValueError(f"bmm: {name} of shape {tuple(t.shape)} cannot hold {L} x {Ma} x {Nb}")
+    if bias is not None and bias.numel() < Nb:
+        raise ValueError(f"bmm: bias has {bias.numel()} elements, {Nb} needed")
+    check_dtypes(precision, operands=(("A", A), ("B", B)), fp32=(("out", out), ("bias", bias)),
+                 lp=(("out_lp", out_lp),))
     d = GemmDesc()
     d.M, d.N, d.K = int(Ma), int(Nb), int(Ka)
     (d.lda, d.stride_a), (d.ldb, d.stride_b) = _ld3(A), _ld3(B)

@@ -24,9 +24,10 @@ EXPORTS = (
     "sg_version", "sg_create", "sg_destroy", "sg_last_error",
     "sg_ew_compile", "sg_ew_forward", "sg_ew_grad", "sg_ew_pack", "sg_ew_check",
     "sg_ew_set_step_limit", "sg_ew_compile_only", "sg_ew_variant_count", "sg_reduce_to",
-    "sg_gemm", "sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast",
+    "sg_gemm", "sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d",
     "sg_dense_forward", "sg_dense_backward", "sg_mlp_small_scratch_bytes", "sg_mlp_small_step",
     "sg_dp_available", "sg_dp_unique_id", "sg_dp_init", "sg_dp_allreduce", "sg_dp_wait", "sg_dp_finalize",
+    "sg_domain_check",
 )
 
 
@@ -138,6 +139,39 @@ def stream_ptr(stream=None) -> int:
 
     s = torch.cuda.current_stream() if stream is None else stream
     return int(s.cuda_stream)
+
+
+# ------------------------------------------------------- domain errors
+SG_DOM_EXP_OVERFLOW, SG_DOM_DIV_ZERO, SG_DOM_LOG_NONPOS = 1, 2, 4
+
+
+def domain_check(stream=None, function: str = "loss") -> None:
+    """Surface the Dense-path domain flags (``sg_domain_check``) the way the
+    reference raises them: ``math.exp`` overflow as ``OverflowError("math
+    range error")`` (uncaught by run_blocks, tensor.py:245-250), division by
+    zero and log of p <= 0 as ``EvalError`` wrapping a ``DomainError``
+    (tensor.py:197-205, 230-233, interp.py:117-119).  When several are set,
+    the one the reference's op order reaches first wins: the forward's
+    exp/sigmoid, then the loss's div, then its log.  Synchronises ``stream``
+    and clears the flags."""
+    lib = load_library()
+    if not getattr(lib.sg_domain_check, "_bound", False):
+        lib.sg_domain_check.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
+        lib.sg_domain_check.restype = ctypes.c_int
+        lib.sg_domain_check._bound = True
+    flags = ctypes.c_int32(0)
+    st = lib.sg_domain_check(context(), stream_ptr(stream), ctypes.byref(flags))
+    if st not in (SG_OK, SG_EDOMAIN):
+        check(st, "sg_domain_check")
+    f = flags.value
+    if not f:
+        return
+    if f & SG_DOM_EXP_OVERFLOW:
+        raise OverflowError("math range error")
+    from .fused import EvalError
+
+    msg = "division by zero" if f & SG_DOM_DIV_ZERO else "log of non-positive value 0.0"
+    raise EvalError(function, "", -1, msg) from DomainError(msg)
 
 
 # ---------------------------------------------------------- descriptors

@@ -13,6 +13,7 @@ that layer's dW/db are enqueued, so they overlap the rest of the pullback.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 
 import numpy as np
@@ -149,6 +150,8 @@ class Trainer:
     or "torch" (``torch.distributed`` async all-reduce; the gloo CPU path).
     """
 
+    MAX_GRAPHS = 4
+
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", lr: float = 0.05,
                  precision: str = "bf16", dp: bool = False, group=None, graph: bool = False,
                  dp_backend: str | None = None, small: bool = True):
@@ -184,7 +187,8 @@ class Trainer:
         # torch.distributed's async work handles are host-side objects; the
         # library's communicator is stream-ordered and can live in a graph
         self.use_graph = graph and (self.dp is None or isinstance(self.dp, NcclDataParallel))
-        self._eager_steps = 0
+        self._graphs = collections.OrderedDict()  # (X, Y) buffers -> captured step (LRU)
+        self._last_key = None
         self._small_key = self._small_graph = None  # one-launch step: replayed graph per (X, Y, lr)
 
     def _device_step(self):
@@ -213,23 +217,76 @@ class Trainer:
                 return self.engine.loss
             self._small_key, self._small_graph = key, None
             return self.engine.small_step(X, Y, self.lr)
-        self.engine.load_batch(X, Y)
-        if self.use_graph and self._eager_steps > 0:
-            # the first step ran eagerly (one-time kernel attribute setup);
-            # capture once without warm-up so no extra update is applied
-            if self.graph is None:
-                self.graph = Tape.capture(self._device_step, warmup=0)
-            self.graph.replay()
-        else:
+        if not self.use_graph:
+            self.engine.load_batch(X, Y)
             self._device_step()
-            self._eager_steps += 1
+            return self.engine.loss
+        # CUDA graphs of the whole step, the minibatch load included (it reads X
+        # and Y in place, so a graph is keyed by their buffers): the first step
+        # on a (X, Y) pair runs eagerly (one-time kernel attribute setup), the
+        # second captures -- without warm-up, so no extra update is applied --
+        # and later ones replay.  A few pairs are kept (double-buffered loaders).
+        key = (X.data_ptr(), Y.data_ptr(), tuple(X.shape), tuple(Y.shape), X.stride(0), Y.stride(0),
+               X.dtype, Y.dtype)
+        g = self._graphs.get(key)
+        if g is None and self._last_key == key:
+            g = Tape.capture(lambda: (self.engine.load_batch(X, Y), self._device_step()), warmup=0)
+            self._graphs[key] = g
+            while len(self._graphs) > self.MAX_GRAPHS:
+                self._graphs.popitem(last=False)
+        self._last_key = key
+        if g is not None:
+            self._graphs.move_to_end(key)
+            self.graph = g
+            g.replay()
+        else:
+            self.engine.load_batch(X, Y)
+            self._device_step()
         return self.engine.loss
+
+    def check(self) -> None:
+        """Raise what the reference would have raised on the steps run since
+        the last check (synchronises): OverflowError for math.exp overflow,
+        EvalError(DomainError) for division by zero / log of p <= 0 in the
+        loss (runtime.domain_check; include/sgb200.h SG_DOM_*).  The values
+        themselves are computed stably whatever the flags say."""
+        from . import runtime as rt
+
+        rt.domain_check(function="loss")
 
     def replicas_identical(self) -> bool:
         """Data parallel: the parameter replicas are bit-identical on all ranks."""
         if self.dp is None:
             return True
         return replicas_identical(self.engine.P, self.dp.group)
+
+    def close(self) -> None:
+        """Release the data-parallel communicator (its NCCL comm and the SMs it
+        keeps free of the GEMM grids) and the captured graphs.  Idempotent;
+        also runs when the Trainer is garbage-collected."""
+        dp, self.dp = getattr(self, "dp", None), None
+        self.graph = self._small_graph = None
+        if getattr(self, "_graphs", None):
+            self._graphs.clear()
+        if getattr(self, "engine", None) is not None:
+            self.engine.grad_ready = None
+        if dp is not None and hasattr(dp, "close"):
+            import torch
+
+            torch.cuda.synchronize()  # in-flight collectives finish before the comm goes
+            dp.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def gradient(self, X, Y):
         """Loss and parameter gradients without the update (the pullback API)."""
@@ -240,6 +297,7 @@ class Trainer:
         e.pullback()
         if self.dp is not None:
             self.dp.finish()
+        self.check()
         return float(e.loss.item()), e.get_grads()
 
 

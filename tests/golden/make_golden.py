@@ -399,6 +399,67 @@ def save_bce():
                                      last_scale=24.0))
 
 
+def domain_cases():
+    """Dense chains whose float64 evaluation hits the reference's domain
+    conditions: the c1 softmax loss IR (exp / reduce_sum / div / log) and the
+    BCE head, run through the UNMODIFIED reference (Machine.call + grad).  The
+    outcome is what it raises -- OverflowError from math.exp (scalar_sigmoid or
+    the loss's exp), EvalError wrapping DomainError from div / log -- or the
+    loss and gradients when nothing is undefined (extreme but finite logits)."""
+    cases = []
+    rng = np.random.default_rng(21)
+    n, d0, d1, d2 = 6, 4, 3, 2
+    X = f32(rng.uniform(0, 1, (n, d0)))
+    W0 = f32(rng.uniform(-0.5, 0.5, (d1, d0)))
+    b0 = f32(rng.uniform(-0.1, 0.1, d1))
+    zeroW1 = np.zeros((d2, d1))
+    plans = [  # (name, loss, hidden act, W0, b0, W1, b1)
+        ("exp_overflow", "softmax_xent", "sigmoid", W0, b0, zeroW1, [800.0, 0.0]),
+        ("div_zero", "softmax_xent", "sigmoid", W0, b0, zeroW1, [-800.0, -900.0]),
+        ("log_zero", "softmax_xent", "sigmoid", W0, b0, zeroW1, [0.0, -800.0]),
+        ("sum_overflow", "softmax_xent", "sigmoid", W0, b0, zeroW1, [709.5, 709.625]),
+        ("sigmoid_overflow", "softmax_xent", "sigmoid", np.full((d1, d0), -800.0), b0, zeroW1, [0.5, -0.5]),
+        ("extreme_finite", "softmax_xent", "sigmoid", W0, b0, zeroW1, [700.0, 0.0]),
+        ("subnormal_p", "softmax_xent", "tanh", W0, b0, zeroW1, [0.0, -740.0]),
+        ("bce_sigmoid_overflow", "bce", "tanh", W0, b0, np.zeros((1, d1)), [-720.0]),
+        ("bce_saturated_ok", "bce", "tanh", W0, b0, np.zeros((1, d1)), [-700.0]),
+    ]
+    for name, loss, act, w0, bb0, w1, bb1 in plans:
+        d_out = 1 if loss == "bce" else d2
+        module = Module()
+        build_chain_loss(module, "chain", (d0, d1, d_out), (act, "identity"), n, loss)
+        if loss == "bce":
+            Y = np.array([0.0, 1.0] * (n // 2))
+        else:
+            Y = np.zeros((n, d_out))
+            Y[np.arange(n), np.arange(n) % d_out] = 1.0
+        params = [(f32(w0), f32(bb0)), (f32(w1), f32(np.array(bb1)))]
+        args = []
+        for W, b in params:
+            args += [DenseTensor(W), DenseTensor(b)]
+        args += [DenseTensor(X), DenseTensor(Y)]
+        out = {"name": name, "loss_kind": loss, "acts": [act, "identity"], "X": X.tolist(),
+               "Y": Y.reshape(n, -1).tolist(),
+               "params": [[W.tolist(), b.tolist()] for W, b in params]}
+        try:
+            lv = Machine(module).call("chain", tuple(args))[0]
+            g = grad(module, "chain", tuple(args))
+            fn = module.get("chain")
+            out["raises"] = None
+            out["loss"] = lv
+            out["grads"] = [[g[fn.params[2 * k][0]].data.tolist(), g[fn.params[2 * k + 1][0]].data.tolist()]
+                            for k in range(2)]
+        except EvalError as e:
+            out["raises"] = "EvalError"
+            out["message"] = e.message
+            out["cause"] = type(e.__cause__).__name__
+        except OverflowError as e:
+            out["raises"] = "OverflowError"
+            out["message"] = str(e)
+        cases.append(out)
+    return cases
+
+
 def main():
     with open(os.path.join(HERE, "fused.json"), "w") as f:
         json.dump(fused_cases(), f, indent=0)
@@ -416,6 +477,8 @@ def main():
                         **chain_case((24, 24, 24, 24), ("tanh", "tanh", "identity"), 16, "mse", 2,
                                      y_kind="uniform"))
     save_bce()
+    with open(os.path.join(HERE, "domain.json"), "w") as f:
+        json.dump(domain_cases(), f, indent=0)
     np.savez_compressed(os.path.join(HERE, "dense_sigmoid.npz"),
                         **chain_case((40, 24), ("sigmoid",), 16, "dot", 3, y_kind="uniform"))
     print("golden fixtures written to", HERE)

@@ -163,3 +163,43 @@ def test_small_step_planner_limits():
     assert plan((2048, 32, 10), 128)[0] != 0                # width beyond 1024
     assert plan((8,) * 6, 64)[0] != 0                       # 5 layers
     assert plan((1024, 1024, 1024), 512)[0] != 0            # working set beyond shared memory
+
+
+def test_bindings_reject_wrong_dtypes_and_shapes_before_any_launch():
+    """The C descriptors carry no dtype: the Python bindings validate dtypes
+    (an fp32 epilogue into a bf16 buffer would write past it) and inner
+    dimensions (no silent truncation), raising ValueError before the library
+    is called -- so these run on CPU tensors."""
+    import torch
+
+    from paper_1811_01457_b200.dense import dense_backward, dense_desc
+    from paper_1811_01457_b200.gemm import bmm, gemm
+
+    bf, f64 = torch.bfloat16, torch.float64
+    A = torch.zeros((64, 32), dtype=bf)
+    B = torch.zeros((48, 32), dtype=bf)
+    with pytest.raises(ValueError, match="out must be"):
+        gemm(A, B, out=torch.zeros((64, 48), dtype=bf))          # fp32 result into bf16
+    with pytest.raises(ValueError, match="A must be"):
+        gemm(A.float(), B, out=torch.zeros((64, 48)))             # fp32 operand for bf16 precision
+    with pytest.raises(ValueError, match="out_lp is a bf16"):
+        gemm(A.float(), B.float(), precision="tf32", out_lp=torch.zeros((64, 48), dtype=bf))
+    with pytest.raises(ValueError, match="inner dimensions differ"):
+        gemm(A, torch.zeros((48, 16), dtype=bf), out=torch.zeros((64, 48)))
+    with pytest.raises(ValueError, match="needs aux"):
+        gemm(A, B, epilogue="act_grad", out=torch.zeros((64, 48)))
+    with pytest.raises(ValueError, match="cannot hold"):
+        bmm(A[None], B[None], out=torch.zeros((1, 32, 48)))
+    with pytest.raises(ValueError, match="out must be"):
+        bmm(A[None].double(), B[None].double(), out=torch.zeros((1, 64, 48)), precision="strict_fp64")
+    with pytest.raises(ValueError, match="b must be"):
+        dense_desc(A, B, torch.zeros(48, dtype=f64), "tanh", "bf16")
+    d = dense_desc(A, B, torch.zeros(48), "tanh", "bf16")
+    dZ = torch.zeros((64, 48), dtype=bf)
+    with pytest.raises(ValueError, match="dW must be"):
+        dense_backward(d, dZ, torch.zeros((48, 32), dtype=bf), torch.zeros(48))
+    with pytest.raises(ValueError, match="dX must be"):
+        dense_backward(d, dZ, torch.zeros((48, 32)), torch.zeros(48), dX=torch.zeros((64, 32), dtype=f64))
+    d64 = dense_desc(A.double(), B.double(), torch.zeros(48, dtype=f64), "tanh", "strict_fp64")
+    with pytest.raises(ValueError, match="dZ must be"):
+        dense_backward(d64, dZ.float(), torch.zeros((48, 32), dtype=f64), torch.zeros(48, dtype=f64))

@@ -381,3 +381,65 @@ def test_small_chain_step_equals_layer_path_and_trains():
         assert abs(a - b) <= 1e-2 * max(1.0, abs(b))
     e = trs.engine
     assert torch.equal(e.S, e.P.to(torch.bfloat16))
+
+
+def _domain_cases():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "domain.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _domain_cases(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("precision", ["bf16", "tf32", "strict_fp32", "strict_fp64"])
+def test_domain_errors_match_reference(case, precision):
+    """Extreme logits / pre-activations (tests/golden/domain.json, produced by
+    the unmodified reference): where the reference raises -- OverflowError
+    from math.exp (sigmoid activation, softmax exp, BCE head), EvalError
+    wrapping DomainError from div (row sum 0) or log (p == 0, also when the
+    row sum overflows) -- Trainer.gradient raises the same exception type and
+    message; where it does not, the stable device loss matches its value and
+    no error is raised (gradients compared where the reference's own are finite;
+    the float64 pullback of log at a subnormal p overflows to inf/NaN there,
+    the stable kernel returns the finite limit)."""
+    from paper_1811_01457_b200.fused import EvalError
+
+    acts = tuple(case["acts"])
+    (W0, b0), (W1, b1) = [(np.array(w, dtype=np.float64), np.array(b, dtype=np.float64)) for w, b in case["params"]]
+    chain = Chain(Dense(W0.shape[1], W0.shape[0], acts[0], W0, b0), Dense(W1.shape[1], W1.shape[0], acts[1], W1, b1))
+    X = np.array(case["X"])
+    Y = np.array(case["Y"])
+    n = X.shape[0]
+    tr = Trainer(chain, n, loss=case["loss_kind"], precision=precision)
+    dt = torch.float64 if precision == "strict_fp64" else torch.float32
+    Xd, Yd = torch.from_numpy(X).to(dt).cuda(), torch.from_numpy(Y).to(dt).cuda()
+    if case["raises"] == "OverflowError":
+        with pytest.raises(OverflowError, match="^math range error$"):
+            tr.gradient(Xd, Yd)
+    elif case["raises"] == "EvalError":
+        with pytest.raises(EvalError) as ei:
+            tr.gradient(Xd, Yd)
+        assert ei.value.message == case["message"]
+        assert type(ei.value.__cause__).__name__ == case["cause"] == "DomainError"
+    else:
+        lv, grads = tr.gradient(Xd, Yd)
+        tol = TOL[precision]
+        assert abs(lv - case["loss"]) <= tol * max(1.0, abs(case["loss"]))
+        for (gW, gb), (rW, rb) in zip(grads, case["grads"]):
+            assert np.isfinite(gW).all() and np.isfinite(gb).all()
+            rW, rb = np.array(rW), np.array(rb)
+            if np.isfinite(rW).all() and np.isfinite(rb).all():
+                assert nrel(gW, rW) <= tol and nrel(gb, rb) <= tol
+    tr.check()  # the flags were consumed by the raise: a clean state for the next step
+    # the one-launch small step (softmax heads, tensor-core precisions) flags the same conditions
+    if tr.engine.small is not None and case["loss_kind"] == "softmax_xent":
+        tr.step(Xd, Yd)
+        if case["raises"] == "OverflowError":
+            with pytest.raises(OverflowError):
+                tr.check()
+        elif case["raises"] == "EvalError":
+            with pytest.raises(EvalError, match=case["message"]):
+                tr.check()
+        else:
+            tr.check()

@@ -66,7 +66,7 @@ def _worker(rank, world, port, q, sliced=False):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1811_01457_b200.dense import slice_first_layer_buckets
+        from paper_1811_01457_b200.dense import pullback_ready_order, slice_first_layer_buckets
         from paper_1811_01457_b200.train import DataParallel, shard_rows
 
         rng = np.random.default_rng(0)  # same data and params on every rank
@@ -87,7 +87,10 @@ def _worker(rank, world, port, q, sliced=False):
             assert all(a[1] == b[0] for a, b in zip(buckets[:3], buckets[1:4]))  # contiguous, no overlap
         G = torch.from_numpy(flat)
         dp = DataParallel(G, buckets)
-        for i in reversed(range(len(buckets))):  # pullback order: top layer first
+        # the engine's own readying order: top layer first, then W0's slices ascending
+        order = pullback_ready_order(len(acts), 4 if sliced else 1)
+        assert sorted(order) == list(range(len(buckets)))
+        for i in order:
             dp.ready(i)
         dp.finish()
         loss = torch.tensor([lv], dtype=torch.float64)
@@ -196,3 +199,30 @@ def test_replica_check_detects_one_ulp_drift():
         assert p.exitcode == 0
     assert all(same for _, same, _ in res)
     assert not any(drift for _, _, drift in res)
+
+
+def test_pullback_ready_order_maps_every_bucket_once():
+    """Host-only: the bucket indices ChainEngine readies (top layer first,
+    layer 0's W0 slices last and ascending) cover the sliced bucket list of
+    slice_first_layer_buckets exactly once, and each bucket index holds the
+    layer the pullback has just finished."""
+    from paper_1811_01457_b200.dense import bucket_of_layer, pullback_ready_order, slice_first_layer_buckets
+
+    for L in (1, 2, 4, 16):
+        assert pullback_ready_order(L, 1) == list(range(L - 1, -1, -1))
+        for S in (2, 4):
+            order = pullback_ready_order(L, S)
+            assert sorted(order) == list(range(L + S - 1))
+            assert order[-S:] == list(range(S))          # W0 slices, ascending, last
+            assert order[:L - 1] == [l + S - 1 for l in range(L - 1, 0, -1)]
+            sizes = [64] + [256] * L
+            _, segs = _layout(sizes)
+            whole = [(wo, (bo + fo + 63) // 64 * 64) for wo, bo, fi, fo in segs]
+            sliced = slice_first_layer_buckets(whole, segs[0][0], sizes[0], sizes[1], S)
+            for l in range(1, L):  # a layer's bucket is its whole segment, shifted by S-1
+                assert sliced[bucket_of_layer(l, S)] == whole[l]
+            rows = sizes[1] // S
+            ldi = (sizes[0] + 7) // 8 * 8
+            for k in range(S):
+                lo, hi = sliced[bucket_of_layer(0, S, k)]
+                assert lo == segs[0][0] + k * rows * ldi

@@ -5,7 +5,9 @@ reproduce the golden vectors produced by the unmodified reference
 import numpy as np
 import pytest
 
-from conftest import decode, load_npz, max_rel
+import os
+
+from conftest import GOLDEN, decode, load_npz, max_rel
 from oracle import dense as OD
 from oracle import scalar as OS
 
@@ -135,3 +137,30 @@ def test_oracle_reproduces_fuzz_corpus_exactly():
         assert np.array_equal(primal, decode(case["primal"])), case["fn"]
         for p, g in zip(parts, case["partials"]):
             assert np.array_equal(p, decode(g)), case["fn"]
+
+
+def test_domain_conditions_match_reference_fixture():
+    """oracle.dense.check_domain raises where the unmodified reference raised on
+    tests/golden/domain.json (OverflowError from math.exp; DomainError -- which
+    run_blocks wraps into EvalError -- from div / log, with the same message),
+    and stays silent on the extreme-but-finite cases."""
+    import json
+
+    from oracle import dense as OD
+
+    with open(os.path.join(GOLDEN, "domain.json")) as f:
+        cases = json.load(f)
+    assert len(cases) >= 8
+    for c in cases:
+        params = [(np.array(w), np.array(b)) for w, b in c["params"]]
+        args = (params, np.array(c["X"]), np.array(c["Y"]), tuple(c["acts"]), c["loss_kind"])
+        if c["raises"] == "OverflowError":
+            with pytest.raises(OverflowError, match="^math range error$"):
+                OD.check_domain(*args)
+        elif c["raises"] == "EvalError":
+            assert c["cause"] == "DomainError"
+            with pytest.raises(OD.DomainError) as ei:
+                OD.check_domain(*args)
+            assert str(ei.value) == c["message"]
+        else:
+            assert OD.check_domain(*args) is None
