@@ -353,6 +353,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     return;
   }
   if (!grp_ok) return;  // the whole 32-row group is past M (warp-uniform)
+  bool ovf = false;      // domain flag of this lane's row (the vote below runs converged)
   if (!row_ok) {
     // rows past M: zeros for the column sums; TMA clips them on store
 #pragma unroll
@@ -377,10 +378,8 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     if (e.act == SG_ACT_SIGMOID) {
       // the reference's scalar_sigmoid computes math.exp(-z): OverflowError for
       // z < -709.78 (tensor.py:214-215); flagged, the value below is still 0
-      bool ovf = false;
 #pragma unroll
       for (int i = 0; i < 32; ++i) ovf |= v[i] <= SIGMOID_OVF_F32;
-      if (__any_sync(0xffffffffu, ovf) && lane == 0 && e.dom) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
     }
     act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
@@ -392,6 +391,9 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
       act_grad_chunk(v, h, e.act);
     }
+  }
+  if (e.mode == SG_EPI_BIAS_ACT && e.act == SG_ACT_SIGMOID && e.dom) {  // warp-uniform
+    if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
   }
   const int row0 = m - lane;
   if (e.out_f32) {
