@@ -527,7 +527,34 @@ def broadcast_variant_bench(args, dist, peaks, variant):
     }
 
 
-TF32_PEAK_TFLOPS = 1100.0  # B200_PROFILING.md dense TF32 figure (no measured TF32 peak in MEASURED_PEAKS.json)
+TF32_PEAK_TFLOPS = 1100.0  # B200_PROFILING.md dense TF32 figure (the fallback when no measurement runs)
+_TF32_PEAK = None
+
+
+def measured_tf32_peak(stream):
+    """Dense TF32 peak measured on this box the way MEASURED_PEAKS.json measures
+    bf16: cuBLAS (torch.matmul, allow_tf32) fp32 8192^3, best of 10 (burst)."""
+    global _TF32_PEAK
+    if _TF32_PEAK is None:
+        import torch
+
+        torch.backends.cuda.matmul.allow_tf32 = True
+        n = 8192
+        a = torch.rand((n, n), device="cuda")
+        b = torch.rand((n, n), device="cuda")
+        for _ in range(3):
+            a @ b
+        best = float("inf")
+        for _ in range(10):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            a @ b
+            s1.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, s0.elapsed_time(s1))
+        _TF32_PEAK = round(2.0 * n ** 3 / (best * 1e-3) / 1e12, 1)
+        del a, b
+    return _TF32_PEAK
 
 
 def dense_c3_bench(args, dist, peaks, precision="bf16"):
@@ -594,7 +621,7 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
         s1.record(stream)
         torch.cuda.synchronize()
         cublas[nm] = round(gf / (s0.elapsed_time(s1) / 10 * 1e-3) / 1e12, 1)
-    peak = TF32_PEAK_TFLOPS if tf32 else peaks["bf16_tflops"]
+    peak = measured_tf32_peak(stream) if tf32 else peaks["bf16_tflops"]
     return {
         "workload": f"c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, {precision} tcgen05",
         "value": round(3 * gf / (ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
@@ -604,7 +631,8 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
         "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel / gemm_tc_pair_kernel (fwd, dX, dW aggregated)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4),
-                     "peak_kind": "spec dense TF32 (B200_PROFILING.md)" if tf32 else "burst",
+                     "peak_kind": "measured cuBLAS TF32 8192^3, best of 10 (burst)" if tf32 else "burst",
+                     "tf32_spec_frac": round(achieved / TF32_PEAK_TFLOPS, 4) if tf32 else None,
                      "traffic": None if tf32 else traffic_of("gemm_bf16_fwd_c3", True),
                      "traffic_algorithmic_bytes": esz * (M * D + D * D + M * D)},
         "gpu_launches_per_step": 5,
@@ -694,6 +722,33 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
     return rec
 
 
+def summary_of(rec):
+    """Compact per-workload digest (value, ms/step, roofline fraction) of the
+    headline and every secondary workload, printed as the line's LAST key so a
+    tail-truncated log still shows every number."""
+    def one(r, name):
+        roof = r.get("roofline") or {}
+        return {"w": name, "v": r.get("value"), "u": r.get("unit"), "ms": r.get("ms_per_step"),
+                "frac": roof.get("frac"), "launches": r.get("gpu_launches_per_step")}
+
+    out = [one(rec, "c2 fp32 (headline)")]
+    if rec.get("e2e"):
+        out[0]["e2e"] = rec["e2e"].get("value")
+    for r in rec.get("secondary", []):
+        name = r.get("workload", "?")
+        if "error" in r:
+            out.append({"w": name[:40], "error": r["error"][:120]})
+            continue
+        key = name.split(" ")[0] + (" " + name.split(",")[-1].strip()[:28] if name.startswith("c2 variant") else "")
+        if name.startswith("c3"):
+            key = "c3 " + ("tf32" if "tf32" in name else "bf16")
+        e = one(r, key)
+        if "gemm_TFLOPs" in r:
+            e["gemm"] = r["gemm_TFLOPs"]
+        out.append(e)
+    return out
+
+
 def secondary_benches(args, world, rank, dist):
     peaks = load_peaks()
     out = []
@@ -760,16 +815,187 @@ def cpu_baseline_mlp(name, sizes, acts, batch, loss, mode, rows=None):
             "s_per_step_sample": round(sec, 4)}
 
 
+def import_reference():
+    """The unmodified reference (pure Python + numpy) installed into
+    baseline/_ref by `pip install --target baseline/_ref` (git-ignored; it
+    travels to the GPU box with the snapshot), or None."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(p, "ssagrad")):
+        return None
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    try:
+        import ssagrad
+
+        return ssagrad
+    except Exception:  # pragma: no cover - broken install: report the port instead
+        return None
+
+
+def reference_broadcast(rows=32):
+    """The reference's own c2 path on a bounded sample: fused_map_with_partials
+    (the per-element dual interpreter that the augmented forward's fused_pack
+    runs, forward_ad.py:194-223 / interp.py:334-352; its row 0 is the primal)
+    + fused_map_pullback (forward_ad.py:226-235), single-threaded."""
+    from ssagrad import DenseTensor, parse_ir
+    from ssagrad.forward_ad import fused_map_pullback, fused_map_with_partials
+    from ssagrad.ir import tensor_type
+
+    m = parse_ir(AFFSIG)
+    rng = np.random.default_rng(0)
+    C = C_COLS
+    x = rng.uniform(-2, 2, (rows, C)).astype(np.float32).astype(np.float64)
+    a = rng.uniform(-2, 2, C).astype(np.float32).astype(np.float64)
+    b = rng.uniform(-2, 2, C).astype(np.float32).astype(np.float64)
+    yb = rng.uniform(-1, 1, (rows, C)).astype(np.float32).astype(np.float64)
+    n = rows * C
+    t0 = time.perf_counter()
+    primal, parts = fused_map_with_partials(m, "affsig", [DenseTensor(a), DenseTensor(x), DenseTensor(b)])
+    t1 = time.perf_counter()
+    fused_map_pullback(parts, [tensor_type(C), tensor_type(rows, C), tensor_type(C)], DenseTensor(yb))
+    t2 = time.perf_counter()
+    sec = t2 - t0
+    return {
+        "value": round(n * BYTES_PER_ELEM / sec / 1e9, 6),
+        "unit": "GB/s",
+        "cores": 1,
+        "kind": "reference",
+        "sample": f"{rows}x{C} = {n} elements through the unmodified reference (baseline/_ref): "
+                  "fused_map_with_partials + fused_map_pullback, 20 B/elem algorithmic",
+        "us_per_elem_pack": round((t1 - t0) / n * 1e6, 3),
+        "us_per_elem_pullback": round((t2 - t1) / n * 1e6, 4),
+        "extrapolated_s_at_2^28": round(sec / n * (1 << 28), 1),
+        "host_cores_available": len(os.sched_getaffinity(0)),
+    }
+
+
+def _reference_chain_module(sizes, acts, n, loss):
+    """A Dense chain's loss IR built with the reference's own emitter, exactly
+    as nn_train's trunk builds layers (nn_train.py:189-196):
+    wt = transpose(W); z = matmul(h, wt); zb = add(z, b); h = act(zb), then the
+    c1 softmax-CE IR, MSE, or 'dot' (sum(h * Y): pulls the seed
+    Y back through a single layer, the c3 fwd + pullback)."""
+    from ssagrad import Module
+    from ssagrad.ir import F64, tensor_type
+    from ssagrad.structure import SEmitter, flatten
+
+    module = Module()
+    em = SEmitter("chain", (F64,), module)
+    pairs = [(em.param(f"W{k}", tensor_type(sizes[k + 1], sizes[k])), em.param(f"b{k}", tensor_type(sizes[k + 1])))
+             for k in range(len(sizes) - 1)]
+    x = em.param("X", tensor_type(n, sizes[0]))
+    y = em.param("Y", tensor_type(n, sizes[-1]))
+    h = x
+    for (w, b), act in zip(pairs, acts):
+        wt = em.emit("transpose", (w,), None, "wt")
+        z = em.emit("matmul", (h, wt), None, "z")
+        zb = em.emit("add", (z, b), None, "zb")
+        h = zb if act == "identity" else em.emit(act, (zb,), None, "h")
+    if loss == "softmax_xent":
+        e = em.emit("exp", (h,), None, "e")
+        ssum = em.emit("reduce_sum", (e,), {"axis": 1}, "s")
+        s2 = em.emit("reshape", (ssum,), {"shape": (n, 1)}, "s2")
+        p = em.emit("div", (e, s2), None, "p")
+        lp = em.emit("log", (p,), None, "lp")
+        t = em.emit("mul", (y, lp), None, "t")
+        tot = em.emit("reduce_sum", (t,), {"axis": "all"}, "tot")
+        sc = em.const_f64(-1.0 / n, "sc")
+    elif loss == "mse":
+        d = em.emit("sub", (h, y), None, "d")
+        sq = em.emit("mul", (d, d), None, "sq")
+        tot = em.emit("reduce_sum", (sq,), {"axis": "all"}, "tot")
+        sc = em.const_f64(1.0 / n, "sc")
+    else:
+        t = em.emit("mul", (h, y), None, "t")
+        tot = em.emit("reduce_sum", (t,), {"axis": "all"}, "tot")
+        sc = em.const_f64(1.0, "sc")
+    loss_v = em.emit("mul", (tot, sc), None, "loss")
+    module.add(flatten(em.finish((loss_v,))))
+    return module
+
+
+def reference_mlp(name, sizes, acts, batch, loss, rows=None, lr=0.05, unit="samples/s"):
+    """The reference's own training step: grad (augment + Machine.call of the
+    aug and pb functions, reverse_ad.py:619-663) of the chain's loss IR, then
+    SGD p - lr * g (nn_train.py:365-372), on the full batch or on a row slice
+    (every matmul is linear in the rows, so samples/s extrapolate)."""
+    from ssagrad import DenseTensor, grad
+
+    n = rows or batch
+    rng = np.random.default_rng(0)
+    params = []
+    for i in range(len(acts)):
+        r = np.sqrt(6.0 / (sizes[i] + sizes[i + 1]))
+        params.append((rng.uniform(-r, r, (sizes[i + 1], sizes[i])), np.zeros(sizes[i + 1])))
+    X = rng.uniform(0, 1, (n, sizes[0]))
+    if loss == "softmax_xent":
+        Y = np.zeros((n, sizes[-1]))
+        Y[np.arange(n), rng.integers(0, sizes[-1], n)] = 1.0
+    else:
+        Y = rng.uniform(-1, 1, (n, sizes[-1]))
+    module = _reference_chain_module(sizes, acts, n, loss)
+    args = []
+    for W, b in params:
+        args += [DenseTensor(W), DenseTensor(b)]
+    args += [DenseTensor(X), DenseTensor(Y)]
+    fn = module.get("chain")
+    grad(module, "chain", tuple(args))  # builds (and caches) the aug / pb IR once
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        g = grad(module, "chain", tuple(args))
+        [W - lr * g[fn.params[2 * k][0]].data for k, (W, _) in enumerate(params)]
+        [b - lr * g[fn.params[2 * k + 1][0]].data for k, (_, b) in enumerate(params)]
+        reps += 1
+        if time.perf_counter() - t0 > 1.0 or rows:
+            break
+    sec = (time.perf_counter() - t0) / reps
+    rec = {"workload": name, "value": round(n / sec, 4), "unit": "samples/s", "kind": "reference", "cores": 1,
+           "sample": f"{n} rows of the {batch}-row batch (extrapolated: cost is linear in rows)" if rows
+           else f"full batch {batch}",
+           "s_per_step_sample": round(sec, 4)}
+    if unit == "TFLOP/s":  # c3: one layer's fwd + dX + dW
+        rec["value"] = round(6.0 * n * sizes[0] * sizes[1] / sec / 1e12, 9)
+        rec["unit"] = "TFLOP/s"
+    return rec
+
+
 def reference_arm(args, world, rank):
+    """`bench.py --impl reference`: the reference's own CPU implementation of
+    the path on this box's host cores -- the unmodified reference from
+    baseline/_ref when installed (kind "reference"), else the oracle's port
+    of its algorithm (kind "port") -- on the same workloads and metrics."""
     if rank != 0:
         return None
     t0 = time.perf_counter()
+    ref = import_reference()
     vals = []
     for _ in range(max(1, min(args.steps, 3))):
-        vals.append(cpu_baseline_broadcast(rows=args.ref_rows))
+        vals.append(reference_broadcast(rows=args.ref_rows) if ref else cpu_baseline_broadcast(rows=args.ref_rows))
     v = statistics.median(r["value"] for r in vals)
     cb = dict(vals[-1])
     cb["value"] = v
+    secondary = []
+    if ref:
+        secondary += [
+            reference_mlp("c1 MLP 784-32-10 train step (reference grad + SGD)", (784, 32, 10), ("sigmoid", "identity"),
+                          128, "softmax_xent"),
+            reference_mlp("c3 Dense 4096->4096 sigmoid fwd+pullback (reference, row slice)", (4096, 4096),
+                          ("sigmoid",), 8192, "dot", rows=1, unit="TFLOP/s"),
+            reference_mlp("c4 MLP 4x4096 train step (reference, row slice)", (4096,) * 5,
+                          ("tanh",) * 3 + ("identity",), 65536, "mse", rows=1, lr=1e-4),
+            reference_mlp("c5 MLP 16x1024 train step (reference, row slice)", (1024,) * 17,
+                          ("tanh",) * 15 + ("identity",), 32768, "mse", rows=4, lr=1e-4),
+        ]
+    secondary += [
+        cpu_baseline_mlp("c1 MLP 784-32-10 train step (port: reference matmul order, C)", (784, 32, 10),
+                         ("sigmoid", "identity"), 128, "softmax_xent", "exact"),
+        cpu_baseline_mlp("c4 MLP 4x4096 train step (port: numpy-BLAS fp64, row slice)", (4096,) * 5,
+                         ("tanh",) * 3 + ("identity",), 65536, "mse", "blas", rows=256),
+    ]
+    if ref:
+        port = cpu_baseline_broadcast(rows=args.ref_rows)
+        secondary.append({"workload": "c2 (port: the oracle's per-element interpreter)", **port})
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -786,13 +1012,10 @@ def reference_arm(args, world, rank):
         "config": c2_config(args.rows, C_COLS, world),
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "secondary": [
-            cpu_baseline_mlp("c1 MLP 784-32-10 train step (reference matmul order)", (784, 32, 10),
-                             ("sigmoid", "identity"), 128, "softmax_xent", "exact"),
-            cpu_baseline_mlp("c4 MLP 4x4096 train step (numpy-BLAS fp64, row slice)", (4096,) * 5,
-                             ("tanh",) * 3 + ("identity",), 65536, "mse", "blas", rows=256),
-        ],
+        "secondary": secondary,
         "wall_s": round(time.perf_counter() - t0, 1),
+        "summary": [{"w": r["workload"][:48], "v": r.get("value"), "u": r.get("unit"), "kind": r.get("kind")}
+                    for r in secondary],
     }
 
 
@@ -824,9 +1047,13 @@ def main():
         rec["secondary"] = secondary_benches(args, world, rank, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            rec["cpu_baseline"] = cpu_baseline_broadcast(rows=args.ref_rows)
+            ref = import_reference()
+            rec["cpu_baseline"] = reference_broadcast(rows=args.ref_rows) if ref else \
+                cpu_baseline_broadcast(rows=args.ref_rows)
             rec["cpu_baseline"]["secondary"] = [
+                reference_mlp("c1", (784, 32, 10), ("sigmoid", "identity"), 128, "softmax_xent") if ref else
                 cpu_baseline_mlp("c1", (784, 32, 10), ("sigmoid", "identity"), 128, "softmax_xent", "exact")]
+        rec["summary"] = summary_of(rec)  # last key: survives a tail-truncated log
         print(json.dumps(rec), flush=True)
     if dist is not None:
         dist.barrier()

@@ -447,6 +447,22 @@ def domain_cases():
             fn = module.get("chain")
             out["raises"] = None
             out["loss"] = lv
+            # where the reference's float64 pullback itself overflows (s*s in the
+            # div adjoint, 1/p of a subnormal p) its gradients are not the
+            # derivative; and log of a subnormal p carries fewer than 53 bits
+            try:
+                with np.errstate(over="raise", invalid="raise", divide="raise"):
+                    grad(module, "chain", tuple(args))
+                out["pullback_overflow"] = False
+            except FloatingPointError:
+                out["pullback_overflow"] = True
+            h = X @ params[0][0].T + params[0][1]
+            h = np.tanh(h) if act == "tanh" else 1.0 / (1.0 + np.exp(-h))
+            z = h @ params[1][0].T + params[1][1]
+            with np.errstate(over="ignore"):
+                e = np.exp(z)
+            p = e / e.sum(axis=1, keepdims=True)
+            out["p_subnormal"] = bool(loss == "softmax_xent" and ((p > 0) & (p < np.finfo(np.float64).tiny)).any())
             out["grads"] = [[g[fn.params[2 * k][0]].data.tolist(), g[fn.params[2 * k + 1][0]].data.tolist()]
                             for k in range(2)]
         except EvalError as e:

@@ -401,8 +401,9 @@ def test_domain_errors_match_reference(case, precision):
     row sum overflows) -- Trainer.gradient raises the same exception type and
     message; where it does not, the stable device loss matches its value and
     no error is raised (gradients compared where the reference's own are finite;
-    the float64 pullback of log at a subnormal p overflows to inf/NaN there,
-    the stable kernel returns the finite limit)."""
+    where the reference's float64 pullback itself overflows -- s*s in div's
+    adjoint, 1/p of a subnormal p -- the stable gradients are checked against
+    the exact softmax-CE gradient instead)."""
     from paper_1811_01457_b200.fused import EvalError
 
     acts = tuple(case["acts"])
@@ -425,12 +426,21 @@ def test_domain_errors_match_reference(case, precision):
     else:
         lv, grads = tr.gradient(Xd, Yd)
         tol = TOL[precision]
-        assert abs(lv - case["loss"]) <= tol * max(1.0, abs(case["loss"]))
+        # log of a subnormal p keeps fewer than 53 bits in the reference (its
+        # loss is off by up to ~1e-5 relative); the stable z - lse is exact
+        ltol = max(tol, 1e-5) if case["p_subnormal"] else tol
+        assert abs(lv - case["loss"]) <= ltol * max(1.0, abs(case["loss"]))
         for (gW, gb), (rW, rb) in zip(grads, case["grads"]):
             assert np.isfinite(gW).all() and np.isfinite(gb).all()
-            rW, rb = np.array(rW), np.array(rb)
-            if np.isfinite(rW).all() and np.isfinite(rb).all():
-                assert nrel(gW, rW) <= tol and nrel(gb, rb) <= tol
+            if not case["pullback_overflow"]:
+                assert nrel(gW, np.array(rW)) <= tol and nrel(gb, np.array(rb)) <= tol
+        if case["pullback_overflow"]:
+            # the reference's float64 pullback overflowed (s*s in div's adjoint,
+            # 1/p of a subnormal p), so its gradients are not the derivative:
+            # check the stable ones against the exact softmax-CE gradient instead
+            _, go, _ = OD.mlp_step([(W0, b0), (W1, b1)], X, Y, acts, case["loss_kind"], mode="blas")
+            for (gW, gb), (oW, ob) in zip(grads, go):
+                assert nrel(gW, oW) <= tol and nrel(gb, ob) <= tol
     tr.check()  # the flags were consumed by the raise: a clean state for the next step
     # the one-launch small step (softmax heads, tensor-core precisions) flags the same conditions
     if tr.engine.small is not None and case["loss_kind"] == "softmax_xent":
