@@ -221,6 +221,29 @@ __device__ __forceinline__ void act_grad_chunk(float (&v)[32], const float (&h)[
   }
 }
 
+// Tile timeline trace (tools only: built with -DSGB200_GEMM_TRACE into a
+// separate library, tools/gemm_trace.py): per CTA and tile iteration, the
+// %globaltimer of MMA start, accumulator complete (epilogue wake-up) and
+// epilogue end.  Compiled out of the product library.
+#ifdef SGB200_GEMM_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_iters = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SG_TRACE(it, slot)                                                                      \
+  do {                                                                                          \
+    if (g_trace && (it) < g_trace_iters)                                                        \
+      g_trace[((long long)blockIdx.x * g_trace_iters + (it)) * 4 + (slot)] = gtimer();          \
+  } while (0)
+#else
+#define SG_TRACE(it, slot) \
+  do {                     \
+  } while (0)
+#endif
+
 struct TileCoord {
   int m0, n0;
 };
@@ -830,7 +853,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < tiles; t += pairs) {
+      int it = 0;
+      for (int t = pair; t < tiles; t += pairs, ++it) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -839,6 +863,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (kb == kb0) SG_TRACE(it, 0);  // first k-block of the tile ready: MMA starts
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -870,7 +895,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0, aux_phase = 0;
-    for (int t = pair; t < tiles; t += pairs) {
+    int it = 0;
+    for (int t = pair; t < tiles; t += pairs, ++it) {
       const TileCoord tc = coord(t);
       const int bidx = (t % out_tiles) / tiles_pb;
       const int row0 = tc.m0 + (int)rank * HALF + q * 32;
@@ -880,6 +906,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       if (staged && lane == 0 && tc.n0 + c0 * 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], tc.n0 + c0 * 32, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane == 0) SG_TRACE(it, 1);  // accumulator complete
       const int m = row0 + lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
@@ -903,6 +930,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
+      if (lane == 0 && ew == 0) SG_TRACE(it, 2);  // epilogue warp 0 done with the tile
+      if (lane == 0 && ew == EPI_WARPS - 1) SG_TRACE(it, 3);  // last epilogue warp done
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -1257,6 +1286,15 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
 }
 
 }  // namespace
+
+#ifdef SGB200_GEMM_TRACE
+extern "C" SG_API int sg_gemm_trace_buffer(void* buf, int iters) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace, &p, sizeof p));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_iters, &iters, sizeof iters));
+  return SG_OK;
+}
+#endif
 
 int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return fail(SG_EINVAL, "gemm: empty problem");

@@ -14,6 +14,9 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libsgb200.so")
+# tools only (tools/gemm_trace.py): an instrumented build of the same library
+if os.environ.get("SGB200_LIB"):
+    LIB_PATH = os.path.join(_HERE, "_lib", os.path.basename(os.environ["SGB200_LIB"]))
 
 SG_OK, SG_EDOMAIN, SG_EINVAL, SG_ECUDA, SG_ENCCL = 0, 1, 2, 3, 4
 SG_F32, SG_F64, SG_BF16 = 0, 1, 2
