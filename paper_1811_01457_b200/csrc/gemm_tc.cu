@@ -225,22 +225,44 @@ __device__ __forceinline__ void act_grad_chunk(float (&v)[32], const float (&h)[
 // separate library, tools/gemm_trace.py): per CTA and tile iteration, the
 // %globaltimer of MMA start, accumulator complete (epilogue wake-up) and
 // epilogue end.  Compiled out of the product library.
+// Launches are numbered on the device (g_trace_seq: read after the grid
+// dependency wait, advanced by the last CTA to finish), so back-to-back and
+// graph-replayed launches each get their own region:
+//   g_trace[((seq * 148 + cta) * iters + it) * 4 + slot], slot 0..3 as above.
 #ifdef SGB200_GEMM_TRACE
 __device__ unsigned long long* g_trace = nullptr;
-__device__ int g_trace_iters = 0;
+__device__ int g_trace_iters = 0, g_trace_launches = 0;
+__device__ unsigned g_trace_seq = 0, g_trace_done = 0;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define SG_TRACE(it, slot)                                                                      \
-  do {                                                                                          \
-    if (g_trace && (it) < g_trace_iters)                                                        \
-      g_trace[((long long)blockIdx.x * g_trace_iters + (it)) * 4 + (slot)] = gtimer();          \
+#define SG_TRACE(it, slot)                                                                                 \
+  do {                                                                                                     \
+    if (g_trace && (it) < g_trace_iters && trace_seq < (unsigned)g_trace_launches)                          \
+      g_trace[(((long long)trace_seq * 148 + blockIdx.x) * g_trace_iters + (it)) * 4 + (slot)] = gtimer(); \
+  } while (0)
+#define SG_TRACE_BEGIN() const unsigned trace_seq = *(volatile unsigned*)&g_trace_seq
+#define SG_TRACE_END()                                                      \
+  do {                                                                      \
+    if (threadIdx.x == 0) {                                                 \
+      __threadfence();                                                      \
+      if (atomicAdd(&g_trace_done, 1u) == gridDim.x - 1) {                  \
+        g_trace_done = 0;                                                   \
+        atomicAdd(&g_trace_seq, 1u);                                        \
+      }                                                                     \
+    }                                                                       \
   } while (0)
 #else
 #define SG_TRACE(it, slot) \
   do {                     \
+  } while (0)
+#define SG_TRACE_BEGIN() \
+  do {                   \
+  } while (0)
+#define SG_TRACE_END() \
+  do {                 \
   } while (0)
 #endif
 
@@ -806,6 +828,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   const uint32_t tmem_base = *tmem_slot;
   grid_dep_wait();  // see gemm_tc_kernel
   grid_dep_launch();
+  SG_TRACE_BEGIN();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -947,6 +970,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                  : "memory");
   }
+  SG_TRACE_END();
 }
 
 }  // namespace tc
@@ -1288,10 +1312,14 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
 }  // namespace
 
 #ifdef SGB200_GEMM_TRACE
-extern "C" SG_API int sg_gemm_trace_buffer(void* buf, int iters) {
+extern "C" SG_API int sg_gemm_trace_buffer(void* buf, int iters, int launches) {
   unsigned long long* p = static_cast<unsigned long long*>(buf);
+  const unsigned zero = 0;
   SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace, &p, sizeof p));
   SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_iters, &iters, sizeof iters));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_launches, &launches, sizeof launches));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_seq, &zero, sizeof zero));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_done, &zero, sizeof zero));
   return SG_OK;
 }
 #endif
