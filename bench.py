@@ -515,6 +515,7 @@ def broadcast_variant_bench(args, dist, peaks, variant):
     bpe = BYTES_PER_ELEM * esz // 4  # 20 B/elem in fp32, 40 in f64
     return {
         "workload": f"c2 variant: sigma.(a.*x.+b) + gradient, 2^28 {'f64' if esz == 8 else 'fp32'}, {desc}",
+        "key": {"scalar": "c2 scalar a,b", "col": "c2 (R,1) a,b", "f64": "c2 f64"}[variant],
         "value": round(n * bpe / (ms * 1e-3) / 1e9, 1), "unit": "GB/s", "ms_per_step": round(ms, 4),
         "bytes_per_elem": bpe,
         "kernels_ms": {"fwd_K1": round(fwd, 4), "grad_K2_plus_finalize": round(grad, 4),
@@ -624,6 +625,7 @@ def dense_c3_bench(args, dist, peaks, precision="bf16"):
     peak = measured_tf32_peak(stream) if tf32 else peaks["bf16_tflops"]
     return {
         "workload": f"c3 Dense 4096->4096 sigmoid fwd+pullback (dX, dW, db), batch 8192, {precision} tcgen05",
+        "key": f"c3 {precision}",
         "value": round(3 * gf / (ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
         "flops_per_step": 3 * gf,
         "kernels_ms": {k: round(v, 4) for k, v in kms.items()},
@@ -739,10 +741,7 @@ def summary_of(rec):
         if "error" in r:
             out.append({"w": name[:40], "error": r["error"][:120]})
             continue
-        key = name.split(" ")[0] + (" " + name.split(",")[-1].strip()[:28] if name.startswith("c2 variant") else "")
-        if name.startswith("c3"):
-            key = "c3 " + ("tf32" if "tf32" in name else "bf16")
-        e = one(r, key)
+        e = one(r, r.get("key", name.split(" ")[0]))
         if "gemm_TFLOPs" in r:
             e["gemm"] = r["gemm_TFLOPs"]
         out.append(e)
@@ -764,7 +763,7 @@ def secondary_benches(args, world, rank, dist):
                 out.append(dense_c3_bench(args, dist, peaks, precision="tf32"))
             elif w == "c4":
                 out.append(mlp_bench(args, world, rank, dist, peaks, "c4", (4096,) * 5,
-                                     ("tanh",) * 3 + ("identity",), 65536, "mse", graph=False))
+                                     ("tanh",) * 3 + ("identity",), 65536, "mse", graph=True))
             elif w == "c5":
                 out.append(mlp_bench(args, world, rank, dist, peaks, "c5", (1024,) * 17,
                                      ("tanh",) * 15 + ("identity",), 32768, "mse", graph=True))
