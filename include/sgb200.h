@@ -187,6 +187,9 @@ SG_API int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_
 /* out[n] = sum_g part[g][n] (fixed order, fp64 accumulation): bias-gradient stage 2. */
 SG_API int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_part, int64_t N, float* out,
                               void* stream);
+/* The same for n bias gradients in one launch (parts[i] [G[i]][ld_part[i]] -> outs[i][N[i]]). */
+SG_API int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int64_t* G,
+                                    const int64_t* ld_part, const int64_t* N, float* const* outs, void* stream);
 /* reduce_to((M,N) -> (N,)) in the reference's exact order (sequential ascending
  * row fold, tensor.py:287-292, 337-338), f32/f64: STRICT precision bias gradients. */
 SG_API int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t ld, int64_t M, int64_t N,
@@ -220,6 +223,37 @@ SG_API int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, i
  * activation rows the first GEMM reads through TMA). */
 SG_API int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, void* dst, int32_t dst_dtype,
                       int64_t ld_dst, int64_t rows, int64_t cols, void* stream);
+
+/* ------------------------------------------------ persistent GEMM chains
+ * A sequence of BF16 GEMMs (each an sg_gemm_desc: the Dense forward, dX and
+ * dW products of nn_train.py:189-196 / rules.py:113-115 with their fused
+ * epilogues) run by ONE persistent launch of CTA pairs.  A problem may depend
+ * on earlier ones; its 256 x 256 output tiles then wait only for the rows
+ * they read:
+ *   SG_DEP_ROWS   A is K-major and is the earlier problem's output: a tile
+ *                 waits for the producer's tiles of its 256-row block;
+ *   SG_DEP_KROWS  A is MN-major over the earlier problem's output rows (dW =
+ *                 dZ^T X): a K-split waits for the row blocks in its K range;
+ *   SG_DEP_ALL    every tile of the earlier problem.
+ * splits > 1 runs a STORE / fp32-output problem as K-splits finished inside
+ * the kernel in ascending split order.  Results are bit-identical to issuing
+ * the same sg_gemm calls one by one.  Buffers are bound at creation: a chain
+ * is a plan (tensor maps, schedule, counters) replayed by sg_chain_run. */
+#define SG_DEP_ROWS 1
+#define SG_DEP_KROWS 2
+#define SG_DEP_ALL 3
+typedef struct sg_chain_problem {
+  sg_gemm_desc gemm;
+  int32_t splits;
+  int32_t n_deps;       /* 0..2 */
+  int32_t dep_kind[2];  /* SG_DEP_* */
+  int32_t dep_on[2];    /* index of an earlier problem */
+} sg_chain_problem;
+typedef struct sg_chain sg_chain;
+SG_API int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* problems, int32_t n, sg_chain** out);
+SG_API int sg_chain_run(sg_chain* chain, void* stream);
+SG_API int sg_chain_info(const sg_chain* chain, int32_t* units, int32_t* ctas, double* est_us);
+SG_API int sg_chain_destroy(sg_chain* chain);
 
 /* ------------------------------------------------ Dense-path domain errors
  * The reference raises where its float64 ops are undefined: math.exp

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <string>
 
 #include "common.h"
 #include "gemm.h"
@@ -222,6 +223,37 @@ __global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, lon
     __syncthreads();
   }
   if (ty == 0 && j < N) out[j] = (float)red[0][tx];
+}
+
+// The same finalize for several bias gradients in one launch (blockIdx.y =
+// job): the chained backward pass finalises every layer's db at once.
+constexpr int MAX_COLSUM_JOBS = 32;
+struct ColsumJobs {
+  const float* part[MAX_COLSUM_JOBS];
+  float* out[MAX_COLSUM_JOBS];
+  long long G[MAX_COLSUM_JOBS], ldp[MAX_COLSUM_JOBS], N[MAX_COLSUM_JOBS];
+};
+__global__ void __launch_bounds__(1024) k_colsum_finalize_multi(const __grid_constant__ ColsumJobs jobs) {
+  constexpr int RG = 128;
+  __shared__ double red[RG][9];
+  const int b = blockIdx.y;
+  const long long N = jobs.N[b], G = jobs.G[b], ldp = jobs.ldp[b];
+  if (blockIdx.x * 8ll >= N) return;  // block-uniform
+  const float* part = jobs.part[b];
+  const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
+  const long long j = blockIdx.x * 8ll + tx;
+  double acc = 0.0;
+  if (j < N) {
+#pragma unroll 4
+    for (long long g = ty; g < G; g += RG) acc += (double)part[g * ldp + j];
+  }
+  red[ty][tx] = acc;
+  __syncthreads();
+  for (int s = RG / 2; s > 0; s >>= 1) {
+    if (ty < s) red[ty][tx] += red[ty + s][tx];
+    __syncthreads();
+  }
+  if (ty == 0 && j < N) jobs.out[b][j] = (float)red[0][tx];
 }
 
 // --- reduce_to over rows in the reference's order: sequential ascending fold
@@ -689,6 +721,32 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
   dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 1024, 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
                                                                                              out);
   SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int64_t* G,
+                             const int64_t* ld_part, const int64_t* N, float* const* outs, void* stream) {
+  if (!ctx || n < 0 || (n && (!parts || !G || !ld_part || !N || !outs))) return fail(SG_EINVAL, "null argument");
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  for (int b0 = 0; b0 < n; b0 += dk::MAX_COLSUM_JOBS) {
+    dk::ColsumJobs jobs{};
+    const int nb = std::min(n - b0, dk::MAX_COLSUM_JOBS);
+    long long nmax = 1;
+    for (int i = 0; i < nb; ++i) {
+      if (!parts[b0 + i] || !outs[b0 + i] || G[b0 + i] < 0 || N[b0 + i] < 0 || ld_part[b0 + i] < N[b0 + i])
+        return fail(SG_EINVAL, "colsum_finalize_multi: bad job " + std::to_string(b0 + i));
+      jobs.part[i] = parts[b0 + i];
+      jobs.out[i] = outs[b0 + i];
+      jobs.G[i] = G[b0 + i];
+      jobs.ldp[i] = ld_part[b0 + i];
+      jobs.N[i] = N[b0 + i];
+      nmax = std::max(nmax, (long long)N[b0 + i]);
+    }
+    dk::k_colsum_finalize_multi<<<dim3((unsigned)((nmax + 7) / 8), (unsigned)nb), 1024, 0, (cudaStream_t)stream>>>(
+        jobs);
+    SG_CUDA_TRY(cudaGetLastError());
+  }
   return SG_OK;
 }
 

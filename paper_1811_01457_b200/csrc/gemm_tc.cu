@@ -22,447 +22,10 @@
 //                             MMA warp already works on the next tile
 // Synchronisation is mbarrier-only: full/empty per smem stage (TMA tx-count and
 // tcgen05.commit), full/empty per accumulator buffer.
-#include <cuda.h>
-#include <cuda_bf16.h>
-#include <cuda_runtime.h>
-
-#include <cstdint>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-
-#include "common.h"
-#include "gemm.h"
+#include "gemm_tc_dev.cuh"
 
 namespace sg {
 namespace tc {
-
-constexpr int BM = 128;           // UMMA M (cta_group::1)
-// A k-block is one 128-byte swizzle row of K: 64 bf16 or 32 fp32 (TF32)
-// elements; one UMMA_K step is 32 bytes of K (16 bf16 / 8 TF32).  Stage
-// bytes per k-block are therefore the same for both operand types.
-template <bool TF32> struct Elem {
-  static constexpr int BK = TF32 ? 32 : 64;
-  static constexpr int UMMA_K = TF32 ? 8 : 16;
-  static constexpr int KSTEPS = BK / UMMA_K;          // 4
-  static constexpr uint32_t MN_CHUNK = BK * 128;      // MN-major: EPR x BK box bytes (= LBO)
-  static constexpr uint32_t MN_KSTEP = UMMA_K * 128;  // MN-major: next UMMA_K K-rows
-  // MN-major 32-bit operands only exist in the 128B swizzle with 32-byte
-  // atoms (layout type 1, TMA SWIZZLE_128B_ATOM_32B): 4-row swizzle groups,
-  // so the K-direction group stride (SBO) is 512 B instead of 1024 B.
-  static constexpr uint32_t MN_SBO = TF32 ? 512 : 1024;
-  static constexpr uint32_t MN_LAYOUT = TF32 ? 1 : 2;
-};
-constexpr int ROW_BYTES = 128;
-constexpr int NUM_THREADS = 384;  // 12 warps: TMA, MMA, TMEM, idle, 8 epilogue
-constexpr int EPI_WARP0 = 4;
-constexpr int EPI_WARPS = 8;      // two per TMEM lane quadrant, each takes half the columns
-
-// ------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Accumulator hand-back: only the TMEM reads must be ordered before it
-// (tcgen05.fence::before_thread_sync), not the epilogue's global stores.
-__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-}
-// Operand maps are 3-D {row, rows, batch}: c2 is the batch index (0 for a plain GEMM).
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-// PDL (griddepcontrol): wait = the prerequisite grid has completed and its
-// memory is visible (a no-op without a programmatic dependency);
-// launch_dependents = the next kernel in the stream may start its prologue.
-__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-template <bool TF32>
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  if (TF32)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  else
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// 32 lanes x 32 consecutive fp32 columns: thread t of warp q gets lane 32q+t
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// UMMA shared-memory descriptor, 128B swizzle (layout type 2), sm_100 version bit.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)layout << 61;
-  return d;
-}
-// Instruction descriptor: fp32 accumulate (bit 4), A/B format at bits 7/10
-// (kind::f16: 1 = bf16; kind::tf32: 2 = tf32), operand majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t idesc_tc(int M, int N, bool a_mn, bool b_mn, bool tf32) {
-  return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) |
-         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// ------------------------------------------------------------- epilogue
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// Epilogue math runs per output element on 8 warps while the tensor cores
-// work on the next tile, so it uses the SFU approximations (rel. error
-// ~2^-11, below the bf16 rounding of the stored activations).
-__device__ __forceinline__ float act_fwd(float z, int act) {
-  switch (act) {
-    case SG_ACT_SIGMOID: return __fdividef(1.0f, 1.0f + __expf(-z));  // tensor.py:214-215
-    case SG_ACT_TANH: return tanh_fast(z);
-    case SG_ACT_RELU: return z > 0.0f ? z : 0.0f;
-    default: return z;
-  }
-}
-// d act / d z expressed through the saved output h (rules.py:82-94)
-__device__ __forceinline__ float act_grad_from_out(float h, int act) {
-  switch (act) {
-    case SG_ACT_SIGMOID: return h * (1.0f - h);
-    case SG_ACT_TANH: return 1.0f - h * h;
-    case SG_ACT_RELU: return h > 0.0f ? 1.0f : 0.0f;
-    default: return 1.0f;
-  }
-}
-
-// The activation is uniform per launch: branch once per 32-element chunk,
-// not per element (a per-element switch compiles to an indirect branch).
-__device__ __forceinline__ void act_fwd_chunk(float (&v)[32], int act) {
-  if (act == SG_ACT_SIGMOID) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __fdividef(1.0f, 1.0f + __expf(-v[i]));
-  } else if (act == SG_ACT_TANH) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
-  } else if (act == SG_ACT_RELU) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
-  }
-}
-__device__ __forceinline__ void act_grad_chunk(float (&v)[32], const float (&h)[32], int act) {
-  if (act == SG_ACT_SIGMOID) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= h[i] * (1.0f - h[i]);
-  } else if (act == SG_ACT_TANH) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= 1.0f - h[i] * h[i];
-  } else if (act == SG_ACT_RELU) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = h[i] > 0.0f ? v[i] : 0.0f * v[i];
-  }
-}
-
-// Tile timeline trace (tools only: built with -DSGB200_GEMM_TRACE into a
-// separate library, tools/gemm_trace.py): per CTA and tile iteration, the
-// %globaltimer of MMA start, accumulator complete (epilogue wake-up) and
-// epilogue end.  Compiled out of the product library.
-// Launches are numbered on the device (g_trace_seq: read after the grid
-// dependency wait, advanced by the last CTA to finish), so back-to-back and
-// graph-replayed launches each get their own region:
-//   g_trace[((seq * 148 + cta) * iters + it) * 4 + slot], slot 0..3 as above.
-#ifdef SGB200_GEMM_TRACE
-__device__ unsigned long long* g_trace = nullptr;
-__device__ int g_trace_iters = 0, g_trace_launches = 0;
-__device__ unsigned g_trace_seq = 0, g_trace_done = 0;
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define SG_TRACE(it, slot)                                                                                 \
-  do {                                                                                                     \
-    if (g_trace && (it) < g_trace_iters && trace_seq < (unsigned)g_trace_launches)                          \
-      g_trace[(((long long)trace_seq * 148 + blockIdx.x) * g_trace_iters + (it)) * 4 + (slot)] = gtimer(); \
-  } while (0)
-#define SG_TRACE_BEGIN() const unsigned trace_seq = *(volatile unsigned*)&g_trace_seq
-#define SG_TRACE_END()                                                      \
-  do {                                                                      \
-    if (threadIdx.x == 0) {                                                 \
-      __threadfence();                                                      \
-      if (atomicAdd(&g_trace_done, 1u) == gridDim.x - 1) {                  \
-        g_trace_done = 0;                                                   \
-        atomicAdd(&g_trace_seq, 1u);                                        \
-      }                                                                     \
-    }                                                                       \
-  } while (0)
-#else
-#define SG_TRACE(it, slot) \
-  do {                     \
-  } while (0)
-#define SG_TRACE_BEGIN() \
-  do {                   \
-  } while (0)
-#define SG_TRACE_END() \
-  do {                 \
-  } while (0)
-#endif
-
-struct TileCoord {
-  int m0, n0;
-};
-__device__ __forceinline__ TileCoord tile_of(int t, int m_tiles, int n_tiles, int bn) {
-  // grouped raster: 8 M-tiles per group so consecutive CTAs share B tiles in L2
-  constexpr int G = 8;
-  const int per_group = G * n_tiles;
-  const int group = t / per_group;
-  const int first_m = group * G;
-  const int gsize = min(m_tiles - first_m, G);
-  const int in_group = t - group * per_group;
-  TileCoord c;
-  c.m0 = (first_m + in_group % gsize) * BM;
-  c.n0 = (in_group / gsize) * bn;
-  return c;
-}
-
-struct KParams {
-  int M, N, K;
-  GemmEpilogue epi;
-  int splits;         // split-K factor (>= 1); splits > 1 writes raw fp32 partials
-  int kb_per_split;   // k-blocks per split
-  float* part;        // [splits][M][ld_part] when splits > 1
-  long long ld_part;
-  int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
-  int aux_stage;        // ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot
-  int raster;           // CTA-pair kernel: M-tiles per raster group
-  int tail_split;       // CTA-pair kernel, > 0: tiles are taken row-major; the last tail_split tiles are
-  int tail_full;        //   computed as two K-halves each, reduce-added into the zeroed fp32 output
-  int batch;            // independent GEMMs (bmm lanes), >= 1
-  long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
-};
-
-// ----------------------------------------------------- TMA-store epilogue
-// Each epilogue warp owns a 4 KB, 1024-byte aligned staging slot.  A 32x32
-// chunk is written row-per-lane in the TMA swizzled layout (conflict-free
-// 16-byte stores) and one lane issues a bulk tensor store, so the global
-// writes are fully coalesced and asynchronous.
-constexpr int STAGE_SLOT = 4096;
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-// bulk tensor store with fp32 add into global memory (the split tail tiles)
-__device__ __forceinline__ void tma_store_add_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// bf16 rows are 64 B: SWIZZLE_64B puts 16-byte chunk c of row r at c ^ ((r >> 1) & 3)
-__device__ __forceinline__ void stage_bf16(uint8_t* slot, const float (&v)[32], int lane) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t w[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * c + 2 * j], v[8 * c + 2 * j + 1]);
-      w[j] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    *reinterpret_cast<uint4*>(slot + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-// fp32 rows are 128 B: SWIZZLE_128B puts chunk c of row r at c ^ (r & 7)
-__device__ __forceinline__ void stage_f32(uint8_t* slot, const float (&v)[32], int lane) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-    *reinterpret_cast<float4*>(slot + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-}
-// warp-collective: stage one chunk and bulk-store it at (n0, row0)
-template <bool BF16>
-__device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap* map, const float (&v)[32], int lane,
-                                               int n0, int row0, int bidx, bool add = false) {
-  if (lane == 0) bulk_wait_read0();  // the slot's previous store has been read out
-  __syncwarp();
-  if (BF16) stage_bf16(slot, v, lane);
-  else stage_f32(slot, v, lane);
-  fence_proxy_async();
-  __syncwarp();
-  if (lane == 0) {
-    if (add) tma_store_add_3d(map, slot, n0, row0, bidx);
-    else tma_store_3d(map, slot, n0, row0, bidx);
-    bulk_commit();
-  }
-}
-
-// ACT_GRAD saved activations through TMA: a 32 x 32 bf16 block (SWIZZLE_64B,
-// the layout stage_bf16 writes) lands in the upper 2 KB of the warp's
-// staging slot, so the next chunk's block is in flight while this one is
-// processed (and the tile's first block while the accumulator is computed).
-constexpr int AUX_OFF = 2048;
-__device__ __forceinline__ void aux_issue(uint8_t* slot, const CUtensorMap* map, uint64_t* bar, int n0, int row0) {
-  mbar_expect_tx(bar, 2048);
-  tma_load_3d(slot + AUX_OFF, map, bar, n0, row0, 0);
-}
-__device__ __forceinline__ void aux_read(const uint8_t* slot, float (&h)[32], int lane) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint4 w = *reinterpret_cast<const uint4*>(slot + AUX_OFF + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4));
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(b[j]);
-      h[8 * c + 2 * j] = f.x;
-      h[8 * c + 2 * j + 1] = f.y;
-    }
-  }
-}
-
-// One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
-// fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
-// `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
-__device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
-                                          bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
-                                          const float (&hs)[32], uint8_t* slot, bool radd,
-                                          const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
-  const GemmEpilogue& e = p.epi;
-  const bool full = n0 + 32 <= p.N;
-  const int nn = full ? 32 : p.N - n0;
-  if (p.splits > 1) {  // split-K: raw fp32 partial of this K range
-    if (row_ok) store_row_f32(p.part + ((long long)split * p.M + m) * p.ld_part + n0, v, nn);
-    return;
-  }
-  if (!grp_ok) return;  // the whole 32-row group is past M (warp-uniform)
-  bool ovf = false;      // domain flag of this lane's row (the vote below runs converged)
-  if (!row_ok) {
-    // rows past M: zeros for the column sums; TMA clips them on store
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-  } else if (e.mode == SG_EPI_BIAS_ACT) {
-    if (e.bias) {
-      float bv[32];
-      if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + i));
-          bv[i] = b4.x, bv[i + 1] = b4.y, bv[i + 2] = b4.z, bv[i + 3] = b4.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += bv[i];
-    }
-    if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
-    if (e.act == SG_ACT_SIGMOID) {
-      // the reference's scalar_sigmoid computes math.exp(-z): OverflowError for
-      // z < -709.78 (tensor.py:214-215); flagged, the value below is still 0
-#pragma unroll
-      for (int i = 0; i < 32; ++i) ovf |= v[i] <= SIGMOID_OVF_F32;
-    }
-    act_fwd_chunk(v, e.act);
-  } else if (e.mode == SG_EPI_ACT_GRAD) {
-    if (hstaged) {
-      act_grad_chunk(v, hs, e.act);
-    } else {
-      float h[32];
-      if (e.aux_f32) load_row_f32(e.aux_f32 + (long long)m * e.ld_aux + n0, h, nn);
-      else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
-      act_grad_chunk(v, h, e.act);
-    }
-  }
-  if (e.mode == SG_EPI_BIAS_ACT && e.act == SG_ACT_SIGMOID && e.dom) {  // warp-uniform
-    if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
-  }
-  const int row0 = m - lane;
-  if (e.out_f32) {
-    if (radd) {  // split tail tile: add this K-half into the zeroed output (two terms: order-free)
-      if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx, true);
-      else if (row_ok) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i < nn) atomicAdd(e.out_f32 + (long long)m * e.ld_f32 + n0 + i, v[i]);
-      }
-    } else if (p.tma_f32) {
-      warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx);
-    } else if (row_ok) {
-      store_row_f32(e.out_f32 + bidx * p.so_f32 + (long long)m * e.ld_f32 + n0, v, nn);
-    }
-  }
-  if (e.out_bf16) {
-    if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0, bidx);
-    else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
-  }
-  // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
-  // transpose-reduce destroys v, so it runs after the stores
-  if (e.colsum) warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
-}
 
 template <bool TF32, int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -668,65 +231,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                  : "memory");
   }
-}
-
-// ===================================================== 2-SM (CTA pair) variant
-// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile.
-// Each CTA stages 128 rows of A and 128 rows (half the N extent) of B per
-// k-block (32 KB, 6-deep ring); the leader CTA issues tcgen05.mma with
-// M = 256 and the tensor cores read both CTAs' shared memory; each CTA's
-// TMEM holds its 128 rows of the fp32 accumulator.  Half the smem operand
-// traffic per SM and 2/3 of the L2->SM bytes per FLOP of the 1-SM kernel.
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  // relaxed: the accumulator hand-back only needs the preceding tcgen05 fence,
-  // not the epilogue's global stores to be acknowledged
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
-                                                 int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-template <bool TF32>
-__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  if (TF32)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  else
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on the barrier in both CTAs
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
 }
 
 template <bool TF32, int STAGES, bool A_MN, bool B_MN>
@@ -979,7 +483,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
 // ================================================================ host side
 namespace sg {
 
-namespace {
+namespace tcmap {  // tensor-map builders, shared with gemm_chain.cu
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1081,6 +585,11 @@ void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& 
   if (g.epi.out_f32)
     p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32, g.batch, g.so_f32);
 }
+
+}  // namespace tcmap
+using namespace tcmap;
+
+namespace {
 
 // split-K finalize: out = sum_s part[s] in ascending s (deterministic)
 // blockIdx.y = row, threads over 4-column groups (no 64-bit divides, float4 loads)

@@ -132,6 +132,7 @@ def _lib():
         lib.sg_act_grad.argtypes = [P, P, I32, I64, P, I32, I64, I64, I64, I32, P, I32, I64, P, I32, I64,
                                     P, I64, P]
         lib.sg_colsum_finalize.argtypes = [P, P, I64, I64, I64, P, P]
+        lib.sg_colsum_finalize_multi.argtypes = [P, I32, P, P, P, P, P, P]
         lib.sg_colsum_strict.argtypes = [P, P, I32, I64, I64, I64, P, P]
         lib.sg_loss.argtypes = [P, I32, P, I32, I64, P, I64, I64, I64, D, P, P, I64, P, I32, I64, P, I32,
                                 I64, P, I64, P]
@@ -142,7 +143,7 @@ def _lib():
         lib.sg_cast_2d.argtypes = [P, P, I32, I64, P, I32, I64, I64, I64, P]
         lib.sg_dense_forward.argtypes = [P, ctypes.POINTER(DenseDesc), P, I64, P, I64, P, I64, P]
         lib.sg_dense_backward.argtypes = [P, ctypes.POINTER(DenseDesc), ctypes.POINTER(DenseGrad), P]
-        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d",
+        for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_finalize_multi", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d",
                   "sg_dense_forward", "sg_dense_backward"):
             getattr(lib, n).restype = ctypes.c_int
         _bound = True
@@ -340,6 +341,21 @@ def slice_first_layer_buckets(buckets, w_off0: int, fan_in: int, fan_out: int, s
     return sub + list(buckets[1:])
 
 
+def _pair_splits(M: int, N: int, K: int, pairs: int) -> int:
+    """The split-K factor the CTA-pair GEMM picks for a plain-store product
+    (gemm_tc.cu run_pair): used for the chained dW so the K-split sums --
+    and hence the gradients -- are bit-identical to the per-layer path."""
+    tiles = -(-M // 256) * -(-N // 256)
+    num_kb = -(-K // 64)
+    if tiles * 2 > pairs or num_kb < 8:
+        return 1
+    s = min(pairs // tiles, num_kb // 4, 16)
+    if s < 2:
+        return 1
+    kb_per = -(-num_kb // s)
+    return -(-num_kb // kb_per)
+
+
 def bucket_of_layer(layer: int, l0_slices: int = 1, slice_k: int = 0) -> int:
     """Index of the gradient bucket that holds `layer` (and, for layer 0 in
     `l0_slices` > 1 row slices, its slice `slice_k`) in the bucket list of
@@ -361,7 +377,9 @@ class ChainEngine:
     """Device state + kernels of a Dense chain's training step on one GPU."""
 
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", precision: str = "bf16",
-                 global_batch: int | None = None, small: bool = True):
+                 global_batch: int | None = None, small: bool = True, gemm_chain: bool | None = None):
+        import os
+
         import torch
 
         if loss not in LOSSES:
@@ -418,9 +436,24 @@ class ChainEngine:
         self.Zt = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
         self.Y = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
         dmax = max(self.sizes[1:])
-        self.dZ = [torch.zeros((B, _ld(dmax)), dtype=self.adt, device=dev) for _ in range(2)]
+        # persistent GEMM chains (sg_chain_*): the forward GEMMs of all layers in
+        # one launch and the dX / dW GEMMs of all layers in another.  They need
+        # every layer's dZ and bias-gradient partials in their own buffers (no
+        # ping-pong: a chained dX may run while an earlier layer's dW still
+        # reads the dZ it would overwrite).  bf16 only; off under data
+        # parallelism (buckets are all-reduced per layer as the pullback goes).
+        if gemm_chain is None:
+            gemm_chain = os.environ.get("SGB200_CHAIN", "1") != "0"
+        self.chainable = bool(gemm_chain) and precision == "bf16" and self.L >= 2
+        self.chains = None
+        if self.chainable:
+            self.dZl = [torch.zeros((B, _ld(d)), dtype=self.adt, device=dev)[:, :d] for d in self.sizes[1:]]
+            self.csl = [torch.zeros(((B + 31) // 32, _ld(d)), dtype=torch.float32, device=dev)
+                        for d in self.sizes[1:]]
+        else:
+            self.dZ = [torch.zeros((B, _ld(dmax)), dtype=self.adt, device=dev) for _ in range(2)]
+            self.colsum = torch.zeros(((B + 31) // 32, _ld(dmax)), dtype=torch.float32, device=dev)
         self.dH = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
-        self.colsum = torch.zeros(((B + 31) // 32, _ld(dmax)), dtype=torch.float32, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         n_part = max(1, ((dmax + 31) // 32) * ((B + 31) // 32))
         self.loss_part = torch.zeros(n_part, dtype=torch.float64, device=dev)
@@ -449,6 +482,18 @@ class ChainEngine:
     def get_grads(self):
         return [(self.gW[l].double().cpu().numpy(), self.gb[l].double().cpu().numpy()) for l in range(self.L)]
 
+    def dz_of(self, l):
+        """dL/d(z_l + b_l) of layer l, [B][fan_out_l] (the layer's pullback seed)."""
+        if self.chainable:
+            return self.dZl[l]
+        return self.dZ[l % 2][:, :self.sizes[l + 1]]
+
+    def cs_of(self, l):
+        """Per-32-row column-sum partials of dz_of(l) (tensor-core precisions)."""
+        if not self.tc:
+            return None
+        return self.csl[l] if self.chainable else self.colsum
+
     # ------------------------------------------------------------- inputs
     def load_batch(self, X, Y) -> None:
         """Load one minibatch (device tensors) with the library's kernels: X is
@@ -471,6 +516,12 @@ class ChainEngine:
     def forward(self):
         """Record the forward pass on the tape; returns the top-layer outputs."""
         self.tape.clear()
+        if self._use_chain():
+            self.chains[0].run()
+            # one tape entry for the whole chain: its pullback is the chained
+            # dX / dW pass (the save set is every H[l] and W[l], as per layer)
+            self.tape.push(TapeEntry("dense_chain", tuple(self.H) + tuple(self.W), self._chain_backward, None))
+            return self.Zt
         L = self.L
         for l in range(L):
             last = l == L - 1
@@ -481,6 +532,59 @@ class ChainEngine:
             self.tape.push(TapeEntry(f"dense{l}", (self.H[l], self.W[l]),
                                      self._make_backward(l), self._ready(l)))
         return self.Zt
+
+    def _use_chain(self) -> bool:
+        """Chains run when this engine can use them and no per-layer hooks are
+        installed (data-parallel buckets, layer-0 slices); planned on first use."""
+        if not self.chainable or self.grad_ready is not None or self.l0_slices > 1:
+            return False
+        if self.chains is None:
+            self.chains = self._plan_chains()
+        return True
+
+    def _plan_chains(self):
+        """The forward and backward GemmChains of this engine's buffers: the
+        same GEMMs (operands, epilogues, split-K factors) sg_dense_forward /
+        sg_dense_backward issue layer by layer, with row-block dependencies."""
+        import torch
+
+        from .gemm import GemmChain, gemm_desc
+
+        L, B = self.L, self.B
+        fwd = []
+        for l in range(L):
+            top = l == L - 1
+            d = gemm_desc(self.H[l], self.Ws[l], epilogue="bias_act", act=self.acts[l], bias=self.b[l],
+                          out_lp=None if top else self.H[l + 1], out=self.Zt if top else None)
+            fwd.append((d, 1, [("rows", l - 1)] if l > 0 else []))
+        pairs = max(1, torch.cuda.get_device_properties(self.P.device).multi_processor_count // 2)
+        bwd, dx_idx = [], {}
+        for l in range(L - 1, -1, -1):
+            dz = self.dz_of(l)
+            if l > 0:
+                act_prev = self.acts[l - 1]
+                d = gemm_desc(dz, self.Ws[l], b_mn=True, epilogue="store" if act_prev == "identity" else "act_grad",
+                              act=act_prev, aux=self.H[l], out_lp=self.dz_of(l - 1), colsum=self.cs_of(l - 1))
+                bwd.append((d, 1, [("rows", dx_idx[l + 1])] if l + 1 in dx_idx else []))
+                dx_idx[l] = len(bwd) - 1
+            d = gemm_desc(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l])
+            bwd.append((d, _pair_splits(self.sizes[l + 1], self.sizes[l], B, pairs),
+                        [("krows", dx_idx[l + 1])] if l + 1 in dx_idx else []))
+        return GemmChain(fwd), GemmChain(bwd)
+
+    def _chain_backward(self, _ctx):
+        """Chained pullback: every layer's dX (with the lower layer's act' and
+        bias-gradient partials fused) and dW in one launch, then every db."""
+        self.chains[1].run()
+        lib = _lib()
+        n = self.L
+        parts = (ctypes.c_void_p * n)(*[_p(self.cs_of(l)) for l in range(n)])
+        outs = (ctypes.c_void_p * n)(*[_p(self.gb[l]) for l in range(n)])
+        G = (ctypes.c_int64 * n)(*[(self.B + 31) // 32] * n)
+        ld = (ctypes.c_int64 * n)(*[self.cs_of(l).stride(0) for l in range(n)])
+        N = (ctypes.c_int64 * n)(*[self.sizes[l + 1] for l in range(n)])
+        rt.check(lib.sg_colsum_finalize_multi(rt.context(), n, parts, G, ld, N, outs, rt.stream_ptr()),
+                 "sg_colsum_finalize_multi")
 
     def _ready(self, l):
         def cb(_entry):
@@ -516,7 +620,8 @@ class ChainEngine:
         ctx, st = rt.context(), rt.stream_ptr()
         top = self.L - 1
         dL = self.sizes[-1]
-        dz = self.dZ[top % 2][:, :dL]
+        dz = self.dz_of(top)
+        cs = self.cs_of(top)
         ident = self.acts[top] == "identity"
         strict = not self.tc
         target = dz if ident else self.dH
@@ -526,13 +631,13 @@ class ChainEngine:
                              _p(Y), Y.stride(0), self.B, dL, self.scale, _p(self.loss),
                              _p(self.loss_part), self.loss_part.numel(), _p(target), _dt(target),
                              target.stride(0), None, 0, 0,
-                             None if (strict or not ident) else _p(self.colsum), self.colsum.stride(0), st),
+                             None if (strict or not ident) else _p(cs), 0 if cs is None else cs.stride(0), st),
                  "sg_loss")
         if not ident:  # top activation: dz = dL/dh * act'(h)  (rules.py:82-94)
             rt.check(lib.sg_act_grad(ctx, _p(self.dH), _dt(self.dH), self.dH.stride(0), _p(self.Zt),
                                      _dt(self.Zt), self.Zt.stride(0), self.B, dL, ACT[self.acts[top]],
                                      _p(dz), _dt(dz), dz.stride(0), None, 0, 0,
-                                     None if strict else _p(self.colsum), self.colsum.stride(0), st),
+                                     None if strict else _p(cs), 0 if cs is None else cs.stride(0), st),
                      "sg_act_grad")
         return self.loss
 
@@ -540,8 +645,8 @@ class ChainEngine:
     def _make_backward(self, l):
         def backward(_ctx):
             d_out, d_in = self.sizes[l + 1], self.sizes[l]
-            dz = self.dZ[l % 2][:, :d_out]
-            cs = self.colsum if self.tc else None
+            dz = self.dz_of(l)
+            cs = self.cs_of(l)
             if l == 0 and self.l0_slices > 1:
                 S = self.l0_slices
                 rows = d_out // S
@@ -557,9 +662,9 @@ class ChainEngine:
             # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
             # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below
             dense_backward(self.descs[l], dz, self.gW[l], self.gb[l],
-                           dX=self.dZ[(l - 1) % 2][:, :d_in] if l > 0 else None,
+                           dX=self.dz_of(l - 1) if l > 0 else None,
                            act_prev=self.acts[l - 1] if l > 0 else "identity",
-                           colsum_in=cs, colsum_out=cs if l > 0 else None)
+                           colsum_in=cs, colsum_out=self.cs_of(l - 1) if l > 0 else None)
         return backward
 
     def pullback(self):

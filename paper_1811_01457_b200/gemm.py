@@ -111,6 +111,15 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     ``colsum`` (fp32 ``[ceil(M/32)][>=N]``) receives per-32-row column sums of
     the result (the first stage of a bias gradient).
     """
+    d = gemm_desc(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, precision=precision, epilogue=epilogue, act=act,
+                  bias=bias, aux=aux, out=out, out_lp=out_lp, out_pre=out_pre, colsum=colsum)
+    rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
+
+
+def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
+              epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
+              out_pre=None, colsum=None) -> GemmDesc:
+    """The validated ``sg_gemm_desc`` of a GEMM (see :func:`gemm`), without launching it."""
     if a_mn:
         Ka, Ma = A.shape
     else:
@@ -151,7 +160,73 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     d.out, d.ld_out = _ptr(out), _ld(out)
     d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
     d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
-    rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
+    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum)  # the buffers stay alive with the descriptor
+    return d
+
+
+DEP = {"rows": 1, "krows": 2, "all": 3}
+
+
+class ChainProblem(ctypes.Structure):  # sg_chain_problem
+    _fields_ = [("gemm", GemmDesc), ("splits", ctypes.c_int32), ("n_deps", ctypes.c_int32),
+                ("dep_kind", ctypes.c_int32 * 2), ("dep_on", ctypes.c_int32 * 2)]
+
+
+class GemmChain:
+    """A persistent GEMM chain (``sg_chain_*``, include/sgb200.h): a list of
+    GEMMs -- each a :class:`GemmDesc` with optional dependencies on earlier
+    ones, ``[(kind, index), ...]`` with kind "rows" / "krows" / "all" -- planned
+    once and run as ONE launch per :meth:`run`.  Bit-identical to running the
+    same GEMMs one by one with :func:`gemm` (same tiles, k order and split-K
+    summation order)."""
+
+    def __init__(self, problems):
+        lib = _lib()
+        if not getattr(lib, "_chain_bound", False):
+            P = ctypes.c_void_p
+            lib.sg_chain_create.argtypes = [P, ctypes.POINTER(ChainProblem), ctypes.c_int32, ctypes.POINTER(P)]
+            lib.sg_chain_run.argtypes = [P, P]
+            lib.sg_chain_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                          ctypes.POINTER(ctypes.c_double)]
+            lib.sg_chain_destroy.argtypes = [P]
+            for n in ("sg_chain_create", "sg_chain_run", "sg_chain_info", "sg_chain_destroy"):
+                getattr(lib, n).restype = ctypes.c_int
+            lib._chain_bound = True
+        self.lib = lib
+        arr = (ChainProblem * len(problems))()
+        self.keep = []
+        for i, (desc, splits, deps) in enumerate(problems):
+            if desc.precision != PREC["bf16"]:
+                raise ValueError("chained GEMMs are bf16 tensor-core GEMMs")
+            arr[i].gemm = desc
+            self.keep.append(getattr(desc, "keep", None))
+            arr[i].splits = int(splits)
+            arr[i].n_deps = len(deps)
+            for k, (kind, q) in enumerate(deps):
+                if not 0 <= q < i:
+                    raise ValueError(f"chain problem {i}: dependency on {q} is not an earlier problem")
+                arr[i].dep_kind[k] = DEP[kind]
+                arr[i].dep_on[k] = q
+        h = ctypes.c_void_p()
+        rt.check(lib.sg_chain_create(rt.context(), arr, len(problems), ctypes.byref(h)), "sg_chain_create")
+        self.handle = h
+        u, c, est = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        rt.check(lib.sg_chain_info(h, ctypes.byref(u), ctypes.byref(c), ctypes.byref(est)), "sg_chain_info")
+        self.units, self.ctas, self.est_us = u.value, c.value, est.value
+
+    def run(self, stream=None) -> None:
+        rt.check(self.lib.sg_chain_run(self.handle, rt.stream_ptr(stream)), "sg_chain_run")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.sg_chain_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _ld3(t):
