@@ -46,8 +46,15 @@ constexpr int PM = 256, PN = 256, HALF = 128, CBK = 64;  // pair tile, k-block (
 constexpr int CSTAGES = 6;
 constexpr int SLOTS = 2 * EPI_WARPS;                     // epilogue warps per pair tile
 
-struct __align__(64) Problem {
-  CUtensorMap map_a, map_b, map_lp, map_f32, map_aux;
+// A problem's tensor maps live in global memory (TMA reads them there); the
+// rest of its description is in the kernel's parameter space, so the
+// epilogue reads it through the constant cache with no alias reloads.
+struct Maps {
+  CUtensorMap a, b, lp, f32, aux;
+};
+constexpr int MAX_PROBS = 96;
+
+struct Problem {
   KParams p;
   int a_mn, b_mn;
   int m_tiles, n_tiles, num_kb;
@@ -63,13 +70,14 @@ struct Unit {
 };
 
 struct Params {
-  const Problem* probs;
+  const Maps* maps;     // [n problems]
   const Unit* units;    // the pairs' lists, concatenated
   const int* list_off;  // [pairs + 1]
   unsigned* cnt;        // row-block arrival counters (zero between launches)
   unsigned* split_cnt;  // split-K arrival counters (reset by their last arriver)
   unsigned* done;       // CTAs finished; the last one clears cnt
   int n_cnt;
+  Problem probs[MAX_PROBS];
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -120,7 +128,7 @@ __device__ __forceinline__ void signal_rows(const Params& P, const Problem& pr, 
   if (lane == 0) {
     bulk_wait0();                // this warp's TMA stores have landed
     fence_proxy_async_global();  // async-proxy writes ordered before the generic release
-    __threadfence();             // and the warp's direct stores (observed through __syncwarp)
+    if (!pr.p.tma_lp && !pr.p.tma_f32) __threadfence();  // direct stores of the warp (seen through __syncwarp)
     red_release(P.cnt + pr.cnt_off + mb, 1u);
   }
 }
@@ -235,6 +243,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
   const uint32_t tmem_base = *tmem_slot;
   grid_dep_wait();
   grid_dep_launch();
+  SG_TRACE_BEGIN();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -259,16 +268,16 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
           if (a_mn) {
 #pragma unroll
             for (int j = 0; j < HALF / CBK; ++j)
-              tma_load_3d_pair(sa + j * E::MN_CHUNK, &pr.map_a, fb, am + CBK * j, k0, 0);
+              tma_load_3d_pair(sa + j * E::MN_CHUNK, &P.maps[un.prob].a, fb, am + CBK * j, k0, 0);
           } else {
-            tma_load_3d_pair(sa, &pr.map_a, fb, k0, am, 0);
+            tma_load_3d_pair(sa, &P.maps[un.prob].a, fb, k0, am, 0);
           }
           if (b_mn) {
 #pragma unroll
             for (int j = 0; j < HALF / CBK; ++j)
-              tma_load_3d_pair(sb + j * E::MN_CHUNK, &pr.map_b, fb, bn + CBK * j, k0, 0);
+              tma_load_3d_pair(sb + j * E::MN_CHUNK, &P.maps[un.prob].b, fb, bn + CBK * j, k0, 0);
           } else {
-            tma_load_3d_pair(sb, &pr.map_b, fb, k0, bn, 0);
+            tma_load_3d_pair(sb, &P.maps[un.prob].b, fb, k0, bn, 0);
           }
           if (++stage == CSTAGES) {
             stage = 0;
@@ -297,6 +306,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (kb == kb0) SG_TRACE(i - u0, 0);  // MMA starts
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -339,32 +349,37 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
       const int c0 = half * CH_PER, c1 = (half + 1) * CH_PER;
       uint8_t* slot = stage_slots + ew * STAGE_SLOT;
       const bool staged = p.aux_stage && row0 < p.M;
-      if (staged && lane == 0 && n0t + c0 * 32 < p.N) aux_issue(slot, &pr.map_aux, &aux_bar[ew], n0t + c0 * 32, row0);
+      if (staged && lane == 0 && n0t + c0 * 32 < p.N) aux_issue(slot, &P.maps[un.prob].aux, &aux_bar[ew], n0t + c0 * 32, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane == 0) SG_TRACE(i - u0, 1);  // accumulator complete
       const int m = row0 + lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
       for (int c = c0; c < c1; ++c) {
         const int n0 = n0t + c * 32;
         float v[32];
+        SG_CPROF_START();
         tmem_ld32(tmem_base + acc * PN + ((uint32_t)(q * 32) << 16) + c * 32, v);
+        SG_CPROF(0);  // TMEM load
         if (n0 >= p.N) continue;
         float h[32];
         if (staged) {
           mbar_wait(&aux_bar[ew], aux_phase);
+          SG_CPROF(1);  // saved activation block arrived
           aux_phase ^= 1;
           aux_read(slot, h, lane);
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &pr.map_aux, &aux_bar[ew], n0 + 32, row0);
+          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &P.maps[un.prob].aux, &aux_bar[ew], n0 + 32, row0);
         }
         epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, un.split, 0, staged, h, slot, false,
-                  &pr.map_lp, &pr.map_f32);
+                  &P.maps[un.prob].lp, &P.maps[un.prob].f32);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
+      if (lane == 0 && ew == 0) SG_TRACE(i - u0, 2);  // chunks done, accumulator released
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -373,6 +388,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
         split_fixup(P, pr, un, (int)rank * EPI_WARPS + ew, row0, n0t + c0 * 32, c1 - c0, lane);
       else if (pr.signal)
         signal_rows(P, pr, un.mb, lane);
+      if (lane == 0 && ew == 0) SG_TRACE(i - u0, 3);  // warp 0 done (signal / split fix-up included)
     }
   }
   if (warp >= EPI_WARP0 && lane == 0) bulk_wait0();
@@ -384,6 +400,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                  : "memory");
   }
+  SG_TRACE_END();
   // the last CTA to finish clears the row-block counters for the next launch
   if (threadIdx.x == 0) {
     __threadfence();
@@ -436,20 +453,51 @@ static_assert(CHAIN_SMEM <= 232448, "shared memory budget");
 
 }  // namespace
 
+#ifdef SGB200_GEMM_TRACE
+extern "C" SG_API int sg_chain_trace_buffer(void* buf, int iters, int launches) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  const unsigned zero = 0;
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace, &p, sizeof p));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_iters, &iters, sizeof iters));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_launches, &launches, sizeof launches));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_seq, &zero, sizeof zero));
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_done, &zero, sizeof zero));
+  return SG_OK;
+}
+#endif
+
+#ifdef SGB200_GEMM_TRACE
+// epilogue stage profile: on != 0 clears and enables, on == 0 disables and reads out
+extern "C" SG_API int sg_chain_cprof(int on, unsigned long long* out8) {
+  if (on) {
+    unsigned long long z[8] = {0};
+    SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_cprof, z, sizeof z));
+  } else if (out8) {
+    SG_CUDA_TRY(cudaMemcpyFromSymbol(out8, tc::g_cprof, 8 * sizeof(unsigned long long)));
+  }
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_cprof_on, &on, sizeof on));
+  return SG_OK;
+}
+#endif
+
 extern "C" {
 
 int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_chain** out) {
   if (!ctx || !probs || !out || n <= 0) return fail(SG_EINVAL, "chain: null argument or empty chain");
   if (int rc = ctx_activate(ctx)) return rc;
   const int pairs = std::max(1, ctx_compute_sms(ctx) / 2);
+  if (n > chain::MAX_PROBS) return fail(SG_EINVAL, "chain: at most 96 GEMMs per chain");
   std::vector<chain::Problem> hp(n);
+  std::vector<chain::Maps> hm(n);
   long long n_cnt = 0, n_split = 0, n_part = 0;
   std::vector<long long> part_off(n, -1);
   for (int i = 0; i < n; ++i) {
     const sg_chain_problem& cp = probs[i];
     const sg_gemm_desc* d = &cp.gemm;
     chain::Problem& pr = hp[i];
+    chain::Maps& mp = hm[i];
     std::memset(&pr, 0, sizeof pr);
+    std::memset(&mp, 0, sizeof mp);
     const std::string at = "chain problem " + std::to_string(i) + ": ";
     if (d->precision != SG_PREC_BF16) return fail(SG_EINVAL, at + "chained GEMMs are BF16 tensor-core GEMMs");
     if (d->M <= 0 || d->N <= 0 || d->K <= 0 || d->M > (1ll << 31) - 1 || d->N > (1ll << 31) - 1 ||
@@ -491,11 +539,11 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
     g.epi.ld_colsum = d->ld_colsum;
     g.epi.dom = ctx_domain_word(ctx);
     g.batch = 1;
-    int rc = g.a_mn ? tcmap::make_map(&pr.map_a, g.A, g.M, g.K, g.lda, chain::CBK, false, true, 1, 0)
-                    : tcmap::make_map(&pr.map_a, g.A, g.K, g.M, g.lda, 128, false, false, 1, 0);
+    int rc = g.a_mn ? tcmap::make_map(&mp.a, g.A, g.M, g.K, g.lda, chain::CBK, false, true, 1, 0)
+                    : tcmap::make_map(&mp.a, g.A, g.K, g.M, g.lda, 128, false, false, 1, 0);
     if (rc) return rc;
-    rc = g.b_mn ? tcmap::make_map(&pr.map_b, g.B, g.N, g.K, g.ldb, chain::CBK, false, true, 1, 0)
-                : tcmap::make_map(&pr.map_b, g.B, g.K, g.N, g.ldb, 128, false, false, 1, 0);
+    rc = g.b_mn ? tcmap::make_map(&mp.b, g.B, g.N, g.K, g.ldb, chain::CBK, false, true, 1, 0)
+                : tcmap::make_map(&mp.b, g.B, g.K, g.N, g.ldb, 128, false, false, 1, 0);
     if (rc) return rc;
     pr.num_kb = (g.K + chain::CBK - 1) / chain::CBK;
     pr.m_tiles = (g.M + chain::PM - 1) / chain::PM;
@@ -509,10 +557,8 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
     const int kb_per = (pr.num_kb + splits - 1) / splits;
     splits = (pr.num_kb + kb_per - 1) / kb_per;
     pr.p = tc::KParams{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, 1, 0, 0};
-    std::memset(&pr.map_lp, 0, sizeof pr.map_lp);
-    std::memset(&pr.map_f32, 0, sizeof pr.map_f32);
-    tcmap::out_maps(g, pr.p, pr.map_lp, pr.map_f32);
-    tcmap::aux_map(g, pr.p, pr.map_aux);
+    tcmap::out_maps(g, pr.p, mp.lp, mp.f32);
+    tcmap::aux_map(g, pr.p, mp.aux);
     if (splits > 1) {
       pr.p.ld_part = (g.N + 3) / 4 * 4;
       part_off[i] = n_part;
@@ -598,7 +644,7 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
   c->n_units = (int)units.size();
   c->est_us = makespan * 1e6;
   auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes < 64 ? 64 : bytes); };
-  cudaError_t e = alloc(&c->d_probs, sizeof(chain::Problem) * n);
+  cudaError_t e = alloc(&c->d_probs, sizeof(chain::Maps) * n);
   if (e == cudaSuccess) e = alloc(&c->d_units, sizeof(chain::Unit) * units.size());
   if (e == cudaSuccess) e = alloc(&c->d_list, sizeof(int) * list_off.size());
   if (e == cudaSuccess) e = alloc((void**)&c->d_cnt, sizeof(unsigned) * std::max(1ll, n_cnt));
@@ -611,7 +657,7 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
   }
   for (int i = 0; i < n; ++i)
     if (part_off[i] >= 0) hp[i].p.part = c->d_part + part_off[i];
-  e = cudaMemcpy(c->d_probs, hp.data(), sizeof(chain::Problem) * n, cudaMemcpyHostToDevice);
+  e = cudaMemcpy(c->d_probs, hm.data(), sizeof(chain::Maps) * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_units, units.data(), sizeof(chain::Unit) * units.size(),
                                        cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
@@ -623,7 +669,8 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
     chain_free(c);
     return cuda_fail(e, "chain: upload");
   }
-  c->params.probs = static_cast<const chain::Problem*>(c->d_probs);
+  c->params.maps = static_cast<const chain::Maps*>(c->d_probs);
+  for (int i = 0; i < n; ++i) c->params.probs[i] = hp[i];
   c->params.units = static_cast<const chain::Unit*>(c->d_units);
   c->params.list_off = static_cast<const int*>(c->d_list);
   c->params.cnt = c->d_cnt;

@@ -247,6 +247,29 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// Epilogue stage profile (trace builds only): cycles spent per stage of a
+// 32 x 32 chunk, summed over the lane-0 threads of the first 8 CTAs.
+#ifdef SGB200_GEMM_TRACE
+__device__ unsigned long long g_cprof[8];
+__device__ int g_cprof_on = 0;
+#define SG_CPROF_START() long long cprof_t = clock64()
+#define SG_CPROF(k)                                                                  \
+  do {                                                                               \
+    if (g_cprof_on && blockIdx.x < 8 && (threadIdx.x & 31) == 0) {                   \
+      const long long now = clock64();                                               \
+      atomicAdd(&g_cprof[k], (unsigned long long)(now - cprof_t));                   \
+      cprof_t = now;                                                                 \
+    }                                                                                \
+  } while (0)
+#else
+#define SG_CPROF_START() \
+  do {                   \
+  } while (0)
+#define SG_CPROF(k) \
+  do {              \
+  } while (0)
+#endif
+
 struct TileCoord {
   int m0, n0;
 };
@@ -371,6 +394,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
                                           bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
                                           const float (&hs)[32], uint8_t* slot, bool radd,
                                           const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
+  SG_CPROF_START();
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
   const int nn = full ? 32 : p.N - n0;
@@ -421,6 +445,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   if (e.mode == SG_EPI_BIAS_ACT && e.act == SG_ACT_SIGMOID && e.dom) {  // warp-uniform
     if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
   }
+  SG_CPROF(2);  // epilogue math
   const int row0 = m - lane;
   if (e.out_f32) {
     if (radd) {  // split tail tile: add this K-half into the zeroed output (two terms: order-free)
@@ -440,9 +465,11 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0, bidx);
     else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
   }
+  SG_CPROF(3);  // stores issued
   // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the
   // transpose-reduce destroys v, so it runs after the stores
   if (e.colsum) warp_colsum_store(v, e.colsum + (long long)grp * e.ld_colsum + n0, lane, nn);
+  SG_CPROF(4);  // column sums
 }
 
 
