@@ -530,8 +530,12 @@ bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, lon
                   long long sbatch) {
   const long long esz = bf16 ? 2 : 4;
   if (batch <= 1) sbatch = ld * M;
+  // (N * esz) % 16: TMA stores clip the row end only to 16 bytes -- a ragged
+  // row (e.g. 300 bf16) would get the elements up to the next 16-byte
+  // boundary written (tools/sanitize_cases.py guard bands); such outputs take
+  // the direct-store path
   if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || (sbatch * esz) % 16 || M <= 0 ||
-      N <= 0)
+      N <= 0 || (N * esz) % 16)
     return false;
   EncodeTiled enc = encode_fn();
   if (!enc) return false;

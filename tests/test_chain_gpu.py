@@ -50,7 +50,7 @@ def test_gemm_chain_dependencies_match_sequential_gemms(M, D):
             (dict(A=x0, B=W0, epilogue="bias_act", act="tanh", bias=b, out_lp=x1), 1, []),
             (dict(A=x1, B=W1, epilogue="bias_act", act="sigmoid", out_lp=x2, colsum=cs), 1, [("rows", 0)]),
             (dict(A=x1, B=x2, a_mn=True, b_mn=True, out=gw), _pair_splits(D, D, M, 74), [("krows", 1)]),
-            (dict(A=x2, B=W1, b_mn=True, out=x3), 1, [("all", 1)]),
+            (dict(A=x2, B=W1, b_mn=True, out=x3), _pair_splits(M, D, D, 74), [("all", 1)]),
         ]
         if mode == "seq":
             for kw, _, _ in specs:
@@ -114,7 +114,7 @@ def test_chained_training_run_matches_layer_path():
         try:
             chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(4)]).init_params(
                 np.random.default_rng(1))
-            tr = Trainer(chain, B, loss="mse", lr=0.01, precision="bf16", graph=True)
+            tr = Trainer(chain, B, loss="mse", lr=1e-3, precision="bf16", graph=True)
             assert tr.engine.chainable == use
             losses = [float(tr.step(X, Y).item()) for _ in range(6)]
             runs[use] = (losses, tr.engine.P.clone())

@@ -280,3 +280,29 @@ def test_split_tail_gemm(layout):
     assert torch.equal(outs[0], outs[1])
     got = outs[0].double().cpu().numpy()
     check_close(got, a, b.T)
+
+
+@pytest.mark.parametrize("N", [300, 296, 130])
+@pytest.mark.parametrize("out_kind", ["bf16", "f32"])
+def test_outputs_never_write_outside_the_result(N, out_kind):
+    """Guard bands: a GEMM writing into a column slice of a wider buffer (rows
+    padded past N, e.g. N = 300 bf16 = 600 bytes, not a 16-byte multiple)
+    leaves the padding and the memory around the buffer untouched.  (TMA
+    stores clip row ends only to 16 bytes; ragged rows take direct stores.)"""
+    M, K, ld = 520, 136, N + 12 + (-(N + 12)) % 8
+    dt = torch.bfloat16 if out_kind == "bf16" else torch.float32
+    A = torch.rand((M, K), device="cuda").to(torch.bfloat16)
+    B = torch.rand((N, K), device="cuda").to(torch.bfloat16)
+    buf = torch.full((M + 2, ld), 7.0, dtype=dt, device="cuda")
+    out = buf[1:M + 1, :N]
+    if out_kind == "bf16":
+        gemm(A, B, epilogue="bias_act", act="tanh", bias=torch.zeros(N, device="cuda"), out_lp=out)
+    else:
+        gemm(A, B, out=out)
+    torch.cuda.synchronize()
+    assert bool((buf[0] == 7).all()) and bool((buf[M + 1] == 7).all())
+    assert bool((buf[1:M + 1, N:] == 7).all())
+    want = A.double() @ B.double().T
+    if out_kind == "bf16":
+        want = torch.tanh(want)
+    assert float((out.double() - want).abs().max()) < 0.05 * float(want.abs().max())

@@ -1,6 +1,13 @@
-"""Small device cases for compute-sanitizer (memcheck / racecheck / synccheck).
+"""Small device cases with guard bands: out-of-bounds write checks without compute-sanitizer.
 
-  compute-sanitizer --tool memcheck python tools/sanitize_cases.py [case ...]
+compute-sanitizer is closed on this GPU pool (it prints "compute-sanitizer is
+closed on this pool ...": runs under it have left GPUs needing a reset), so
+every output here lives inside a guarded allocation -- sentinel bands before
+and after it and in the padding columns between its width and its row
+stride -- and each case checks that no kernel wrote outside its tensor, that
+the result is right (loose tolerance), and that a second run is bit-identical.
+
+  python tools/sanitize_cases.py [case ...]
 
 Cases: fused (K1 + K2 + pack of sigma(a*x+b)), gemm1 (1-SM tcgen05 tiles),
 pair (CTA-pair tiles), splitk (pair split-K + reduce), tail (split tail with
@@ -24,6 +31,33 @@ from paper_1811_01457_b200.train import Trainer  # noqa: E402
 
 bf = torch.bfloat16
 g = torch.Generator(device="cuda").manual_seed(0)
+GUARDS = []
+SENTINEL = {torch.float32: float("nan"), bf: float("nan"), torch.float64: float("nan")}
+
+
+def guarded(rows, cols, dtype=torch.float32, ld=None, band=4096):
+    """A [rows, cols] tensor of row stride ld (default: cols rounded up to 8, +8)
+    inside sentinel bands; registered for check_guards()."""
+    ld = ld or ((cols + 7) // 8 * 8 + 8)
+    buf = torch.full((band + rows * ld + band,), 12345.0, dtype=dtype, device="cuda")
+    body = buf[band:band + rows * ld].view(rows, ld)
+    body[:, :cols].fill_(0)
+    view = body[:, :cols]
+    GUARDS.append((buf, band, rows, ld, cols))
+    return view
+
+
+def check_guards():
+    for k, (buf, band, rows, ld, cols) in enumerate(GUARDS):
+        sentinel = torch.tensor(12345.0, dtype=buf.dtype, device="cuda")
+        what = f"guarded tensor #{k} ({rows} x {cols}, ld {ld}, {buf.dtype})"
+        assert bool((buf[:band] == sentinel).all()), f"write before {what}"
+        assert bool((buf[band + rows * ld:] == sentinel).all()), f"write after {what}"
+        if ld > cols:
+            pad = buf[band:band + rows * ld].view(rows, ld)[:, cols:]
+            bad = (pad != sentinel).nonzero()
+            assert len(bad) == 0, f"write into the row padding of {what}: {len(bad)} elements, first {bad[:4].tolist()}"
+    GUARDS.clear()
 
 
 def rnd(*shape, dtype=torch.float32, scale=1.0):
@@ -33,8 +67,11 @@ def rnd(*shape, dtype=torch.float32, scale=1.0):
 def check_gemm(M, N, K, a_mn=False, b_mn=False):
     A = rnd(K, M, dtype=bf) if a_mn else rnd(M, K, dtype=bf)
     B = rnd(K, N, dtype=bf) if b_mn else rnd(N, K, dtype=bf)
-    out = torch.empty((M, N), device="cuda")
+    out = guarded(M, N)
     gemm(A, B, a_mn=a_mn, b_mn=b_mn, out=out)
+    first = out.clone()
+    gemm(A, B, a_mn=a_mn, b_mn=b_mn, out=out)
+    assert torch.equal(first, out), "not deterministic"
     a = A.double().T if a_mn else A.double()
     b = B.double() if b_mn else B.double().T
     err = float((out.double() - a @ b).abs().max())
@@ -80,8 +117,8 @@ def case_tail():
 def case_actgrad():
     M, N, K = 512, 384, 256
     dZ, W, H = rnd(M, N, dtype=bf), rnd(N, K, dtype=bf, scale=0.1), (torch.rand((M, K), device="cuda")).to(bf)
-    lp = torch.empty((M, K), dtype=bf, device="cuda")
-    cs = torch.empty(((M + 31) // 32, K), device="cuda")
+    lp = guarded(M, K, bf)
+    cs = guarded((M + 31) // 32, K)
     gemm(dZ, W, b_mn=True, epilogue="act_grad", act="tanh", aux=H, out_lp=lp, colsum=cs)
     want = (dZ.double() @ W.double()) * (1 - H.double() ** 2)
     assert float((lp.double() - want).abs().max()) < 5e-2
@@ -101,9 +138,12 @@ def case_small():
 
 def case_chain():
     M, D = 1000, 300
-    x0, W0, W1 = rnd(M, D, dtype=bf), rnd(D, D, dtype=bf, scale=0.05), rnd(D, D, dtype=bf, scale=0.05)
-    x1, x2 = torch.empty((M, D), dtype=bf, device="cuda"), torch.empty((M, D), dtype=bf, device="cuda")
-    gw = torch.empty((D, D), device="cuda")
+    x0, W0, W1 = guarded(M, D, bf), guarded(D, D, bf), guarded(D, D, bf)
+    x0.copy_(rnd(M, D, dtype=bf))
+    W0.copy_(rnd(D, D, dtype=bf, scale=0.05))
+    W1.copy_(rnd(D, D, dtype=bf, scale=0.05))
+    x1, x2 = guarded(M, D, bf), guarded(M, D, bf)
+    gw = guarded(D, D)
     ch = GemmChain([
         (gemm_desc(x0, W0, epilogue="bias_act", act="tanh", out_lp=x1), 1, []),
         (gemm_desc(x1, W1, epilogue="bias_act", act="sigmoid", out_lp=x2), 1, [("rows", 0)]),
@@ -145,4 +185,5 @@ if __name__ == "__main__":
     for n in names:
         CASES[n]()
         torch.cuda.synchronize()
-        print("case", n, "ok", flush=True)
+        check_guards()
+        print("case", n, "ok (result, determinism, guard bands)", flush=True)
