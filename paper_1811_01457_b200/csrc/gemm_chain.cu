@@ -43,7 +43,7 @@ namespace chain {
 using namespace tc;
 
 constexpr int PM = 256, PN = 256, HALF = 128, CBK = 64;  // pair tile, k-block (bf16)
-constexpr int CSTAGES = 6;
+constexpr int CSTAGES = 5;  // + wide epilogue slots (see gemm_tc_dev.cuh)
 constexpr int SLOTS = 2 * EPI_WARPS;                     // epilogue warps per pair tile
 
 // A problem's tensor maps live in global memory (TMA reads them there); the
@@ -227,7 +227,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2 * EPI_WARPS);
     }
-    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
+    for (int w = 0; w < 2 * EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -340,42 +340,24 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
     const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0, aux_phase = 0;
+    int next_buf = 0;
+    uint8_t* slot = stage_slots + ew * Slot<true>::BYTES;
+    uint64_t* my_aux = &aux_bar[2 * ew];
     for (int i = u0; i < u1; ++i) {
       const Unit un = P.units[i];
       const Problem& pr = P.probs[un.prob];
       const KParams& p = pr.p;
       const int m0 = un.mb * PM, n0t = un.nb * PN;
       const int row0 = m0 + (int)rank * HALF + q * 32;
-      const int c0 = half * CH_PER, c1 = (half + 1) * CH_PER;
-      uint8_t* slot = stage_slots + ew * STAGE_SLOT;
+      const int c0 = half * CH_PER;
       const bool staged = p.aux_stage && row0 < p.M;
-      if (staged && lane == 0 && n0t + c0 * 32 < p.N) aux_issue(slot, &P.maps[un.prob].aux, &aux_bar[ew], n0t + c0 * 32, row0);
+      const Maps* mp = &P.maps[un.prob];
+      epi_aux_prologue<true>(staged, lane, slot, &mp->aux, my_aux, n0t + c0 * 32, CH_PER, p.N, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane == 0) SG_TRACE(i - u0, 1);  // accumulator complete
-      const int m = row0 + lane;
-      const bool row_ok = m < p.M;
-#pragma unroll 1
-      for (int c = c0; c < c1; ++c) {
-        const int n0 = n0t + c * 32;
-        float v[32];
-        SG_CPROF_START();
-        tmem_ld32(tmem_base + acc * PN + ((uint32_t)(q * 32) << 16) + c * 32, v);
-        SG_CPROF(0);  // TMEM load
-        if (n0 >= p.N) continue;
-        float h[32];
-        if (staged) {
-          mbar_wait(&aux_bar[ew], aux_phase);
-          SG_CPROF(1);  // saved activation block arrived
-          aux_phase ^= 1;
-          aux_read(slot, h, lane);
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &P.maps[un.prob].aux, &aux_bar[ew], n0 + 32, row0);
-        }
-        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, un.split, 0, staged, h, slot, false,
-                  &P.maps[un.prob].lp, &P.maps[un.prob].f32);
-      }
+      epi_chunks<true>(p, tmem_base + acc * PN + ((uint32_t)(q * 32) << 16), n0t + c0 * 32, c0, CH_PER, row0, lane,
+                       un.split, 0, false, slot, staged, &mp->aux, my_aux, aux_phase, &mp->lp, &mp->f32, next_buf);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
@@ -385,7 +367,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
         acc_phase ^= 1;
       }
       if (p.splits > 1)
-        split_fixup(P, pr, un, (int)rank * EPI_WARPS + ew, row0, n0t + c0 * 32, c1 - c0, lane);
+        split_fixup(P, pr, un, (int)rank * EPI_WARPS + ew, row0, n0t + c0 * 32, CH_PER, lane);
       else if (pr.signal)
         signal_rows(P, pr, un.mb, lane);
       if (lane == 0 && ew == 0) SG_TRACE(i - u0, 3);  // warp 0 done (signal / split fix-up included)
@@ -448,7 +430,7 @@ void chain_free(sg_chain* c) {
 }
 
 constexpr size_t CHAIN_SMEM = (size_t)chain::CSTAGES * 2 * 128 * tc::ROW_BYTES + 1024 + 1024 +
-                              tc::EPI_WARPS * tc::STAGE_SLOT;
+                              tc::EPI_WARPS * tc::Slot<true>::BYTES;
 static_assert(CHAIN_SMEM <= 232448, "shared memory budget");
 
 }  // namespace

@@ -233,7 +233,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   }
 }
 
-template <bool TF32, int STAGES, bool A_MN, bool B_MN>
+template <bool TF32, int STAGES, bool A_MN, bool B_MN, bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
@@ -316,7 +316,7 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2 * EPI_WARPS);  // every epilogue warp of both CTAs
     }
-    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
+    for (int w = 0; w < 2 * EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -422,38 +422,23 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0, aux_phase = 0;
+    int next_buf = 0;
     int it = 0;
+    uint8_t* slot = stage_slots + ew * Slot<WIDE>::BYTES;
+    uint64_t* my_aux = &aux_bar[2 * ew];
     for (int t = pair; t < tiles; t += pairs, ++it) {
       const TileCoord tc = coord(t);
       const int bidx = (t % out_tiles) / tiles_pb;
       const int row0 = tc.m0 + (int)rank * HALF + q * 32;
-      const int c0 = half * CH_PER, c1 = (half + 1) * CH_PER;
-      uint8_t* slot = stage_slots + ew * STAGE_SLOT;
+      const int c0 = half * CH_PER;
       const bool staged = p.aux_stage && row0 < p.M;  // warp-uniform
-      if (staged && lane == 0 && tc.n0 + c0 * 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], tc.n0 + c0 * 32, row0);
+      epi_aux_prologue<WIDE>(staged, lane, slot, &tma_aux, my_aux, tc.n0 + c0 * 32, CH_PER, p.N, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane == 0) SG_TRACE(it, 1);  // accumulator complete
-      const int m = row0 + lane;
-      const bool row_ok = m < p.M;
-#pragma unroll 1
-      for (int c = c0; c < c1; ++c) {
-        const int n0 = tc.n0 + c * 32;
-        float v[32];
-        tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
-        if (n0 >= p.N) continue;
-        float h[32];
-        if (staged) {
-          mbar_wait(&aux_bar[ew], aux_phase);
-          aux_phase ^= 1;
-          aux_read(slot, h, lane);
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
-        }
-        epi_chunk(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
-                  p.tail_split > 0 && t >= p.tail_full, &tma_olp, &tma_of32);
-      }
+      epi_chunks<WIDE>(p, tmem_base + acc * BN + ((uint32_t)(q * 32) << 16), tc.n0 + c0 * 32, c0, CH_PER, row0, lane,
+                       t / out_tiles, bidx, p.tail_split > 0 && t >= p.tail_full, slot, staged, &tma_aux, my_aux,
+                       aux_phase, &tma_olp, &tma_of32, next_buf);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
@@ -715,13 +700,15 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   return SG_OK;
 }
 
-template <bool TF32, bool A_MN, bool B_MN>
+template <bool TF32, bool A_MN, bool B_MN, bool WIDE>
 int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   constexpr int BK = tc::Elem<TF32>::BK;
-  constexpr int STAGES = 6;
+  // wide epilogue slots (double-buffered staging, aux two chunks ahead) cost
+  // one operand stage of the 227 KB
+  constexpr int STAGES = WIDE ? 5 : 6;
   constexpr int STAGE = 128 * tc::ROW_BYTES * 2;
   // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
-  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::STAGE_SLOT;
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::Slot<WIDE>::BYTES;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
@@ -731,7 +718,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true, g.batch, g.sb);
   else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false, g.batch, g.sb);
   if (rc) return rc;
-  auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN>;
+  auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN, WIDE>;
   static std::atomic<uint64_t> attr_set{0};  // per device
   if (first_on_device(attr_set))
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -813,11 +800,21 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
     const char* e = std::getenv("SGB200_GEMM_PAIR");
     return !(e && e[0] == '0');
   }();
+  static const bool wide = [] {
+    const char* e = std::getenv("SGB200_GEMM_WIDE");
+    return !(e && e[0] == '0');
+  }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
-    if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false>(g, num_sms, st);
-    if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true>(g, num_sms, st);
-    if (g.a_mn && g.b_mn) return run_pair<TF32, true, true>(g, num_sms, st);
-    return run_pair<TF32, true, false>(g, num_sms, st);
+    if (wide) {
+      if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, true>(g, num_sms, st);
+      if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, true>(g, num_sms, st);
+      if (g.a_mn && g.b_mn) return run_pair<TF32, true, true, true>(g, num_sms, st);
+      return run_pair<TF32, true, false, true>(g, num_sms, st);
+    }
+    if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, false>(g, num_sms, st);
+    if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, false>(g, num_sms, st);
+    if (g.a_mn && g.b_mn) return run_pair<TF32, true, true, false>(g, num_sms, st);
+    return run_pair<TF32, true, false, false>(g, num_sms, st);
   }
   return run_bn<TF32, 256>(g, num_sms, st);
 }

@@ -304,11 +304,22 @@ struct KParams {
 };
 
 // ----------------------------------------------------- TMA-store epilogue
-// Each epilogue warp owns a 4 KB, 1024-byte aligned staging slot.  A 32x32
-// chunk is written row-per-lane in the TMA swizzled layout (conflict-free
-// 16-byte stores) and one lane issues a bulk tensor store, so the global
-// writes are fully coalesced and asynchronous.
+// Each epilogue warp owns a 1024-byte aligned staging slot.  A 32x32 chunk is
+// written row-per-lane in the TMA swizzled layout (conflict-free 16-byte
+// stores) and one lane issues a bulk tensor store, so the global writes are
+// fully coalesced and asynchronous.
+//   narrow slot (4 KB): one staging buffer; the ACT_GRAD aux block in its
+//     upper 2 KB, one chunk ahead;
+//   wide slot (8 KB, WIDE kernels): two staging buffers used alternately, so
+//     a chunk is staged while the previous chunk's store still reads its
+//     buffer; for bf16 outputs [stage0 2K | stage1 2K | aux0 2K | aux1 2K]
+//     with the aux blocks streamed two chunks ahead, for fp32 outputs
+//     [stage0 4K | stage1 4K].
 constexpr int STAGE_SLOT = 4096;
+constexpr int STAGE_SLOT_WIDE = 8192;
+template <bool WIDE> struct Slot {
+  static constexpr int BYTES = WIDE ? STAGE_SLOT_WIDE : STAGE_SLOT;
+};
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -325,6 +336,7 @@ __device__ __forceinline__ void tma_store_add_3d(const CUtensorMap* m, const voi
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // bf16 rows are 64 B: SWIZZLE_64B puts 16-byte chunk c of row r at c ^ ((r >> 1) & 3)
@@ -347,11 +359,16 @@ __device__ __forceinline__ void stage_f32(uint8_t* slot, const float (&v)[32], i
     *reinterpret_cast<float4*>(slot + lane * 128 + ((c ^ (lane & 7)) << 4)) =
         make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
 }
-// warp-collective: stage one chunk and bulk-store it at (n0, row0)
+// warp-collective: stage one chunk and bulk-store it at (n0, row0).
+// `alt`: the buffer was last used two stores ago (wide slots), so only the
+// older of the (at most two) outstanding stores must have read it out.
 template <bool BF16>
 __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap* map, const float (&v)[32], int lane,
-                                               int n0, int row0, int bidx, bool add = false) {
-  if (lane == 0) bulk_wait_read0();  // the slot's previous store has been read out
+                                               int n0, int row0, int bidx, bool add = false, bool alt = false) {
+  if (lane == 0) {
+    if (alt) bulk_wait_read1();
+    else bulk_wait_read0();  // the slot's previous store has been read out
+  }
   __syncwarp();
   if (BF16) stage_bf16(slot, v, lane);
   else stage_f32(slot, v, lane);
@@ -387,13 +404,24 @@ __device__ __forceinline__ void aux_read(const uint8_t* slot, float (&h)[32], in
   }
 }
 
+// Wide slots: aux buffer b of the warp's slot, addressed like the narrow
+// layout's (slot + AUX_OFF), so aux_issue / aux_read take the returned base.
+__device__ __forceinline__ uint8_t* aux_base_wide(uint8_t* slot, int b) { return slot + 4096 + 2048 * b - AUX_OFF; }
+// Wide slots: staging buffer b of the warp's slot.
+template <bool BF16>
+__device__ __forceinline__ uint8_t* stage_buf(uint8_t* slot, int b) {
+  return slot + b * (BF16 ? 2048 : 4096);
+}
+
 // One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
+template <bool WIDE = false>
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
                                           bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
                                           const float (&hs)[32], uint8_t* slot, bool radd,
-                                          const CUtensorMap* map_lp, const CUtensorMap* map_f32) {
+                                          const CUtensorMap* map_lp, const CUtensorMap* map_f32,
+                                          int* next_buf = nullptr) {
   SG_CPROF_START();
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -447,22 +475,30 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   }
   SG_CPROF(2);  // epilogue math
   const int row0 = m - lane;
+  // wide slots alternate the two buffers from store to store (*next_buf: the
+  // one not holding the newest outstanding store) -- unless the chunk stores
+  // twice (fp32 and bf16 through TMA): those serialise on buffer 0
+  const bool alt = WIDE && !(e.out_f32 && p.tma_f32 && e.out_bf16 && p.tma_lp);
+  const int nb = WIDE ? *next_buf : 0;
+  uint8_t* sbuf32 = alt ? stage_buf<false>(slot, nb) : slot;
+  uint8_t* sbuf16 = alt ? stage_buf<true>(slot, nb) : slot;
+  if (WIDE && ((e.out_f32 && p.tma_f32) || (e.out_bf16 && p.tma_lp))) *next_buf = alt ? nb ^ 1 : 1;
   if (e.out_f32) {
     if (radd) {  // split tail tile: add this K-half into the zeroed output (two terms: order-free)
-      if (p.tma_f32) warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx, true);
+      if (p.tma_f32) warp_tma_store<false>(sbuf32, map_f32, v, lane, n0, row0, bidx, true, alt);
       else if (row_ok) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (i < nn) atomicAdd(e.out_f32 + (long long)m * e.ld_f32 + n0 + i, v[i]);
       }
     } else if (p.tma_f32) {
-      warp_tma_store<false>(slot, map_f32, v, lane, n0, row0, bidx);
+      warp_tma_store<false>(sbuf32, map_f32, v, lane, n0, row0, bidx, false, alt);
     } else if (row_ok) {
       store_row_f32(e.out_f32 + bidx * p.so_f32 + (long long)m * e.ld_f32 + n0, v, nn);
     }
   }
   if (e.out_bf16) {
-    if (p.tma_lp) warp_tma_store<true>(slot, map_lp, v, lane, n0, row0, bidx);
+    if (p.tma_lp) warp_tma_store<true>(sbuf16, map_lp, v, lane, n0, row0, bidx, false, alt);
     else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
   }
   SG_CPROF(3);  // stores issued
@@ -532,6 +568,55 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
       : "memory");
 }
 
+
+// ----------------------------------------------- pair-tile epilogue loop
+// The chunks of one 256-wide pair tile for epilogue warp (q, half): TMEM ->
+// epi_chunk, with the ACT_GRAD saved-activation blocks streamed by TMA one
+// (narrow slots) or two (wide slots) chunks ahead.  epi_aux_prologue issues
+// the first block(s) before the accumulator wait; aux_phase holds one
+// parity bit per aux buffer.
+template <bool WIDE>
+__device__ __forceinline__ void epi_aux_prologue(bool staged, int lane, uint8_t* slot, const CUtensorMap* map_aux,
+                                                 uint64_t* aux_bars, int n_first, int nch, int N, int row0) {
+  if (!staged || lane != 0) return;
+  if (n_first < N) aux_issue(WIDE ? aux_base_wide(slot, 0) : slot, map_aux, &aux_bars[0], n_first, row0);
+  if (WIDE && nch > 1 && n_first + 32 < N) aux_issue(aux_base_wide(slot, 1), map_aux, &aux_bars[1], n_first + 32, row0);
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void epi_chunks(const KParams& p, uint32_t tmem_row, int n_first, int c_first, int nch,
+                                           int row0, int lane, int split, int bidx, bool radd, uint8_t* slot,
+                                           bool staged, const CUtensorMap* map_aux, uint64_t* aux_bars,
+                                           uint32_t& aux_phase, const CUtensorMap* map_lp,
+                                           const CUtensorMap* map_f32, int& next_buf) {
+  const int m = row0 + lane;
+  const bool row_ok = m < p.M;
+#pragma unroll 1
+  for (int j = 0; j < nch; ++j) {
+    const int n0 = n_first + j * 32;
+    float v[32];
+    SG_CPROF_START();
+    tmem_ld32(tmem_row + (c_first + j) * 32, v);
+    SG_CPROF(0);  // TMEM load
+    if (n0 >= p.N) continue;  // warp-uniform; later chunks are past N as well
+    float h[32];
+    if (staged) {
+      const int b = WIDE ? (j & 1) : 0;
+      mbar_wait(&aux_bars[b], (aux_phase >> b) & 1);
+      aux_phase ^= 1u << b;
+      SG_CPROF(1);  // saved activation block arrived
+      uint8_t* base = WIDE ? aux_base_wide(slot, b) : slot;
+      aux_read(base, h, lane);
+      fence_proxy_async();  // our reads precede the next async write of the buffer
+      __syncwarp();
+      const int ahead = WIDE ? 2 : 1;
+      if (lane == 0 && j + ahead < nch && n0 + 32 * ahead < p.N)
+        aux_issue(base, map_aux, &aux_bars[b], n0 + 32 * ahead, row0);
+    }
+    epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, staged, h, slot, radd, map_lp,
+                    map_f32, &next_buf);
+  }
+}
 
 }  // namespace tc
 
