@@ -558,18 +558,27 @@ class ChainEngine:
                           out_lp=None if top else self.H[l + 1], out=self.Zt if top else None)
             fwd.append((d, 1, [("rows", l - 1)] if l > 0 else []))
         pairs = max(1, torch.cuda.get_device_properties(self.P.device).multi_processor_count // 2)
+        # backward order: the dX chain is the critical path (each layer's dZ
+        # feeds the next dX row block by row block); layer l's dW (which only
+        # needs dZ_l) is placed one layer later so it fills the gaps
         bwd, dx_idx = [], {}
-        for l in range(L - 1, -1, -1):
-            dz = self.dz_of(l)
-            if l > 0:
-                act_prev = self.acts[l - 1]
-                d = gemm_desc(dz, self.Ws[l], b_mn=True, epilogue="store" if act_prev == "identity" else "act_grad",
-                              act=act_prev, aux=self.H[l], out_lp=self.dz_of(l - 1), colsum=self.cs_of(l - 1))
-                bwd.append((d, 1, [("rows", dx_idx[l + 1])] if l + 1 in dx_idx else []))
-                dx_idx[l] = len(bwd) - 1
-            d = gemm_desc(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l])
+
+        def add_dw(l):
+            d = gemm_desc(self.dz_of(l), self.H[l], a_mn=True, b_mn=True, out=self.gW[l])
             bwd.append((d, _pair_splits(self.sizes[l + 1], self.sizes[l], B, pairs),
                         [("krows", dx_idx[l + 1])] if l + 1 in dx_idx else []))
+
+        for l in range(L - 1, -1, -1):
+            if l > 0:
+                act_prev = self.acts[l - 1]
+                d = gemm_desc(self.dz_of(l), self.Ws[l], b_mn=True,
+                              epilogue="store" if act_prev == "identity" else "act_grad", act=act_prev,
+                              aux=self.H[l], out_lp=self.dz_of(l - 1), colsum=self.cs_of(l - 1))
+                bwd.append((d, 1, [("rows", dx_idx[l + 1])] if l + 1 in dx_idx else []))
+                dx_idx[l] = len(bwd) - 1
+            if l + 1 < L:
+                add_dw(l + 1)
+        add_dw(0)
         return GemmChain(fwd), GemmChain(bwd)
 
     def _chain_backward(self, _ctx):

@@ -57,12 +57,18 @@ def _ptr(t):
 
 
 def _ld(t):
+    """Row stride (elements) of a 2-D operand with unit column stride.  A
+    size-1 dimension's stride is arbitrary in torch: one column needs no
+    column stride, and one row takes at least its own width."""
     if t is None:
         return 0
-    if t.dim() == 2 and t.is_contiguous():  # also covers size-1 dims with arbitrary strides
-        return t.shape[1]
-    if t.dim() != 2 or t.stride(1) != 1:
+    if t.dim() != 2:
         raise ValueError("gemm operands must be 2-D with unit column stride")
+    rows, cols = t.shape
+    if cols != 1 and t.stride(1) != 1:
+        raise ValueError("gemm operands must be 2-D with unit column stride")
+    if rows == 1:
+        return max(cols, t.stride(0))
     return t.stride(0)
 
 

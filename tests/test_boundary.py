@@ -203,3 +203,18 @@ def test_bindings_reject_wrong_dtypes_and_shapes_before_any_launch():
     d64 = dense_desc(A.double(), B.double(), torch.zeros(48, dtype=f64), "tanh", "strict_fp64")
     with pytest.raises(ValueError, match="dZ must be"):
         dense_backward(d64, dZ.float(), torch.zeros((48, 32), dtype=f64), torch.zeros(48, dtype=f64))
+
+
+def test_leading_dimension_of_size_one_views():
+    """gemm's row stride of views with a size-1 dimension (torch reports them
+    contiguous whatever their strides): a one-column slice of a padded buffer
+    keeps the buffer's row stride."""
+    import torch
+
+    from paper_1811_01457_b200.gemm import _ld
+
+    buf = torch.zeros((6, 8))
+    assert _ld(buf[:, :1]) == 8
+    assert _ld(buf[:1, :]) == 8
+    assert _ld(buf[:, :5]) == 8
+    assert _ld(torch.zeros((1, 24))) == 24
