@@ -15,6 +15,7 @@
 
 namespace sg {
 int ctx_activate(sg_ctx* ctx);
+int ctx_compute_sms(sg_ctx* ctx);
 int colsum_partials(const void* x, int dtype, long long ld, long long M, long long N, float* part, long long ldp,
                     cudaStream_t st);
 }  // namespace sg
@@ -114,15 +115,27 @@ int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* 
   g.epilogue = SG_EPI_STORE;
   g.out = gr->dW;
   g.ld_out = gr->ld_dw;
-  if ((rc = sg_gemm(ctx, &g, stream))) return rc;
-
   // db = reduce_like(dZ, (fan_out,))   (rules.py:45-46)
   const long long G = (d->batch + 31) / 32;
+  if (tc && gr->colsum_in) {
+    // the dW GEMM finalises db from the producer-fused partial sums as its
+    // tail job (one launch for dW and db; k_colsum_finalize's arithmetic)
+    if (d->fan_in <= 0 || g.K <= 0) return fail(SG_EINVAL, "dense: empty dW");
+    GemmArgs ga{};
+    gemm_args_from_desc(ctx, &g, ga);
+    ga.fin.part = gr->colsum_in;
+    ga.fin.G = G;
+    ga.fin.ld = gr->ld_colsum_in;
+    ga.fin.N = d->fan_out;
+    ga.fin.out = (float*)gr->db;
+    if ((rc = launch_gemm_tc(ga, d->precision == SG_PREC_TF32, ctx_compute_sms(ctx), st))) return rc;
+  } else if ((rc = sg_gemm(ctx, &g, stream))) {
+    return rc;
+  }
   if (!tc) {
     if ((rc = sg_colsum_strict(ctx, gr->dZ, adt, gr->ld_dz, d->batch, d->fan_out, gr->db, stream))) return rc;
   } else if (gr->colsum_in) {
-    if ((rc = sg_colsum_finalize(ctx, gr->colsum_in, G, gr->ld_colsum_in, d->fan_out, (float*)gr->db, stream)))
-      return rc;
+    // finalised by the dW GEMM above
   } else {
     const long long ldp = (d->fan_out + 3) / 4 * 4;
     float* part = nullptr;

@@ -657,6 +657,13 @@ inline bool fdt(int d) { return d == SG_F32 || d == SG_F64; }
 }  // namespace
 
 namespace sg {
+int colsum_finalize_launch(const float* part, long long G, long long ld, long long N, float* out, int,
+                           cudaStream_t st) {
+  if (N <= 0) return SG_OK;
+  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 1024, 0, st>>>(part, G, ld, N, out);
+  SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
 // stage 1 of a bias gradient for an already materialised dZ (bf16 / f32)
 int colsum_partials(const void* x, int dtype, long long ld, long long M, long long N, float* part, long long ldp,
                     cudaStream_t st) {

@@ -44,6 +44,14 @@ __device__ __forceinline__ void warp_colsum_store(float (&v)[32], float* dst, in
   if (lane < n) dst[lane] = v[0];
 }
 
+// Optional bias-gradient finalize a GEMM runs as its tail job:
+// out[j] = sum_g part[g][j], g < G, j < N (k_colsum_finalize's arithmetic).
+struct FinalizeJob {
+  const float* part = nullptr;
+  long long G = 0, ld = 0, N = 0;
+  float* out = nullptr;
+};
+
 struct GemmArgs {
   int M, N, K;
   const void* A;  // bf16, or fp32 with tf32 (operands read as TF32 by the tensor cores)
@@ -56,9 +64,14 @@ struct GemmArgs {
   int batch = 1;             // independent GEMMs (bmm lanes)
   long long sa = 0, sb = 0;  // operand batch strides (elements)
   long long so_f32 = 0, so_lp = 0;  // output batch strides (elements)
+  FinalizeJob fin;            // run after the tiles (CTA-pair kernels) or as its own launch
 };
 
 int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st);
+// sg_gemm_desc -> GemmArgs of the tensor-core kernels (validated by sg_gemm)
+void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g);
+int colsum_finalize_launch(const float* part, long long G, long long ld, long long N, float* out, int num_sms,
+                           cudaStream_t st);
 
 namespace strict {
 struct StrictArgs {

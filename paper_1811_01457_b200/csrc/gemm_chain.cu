@@ -133,56 +133,12 @@ __device__ __forceinline__ void signal_rows(const Params& P, const Problem& pr, 
   }
 }
 
-// Split-K: this warp stored its 32 x (CH_PER*32) fp32 partial of split `split`;
-// the last of the tile's splits to arrive for this region sums all of them in
-// ascending split order (as k_splitk_reduce does) and writes the output.
+// Split-K: the last split to arrive for a region finishes it (split_region_fixup)
+// and publishes the finished rows to dependents.
 __device__ __forceinline__ void split_fixup(const Params& P, const Problem& pr, const Unit& un, int slot_id,
                                             int row0, int n_first, int chunks, int lane) {
-  const KParams& p = pr.p;
-  __syncwarp();
-  unsigned last = 0;
-  if (lane == 0) {
-    unsigned* c = P.split_cnt + pr.split_off + (un.mb * pr.n_tiles + un.nb) * SLOTS + slot_id;
-    const unsigned old = atom_acq_rel(c, 1u);
-    last = old == (unsigned)(p.splits - 1);
-    if (last) *c = 0;  // every split of this region has arrived: reset for the next launch
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-  const int m = row0 + lane;
-  const bool row_ok = m < p.M;
-  for (int c = 0; c < chunks; ++c) {
-    const int n0 = n_first + c * 32;
-    if (n0 >= p.N) break;
-    const int nn = min(32, p.N - n0);
-    float acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-    if (row_ok) {
-      for (int s = 0; s < p.splits; ++s) {
-        const float* src = p.part + ((long long)s * p.M + m) * p.ld_part + n0;
-        if (nn == 32) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
-            if (s == 0) {
-              acc[i] = f.x, acc[i + 1] = f.y, acc[i + 2] = f.z, acc[i + 3] = f.w;
-            } else {
-              acc[i] += f.x, acc[i + 1] += f.y, acc[i + 2] += f.z, acc[i + 3] += f.w;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nn) acc[i] = s == 0 ? __ldcg(src + i) : acc[i] + __ldcg(src + i);
-        }
-      }
-      const GemmEpilogue& e = p.epi;
-      if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, acc, nn);
-      if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, acc, nn);
-    }
-  }
+  unsigned* c = P.split_cnt + pr.split_off + (un.mb * pr.n_tiles + un.nb) * SLOTS + slot_id;
+  if (!split_region_fixup(pr.p, c, row0, n_first, chunks, lane)) return;
   if (pr.signal) {
     __syncwarp();
     if (lane == 0) {

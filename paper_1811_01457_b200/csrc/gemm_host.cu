@@ -33,35 +33,7 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
     if (d->K == 0) return fail(SG_EINVAL, "gemm: K must be positive");
     if (tf32 && d->out_lp) return fail(SG_EINVAL, "gemm: out_lp is a BF16-precision output");
     GemmArgs g{};
-    g.M = (int)d->M;
-    g.N = (int)d->N;
-    g.K = (int)d->K;
-    g.A = d->A;
-    g.lda = d->lda;
-    g.a_mn = d->a_mn_major != 0;
-    g.B = d->B;
-    g.ldb = d->ldb;
-    g.b_mn = d->b_mn_major != 0;
-    g.epi.mode = d->epilogue;
-    g.epi.act = d->act;
-    g.epi.bias = (const float*)d->bias;
-    g.epi.aux = tf32 ? nullptr : (const __nv_bfloat16*)d->aux;
-    g.epi.aux_f32 = tf32 ? (const float*)d->aux : nullptr;
-    g.epi.ld_aux = d->ld_aux;
-    g.epi.out_pre = (float*)d->out_pre;
-    g.epi.ld_pre = d->ld_pre;
-    g.epi.out_f32 = (float*)d->out;
-    g.epi.ld_f32 = d->ld_out;
-    g.epi.out_bf16 = (__nv_bfloat16*)d->out_lp;
-    g.epi.ld_bf16 = d->ld_lp;
-    g.epi.colsum = d->colsum;
-    g.epi.ld_colsum = d->ld_colsum;
-    g.epi.dom = ctx_domain_word(ctx);
-    g.batch = (int)batch;
-    g.sa = d->stride_a;
-    g.sb = d->stride_b;
-    g.so_f32 = d->stride_out;
-    g.so_lp = d->stride_lp;
+    gemm_args_from_desc(ctx, d, g);
     return launch_gemm_tc(g, tf32, ctx_compute_sms(ctx), st);
   }
   if (d->precision == SG_PREC_STRICT_FP32 || d->precision == SG_PREC_STRICT_FP64) {
@@ -74,3 +46,39 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
   }
   return fail(SG_EINVAL, "gemm: unknown precision");
 }
+
+namespace sg {
+void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g) {
+  const bool tf32 = d->precision == SG_PREC_TF32;
+  const long long batch = d->batch < 1 ? 1 : d->batch;
+  g.M = (int)d->M;
+  g.N = (int)d->N;
+  g.K = (int)d->K;
+  g.A = d->A;
+  g.lda = d->lda;
+  g.a_mn = d->a_mn_major != 0;
+  g.B = d->B;
+  g.ldb = d->ldb;
+  g.b_mn = d->b_mn_major != 0;
+  g.epi.mode = d->epilogue;
+  g.epi.act = d->act;
+  g.epi.bias = (const float*)d->bias;
+  g.epi.aux = tf32 ? nullptr : (const __nv_bfloat16*)d->aux;
+  g.epi.aux_f32 = tf32 ? (const float*)d->aux : nullptr;
+  g.epi.ld_aux = d->ld_aux;
+  g.epi.out_pre = (float*)d->out_pre;
+  g.epi.ld_pre = d->ld_pre;
+  g.epi.out_f32 = (float*)d->out;
+  g.epi.ld_f32 = d->ld_out;
+  g.epi.out_bf16 = (__nv_bfloat16*)d->out_lp;
+  g.epi.ld_bf16 = d->ld_lp;
+  g.epi.colsum = d->colsum;
+  g.epi.ld_colsum = d->ld_colsum;
+  g.epi.dom = ctx_domain_word(ctx);
+  g.batch = (int)batch;
+  g.sa = d->stride_a;
+  g.sb = d->stride_b;
+  g.so_f32 = d->stride_out;
+  g.so_lp = d->stride_lp;
+}
+}  // namespace sg

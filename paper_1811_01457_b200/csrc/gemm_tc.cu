@@ -442,6 +442,11 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
+      if (p.splits > 1 && p.split_cnt) {  // in-kernel split-K fix-up of this warp's region of the tile
+        const int tile = (tc.m0 / PM) * n_tiles + tc.n0 / BN;
+        split_region_fixup(p, p.split_cnt + tile * (2 * EPI_WARPS) + (int)rank * EPI_WARPS + ew, row0,
+                           tc.n0 + c0 * 32, CH_PER, lane);
+      }
       if (lane == 0 && ew == 0) SG_TRACE(it, 2);  // epilogue warp 0 done with the tile
       if (lane == 0 && ew == EPI_WARPS - 1) SG_TRACE(it, 3);  // last epilogue warp done
       if (++acc == 2) {
@@ -449,6 +454,13 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
         acc_phase ^= 1;
       }
     }
+  }
+  if (warp >= EPI_WARP0 && p.fin_out) {
+    // bias-gradient finalize as the epilogue's tail job, in warp 0's staging slot
+    if (lane == 0) bulk_wait_read0();
+    epi_bar();
+    colsum_finalize_tail(p, reinterpret_cast<double*>(stage_slots), threadIdx.x - EPI_WARP0 * 32, blockIdx.x,
+                         gridDim.x);
   }
   if (warp >= EPI_WARP0 && lane == 0) bulk_wait0();  // staged stores drained before smem goes away
   tc_fence_before();
@@ -697,6 +709,8 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
   }
+  // the 1-SM kernels run a requested bias-gradient finalize as its own launch
+  if (g.fin.out) return colsum_finalize_launch(g.fin.part, g.fin.G, g.fin.ld, g.fin.N, g.fin.out, num_sms, st);
   return SG_OK;
 }
 
@@ -741,10 +755,23 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   out_maps(g, p, mlp, mf32);
   aux_map(g, p, maux);
   float* part = nullptr;
+  unsigned* cnt = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
     SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
     p.part = part;
+    // the last split of each tile region sums the partials inside the kernel
+    const size_t ncnt = (size_t)tiles * 2 * tc::EPI_WARPS;
+    SG_CUDA_TRY(cudaMallocAsync((void**)&cnt, ncnt * sizeof(unsigned), st));
+    SG_CUDA_TRY(cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned), st));
+    p.split_cnt = cnt;
+  }
+  if (g.fin.out) {
+    p.fin_part = g.fin.part;
+    p.fin_G = g.fin.G;
+    p.fin_ld = g.fin.ld;
+    p.fin_N = g.fin.N;
+    p.fin_out = g.fin.out;
   }
   int work = tiles * splits;
   // Split tail: when the last wave of pair tiles would run mostly empty (e.g. a
@@ -771,8 +798,8 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
-    if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
+    SG_CUDA_TRY(cudaFreeAsync(cnt, st));
   }
   return SG_OK;
 }

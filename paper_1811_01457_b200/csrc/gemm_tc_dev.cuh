@@ -301,6 +301,15 @@ struct KParams {
   int tail_full;        //   computed as two K-halves each, reduce-added into the zeroed fp32 output
   int batch;            // independent GEMMs (bmm lanes), >= 1
   long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
+  // CTA-pair kernel, splits > 1: per (tile, epilogue-warp region) arrival
+  // counters (zeroed) -- the last split to arrive sums the partials in split
+  // order and writes the output (no separate reduce launch)
+  unsigned* split_cnt = nullptr;
+  // optional bias-gradient finalize run by the epilogue warps after their
+  // tiles: fin_out[j] = sum_g fin_part[g][j] (the k_colsum_finalize order)
+  const float* fin_part = nullptr;
+  long long fin_G = 0, fin_ld = 0, fin_N = 0;
+  float* fin_out = nullptr;
 };
 
 // ----------------------------------------------------- TMA-store epilogue
@@ -568,6 +577,91 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
       : "memory");
 }
 
+
+// ------------------------------------------- split-K fix-up and finalize
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+// Split-K: this epilogue warp stored its 32 x (chunks*32) fp32 partial of one
+// split of a tile; the last of the tile's splits to arrive for this region
+// sums all of them in ascending split order (k_splitk_reduce's order) and
+// writes the output.  `counter` is the region's arrival counter (reset here
+// by the last arriver).  Returns whether this warp finished the region.
+__device__ __forceinline__ bool split_region_fixup(const KParams& p, unsigned* counter, int row0, int n_first,
+                                                   int chunks, int lane) {
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) {
+    const unsigned old = atom_add_acq_rel_gpu(counter, 1u);
+    last = old == (unsigned)(p.splits - 1);
+    if (last) *counter = 0;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  __threadfence();
+  const int m = row0 + lane;
+  if (m < p.M) {
+    for (int c = 0; c < chunks; ++c) {
+      const int n0 = n_first + c * 32;
+      if (n0 >= p.N) break;
+      const int nn = min(32, p.N - n0);
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+      for (int s = 0; s < p.splits; ++s) {
+        const float* src = p.part + ((long long)s * p.M + m) * p.ld_part + n0;
+        if (nn == 32) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
+            if (s == 0) {
+              acc[i] = f.x, acc[i + 1] = f.y, acc[i + 2] = f.z, acc[i + 3] = f.w;
+            } else {
+              acc[i] += f.x, acc[i + 1] += f.y, acc[i + 2] += f.z, acc[i + 3] += f.w;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nn) acc[i] = s == 0 ? __ldcg(src + i) : acc[i] + __ldcg(src + i);
+        }
+      }
+      const GemmEpilogue& e = p.epi;
+      if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, acc, nn);
+      if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, acc, nn);
+    }
+  }
+  return true;
+}
+
+// Bias-gradient finalize as the epilogue warps' tail job (after their tiles):
+// columns j = cta, cta + ctas, ...; for each, 128 threads fold the partial
+// rows g = t, t + 128, ... in fp64 and a fixed tree combines them -- the
+// arithmetic of k_colsum_finalize, so the result is bit-identical to it.
+// `red` is 2 x 128 doubles of shared memory only the epilogue warps use
+// (tid = 0..255 over the 8 epilogue warps; named barrier 1).
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void colsum_finalize_tail(const KParams& p, double* red, int tid, int cta, int ctas) {
+  const int half = tid >> 7, t = tid & 127;
+  for (long long j0 = (long long)cta * 2; j0 < p.fin_N; j0 += 2ll * ctas) {
+    const long long j = j0 + half;
+    double acc = 0.0;
+    if (j < p.fin_N) {
+#pragma unroll 4
+      for (long long g = t; g < p.fin_G; g += 128) acc += (double)p.fin_part[g * p.fin_ld + j];
+    }
+    red[half * 128 + t] = acc;
+    epi_bar();
+    for (int s = 64; s > 0; s >>= 1) {
+      if (t < s) red[half * 128 + t] += red[half * 128 + t + s];
+      epi_bar();
+    }
+    if (t == 0 && j < p.fin_N) p.fin_out[j] = (float)red[half * 128];
+    epi_bar();
+  }
+}
 
 // ----------------------------------------------- pair-tile epilogue loop
 // The chunks of one 256-wide pair tile for epilogue warp (q, half): TMEM ->

@@ -442,8 +442,12 @@ class ChainEngine:
         # ping-pong: a chained dX may run while an earlier layer's dW still
         # reads the dZ it would overwrite).  bf16 only; off under data
         # parallelism (buckets are all-reduced per layer as the pullback goes).
+        # Opt-in (SGB200_CHAIN=1 or gemm_chain=True): bit-identical to the
+        # per-layer path but, measured on B200, not yet faster:
+        # a chained unit's epilogue also waits for its TMA stores to land and
+        # publishes them, and that is on the critical path at K = 1024.
         if gemm_chain is None:
-            gemm_chain = os.environ.get("SGB200_CHAIN", "1") != "0"
+            gemm_chain = os.environ.get("SGB200_CHAIN", "0") == "1"
         self.chainable = bool(gemm_chain) and precision == "bf16" and self.L >= 2
         self.chains = None
         if self.chainable:

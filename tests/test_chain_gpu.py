@@ -115,7 +115,7 @@ def test_chained_training_run_matches_layer_path():
             chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(4)]).init_params(
                 np.random.default_rng(1))
             tr = Trainer(chain, B, loss="mse", lr=1e-3, precision="bf16", graph=True)
-            assert tr.engine.chainable == use
+            assert tr.engine.chainable == use  # SGB200_CHAIN=1 opts in
             losses = [float(tr.step(X, Y).item()) for _ in range(6)]
             runs[use] = (losses, tr.engine.P.clone())
         finally:
