@@ -10,6 +10,8 @@
 // fused into the epilogue.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.h"
 #include "gemm.h"
 
@@ -117,7 +119,14 @@ int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* 
   g.ld_out = gr->ld_dw;
   // db = reduce_like(dZ, (fan_out,))   (rules.py:45-46)
   const long long G = (d->batch + 31) / 32;
-  if (tc && gr->colsum_in) {
+  // db finalised as the dW GEMM's tail job (SGB200_DENSE_FUSED_DB=1): one
+  // launch fewer per layer but measured slower (c5 step +0.1..0.15 ms: the
+  // tail runs after every CTA's tiles); default: its own full-width launch.
+  static const bool fused_db = [] {
+    const char* e = std::getenv("SGB200_DENSE_FUSED_DB");
+    return e && e[0] == '1';
+  }();
+  if (tc && gr->colsum_in && fused_db) {
     // the dW GEMM finalises db from the producer-fused partial sums as its
     // tail job (one launch for dW and db; k_colsum_finalize's arithmetic)
     if (d->fan_in <= 0 || g.K <= 0) return fail(SG_EINVAL, "dense: empty dW");
@@ -135,7 +144,9 @@ int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* 
   if (!tc) {
     if ((rc = sg_colsum_strict(ctx, gr->dZ, adt, gr->ld_dz, d->batch, d->fan_out, gr->db, stream))) return rc;
   } else if (gr->colsum_in) {
-    // finalised by the dW GEMM above
+    if (!fused_db &&
+        (rc = sg_colsum_finalize(ctx, gr->colsum_in, G, gr->ld_colsum_in, d->fan_out, (float*)gr->db, stream)))
+      return rc;
   } else {
     const long long ldp = (d->fan_out + 3) / 4 * 4;
     float* part = nullptr;

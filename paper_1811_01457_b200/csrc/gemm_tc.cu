@@ -756,15 +756,24 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   aux_map(g, p, maux);
   float* part = nullptr;
   unsigned* cnt = nullptr;
+  // In-kernel split-K fix-up (SGB200_GEMM_SPLIT_FIXUP=1): measured slower on
+  // B200 than the separate ordered reduce (c5 step 3.54 vs 3.16 ms): the last
+  // split's reduction lengthens every dW kernel's tail, while k_splitk_reduce
+  // runs at full width.  The persistent chain kernel uses it (no launches).
+  static const bool fixup = [] {
+    const char* e = std::getenv("SGB200_GEMM_SPLIT_FIXUP");
+    return e && e[0] == '1';
+  }();
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
     SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
     p.part = part;
-    // the last split of each tile region sums the partials inside the kernel
-    const size_t ncnt = (size_t)tiles * 2 * tc::EPI_WARPS;
-    SG_CUDA_TRY(cudaMallocAsync((void**)&cnt, ncnt * sizeof(unsigned), st));
-    SG_CUDA_TRY(cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned), st));
-    p.split_cnt = cnt;
+    if (fixup) {  // the last split of each tile region sums the partials inside the kernel
+      const size_t ncnt = (size_t)tiles * 2 * tc::EPI_WARPS;
+      SG_CUDA_TRY(cudaMallocAsync((void**)&cnt, ncnt * sizeof(unsigned), st));
+      SG_CUDA_TRY(cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned), st));
+      p.split_cnt = cnt;
+    }
   }
   if (g.fin.out) {
     p.fin_part = g.fin.part;
@@ -798,8 +807,10 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
+    if (!cnt)
+      if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
-    SG_CUDA_TRY(cudaFreeAsync(cnt, st));
+    if (cnt) SG_CUDA_TRY(cudaFreeAsync(cnt, st));
   }
   return SG_OK;
 }
@@ -827,9 +838,11 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
     const char* e = std::getenv("SGB200_GEMM_PAIR");
     return !(e && e[0] == '0');
   }();
+  // Wide epilogue slots (SGB200_GEMM_WIDE=1): -2..3 % per c5 GEMM alone but
+  // neutral to slightly slower over the c5 step (one operand stage fewer).
   static const bool wide = [] {
     const char* e = std::getenv("SGB200_GEMM_WIDE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
     if (wide) {

@@ -601,36 +601,50 @@ __device__ __forceinline__ bool split_region_fixup(const KParams& p, unsigned* c
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return false;
   __threadfence();
-  const int m = row0 + lane;
-  if (m < p.M) {
-    for (int c = 0; c < chunks; ++c) {
-      const int n0 = n_first + c * 32;
-      if (n0 >= p.N) break;
-      const int nn = min(32, p.N - n0);
-      float acc[32];
+  // rows of the region one at a time, the warp's lanes across its columns
+  // (4 per lane, coalesced 16-byte loads); every split's partial of a row is
+  // loaded before it is summed in ascending split order
+  const GemmEpilogue& e = p.epi;
+  const int n = n_first + lane * 4;
+  const int nn = min(4, p.N - n);
+  const int cols = chunks * 32;
+  if (lane * 4 >= cols || nn <= 0) return true;
+  const bool vec_out = e.out_f32 && (reinterpret_cast<uintptr_t>(e.out_f32) & 15) == 0 && (e.ld_f32 & 3) == 0;
+  constexpr int R = 4;
+  for (int r0 = 0; r0 < 32; r0 += R) {
+    float4 acc[R];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-      for (int s = 0; s < p.splits; ++s) {
-        const float* src = p.part + ((long long)s * p.M + m) * p.ld_part + n0;
-        if (nn == 32) {
+    for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < p.splits; ++s) {
+      float4 f[R];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
-            if (s == 0) {
-              acc[i] = f.x, acc[i + 1] = f.y, acc[i + 2] = f.z, acc[i + 3] = f.w;
-            } else {
-              acc[i] += f.x, acc[i + 1] += f.y, acc[i + 2] += f.z, acc[i + 3] += f.w;
-            }
-          }
+      for (int r = 0; r < R; ++r) {
+        const int m = row0 + r0 + r;
+        f[r] = m < p.M ? __ldcg(reinterpret_cast<const float4*>(p.part + ((long long)s * p.M + m) * p.ld_part + n))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (s == 0) {
+          acc[r] = f[r];
         } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nn) acc[i] = s == 0 ? __ldcg(src + i) : acc[i] + __ldcg(src + i);
+          acc[r].x += f[r].x, acc[r].y += f[r].y, acc[r].z += f[r].z, acc[r].w += f[r].w;
         }
       }
-      const GemmEpilogue& e = p.epi;
-      if (e.out_f32) store_row_f32(e.out_f32 + (long long)m * e.ld_f32 + n0, acc, nn);
-      if (e.out_bf16) store_row_bf16(e.out_bf16 + (long long)m * e.ld_bf16 + n0, acc, nn);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = row0 + r0 + r;
+      if (m >= p.M) break;
+      const float a[4] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
+      if (e.out_f32) {
+        float* dst = e.out_f32 + (long long)m * e.ld_f32 + n;
+        if (nn == 4 && vec_out) *reinterpret_cast<float4*>(dst) = acc[r];
+        else
+          for (int i = 0; i < nn; ++i) dst[i] = a[i];
+      }
+      if (e.out_bf16)
+        for (int i = 0; i < nn; ++i) e.out_bf16[(long long)m * e.ld_bf16 + n + i] = __float2bfloat16_rn(a[i]);
     }
   }
   return true;

@@ -453,3 +453,41 @@ def test_domain_errors_match_reference(case, precision):
                 tr.check()
         else:
             tr.check()
+
+
+@pytest.mark.parametrize("knobs", [
+    {"SGB200_GEMM_SPLIT_FIXUP": "1"}, {"SGB200_DENSE_FUSED_DB": "1"}, {"SGB200_GEMM_WIDE": "1"},
+])
+def test_opt_in_gemm_variants_are_bit_identical(knobs):
+    """The opt-in kernel variants -- in-kernel split-K fix-up, bias-gradient
+    finalize fused into the dW GEMM, wide epilogue slots -- compute the same
+    tiles in the same order: a training step is bit-identical to the default
+    path.  (Run in a subprocess: the knobs are read once per process.)"""
+    import os
+    import subprocess
+    import sys
+
+    code = """
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+from paper_1811_01457_b200.dense import Chain, ChainEngine, Dense
+rng = np.random.default_rng(2)
+sizes, acts, B = (512, 768, 512, 256), ('tanh', 'sigmoid', 'identity'), 2048
+chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(3)]).init_params(rng)
+e = ChainEngine(chain, B, 'mse', 'bf16', small=False)
+X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+e.load_batch(X, Y); e.forward(); e.loss_and_seed(); e.pullback()
+torch.cuda.synchronize()
+np.save(sys.argv[1], np.concatenate([e.G.double().cpu().numpy(), e.loss.cpu().numpy()]))
+"""
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for env in ({}, knobs):
+            f = os.path.join(d, f"g{len(outs)}.npy")
+            subprocess.run([sys.executable, "-c", code, f], check=True, env={**os.environ, **env},
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
