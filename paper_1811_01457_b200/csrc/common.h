@@ -28,6 +28,7 @@ struct Driver {
                            unsigned, CUstream, void**, void**);
   CUresult (*getErrorString)(CUresult, const char**);
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+  CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**);  // optional (PDL)
 };
 // Returns nullptr (and sets the error) if the driver cannot be reached.
 const Driver* driver();

@@ -57,6 +57,7 @@ const Driver* driver() {
               get("cuLaunchKernel", (void**)&d.launchKernel) &&
               get("cuGetErrorString", (void**)&d.getErrorString) &&
               get("cuFuncSetAttribute", (void**)&d.funcSetAttribute);
+    if (!get("cuLaunchKernelEx", (void**)&d.launchKernelEx)) d.launchKernelEx = nullptr;
     state = ok ? 1 : 2;
   }
   if (state != 1) {
@@ -566,6 +567,30 @@ int launch(CUfunction f, const Launch& L, SgEwParams& p, cudaStream_t st) {
   void* params[] = {&p};
   const Driver* drv = driver();
   if (!drv) return SG_ECUDA;
+  // programmatic dependent launch: the kernel's prologue and launch overlap the
+  // previous grid's tail (its griddepcontrol.wait orders the memory accesses)
+  static const bool pdl = [] {
+    const char* e = std::getenv("SGB200_EW_PDL");
+    return !(e && e[0] == '0');
+  }();
+  if (pdl && drv->launchKernelEx) {
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = L.gx;
+    cfg.gridDimY = L.gy;
+    cfg.gridDimZ = 1;
+    cfg.blockDimX = L.bdx;
+    cfg.blockDimY = L.bdy;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = 0;
+    cfg.hStream = (CUstream)st;
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SG_CU_TRY(drv->launchKernelEx(&cfg, f, params, nullptr));
+    return SG_OK;
+  }
   SG_CU_TRY(drv->launchKernel(f, L.gx, L.gy, 1, L.bdx, L.bdy, 1, 0, (CUstream)st, params, nullptr));
   return SG_OK;
 }

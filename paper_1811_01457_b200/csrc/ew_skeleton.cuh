@@ -1,3 +1,15 @@
+// Programmatic dependent launch (the runtime launches these kernels with
+// programmatic stream serialisation): wait until the previous grid in the
+// stream has completed and its memory is visible, then let the next grid's
+// CTAs launch as soon as ours leave room (they wait in their own
+// griddepcontrol.wait).  Both are no-ops without the launch attribute.
+#define SG_PDL_BEGIN()                                        \
+  do {                                                        \
+    asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+#define SG_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 // Fused elementwise kernel skeleton (K1 forward, K2 gradient, pack).
 //
 // Compiled at run time by NVRTC together with the code generated from the
@@ -230,6 +242,7 @@ __device__ __forceinline__ void sg_load_elem(const SgEwParams& p, long long r, l
 }
 extern "C" __global__ void __launch_bounds__(256)
 sg_ew_forward(const SgEwParams p) {
+  SG_PDL_WAIT();  // multi-wave grid: no early trigger
   const long long nvec = p.R * p.C / SG_VEC;
   const long long v0 = (long long)blockIdx.x * (256 * SG_UNROLL) + threadIdx.x;
   T* out = reinterpret_cast<T*>(p.out);
@@ -255,6 +268,7 @@ extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_FWD_MINB)
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
 #endif
 sg_ew_forward(const SgEwParams p) {
+  SG_PDL_BEGIN();
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;
@@ -371,6 +385,7 @@ __device__ __forceinline__ void sg_flush_pre(SgGradAcc& acc, T (&pre)[SG_KT][SG_
 
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY, SG_GRAD_MINB)
 sg_ew_grad(const SgEwParams p) {
+  SG_PDL_BEGIN();
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   const bool active = c < p.C;
@@ -535,6 +550,7 @@ sg_ew_grad(const SgEwParams p) {
 // fused_pack layout of interp.py:334-352: pack[0] = primal, pack[1+i] = d f/d arg_i.
 extern "C" __global__ void __launch_bounds__(SG_BDX * SG_BDY)
 sg_ew_pack(const SgEwParams p) {
+  SG_PDL_BEGIN();
   const int tx = threadIdx.x, ty = threadIdx.y;
   const long long c = ((long long)blockIdx.x * SG_BDX + tx) * SG_VEC;
   if (c >= p.C) return;

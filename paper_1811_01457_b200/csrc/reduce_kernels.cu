@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include "common.h"
+#include <cstdlib>
+
 #include "reduce_kernels.h"
 
 namespace sg {
@@ -21,6 +23,8 @@ namespace {
 template <class T>
 __global__ void __launch_bounds__(1024) k_sum_cols(const double* __restrict__ part, long long G, long long N,
                                                    T* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials come from the previous grid (PDL launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double red[32][33];
   const long long j = blockIdx.x * 32ll + threadIdx.x;
   double acc = 0.0;
@@ -42,6 +46,8 @@ __global__ void __launch_bounds__(1024) k_sum_cols(const double* __restrict__ pa
 template <class T>
 __global__ void __launch_bounds__(256) k_sum_block(const double* __restrict__ part, long long G, long long N,
                                                    T* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double red[256];
   for (long long j = blockIdx.x; j < N; j += gridDim.x) {
     double acc = 0.0;
@@ -145,19 +151,38 @@ inline int grid_for(long long n, int block, int cap) {
 
 }  // namespace
 
+template <class Kern, class... Args>
+static cudaError_t launch_pdl_ew(Kern kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("SGB200_EW_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 int launch_sum_partials(const double* part, long long G, long long N, void* out, int dtype,
                         cudaStream_t s) {
   const bool blockwise = N < 256 && G >= 256;
+  const dim3 gb(grid_for(N, 1, 4096)), gc((unsigned)((N + 31) / 32));
   if (dtype == SG_F32) {
     if (blockwise)
-      k_sum_block<float><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (float*)out);
+      SG_CUDA_TRY(launch_pdl_ew(k_sum_block<float>, gb, dim3(256), s, part, G, N, (float*)out));
     else
-      k_sum_cols<float><<<(unsigned)((N + 31) / 32), dim3(32, 32), 0, s>>>(part, G, N, (float*)out);
+      SG_CUDA_TRY(launch_pdl_ew(k_sum_cols<float>, gc, dim3(32, 32), s, part, G, N, (float*)out));
   } else {
     if (blockwise)
-      k_sum_block<double><<<grid_for(N, 1, 4096), 256, 0, s>>>(part, G, N, (double*)out);
+      SG_CUDA_TRY(launch_pdl_ew(k_sum_block<double>, gb, dim3(256), s, part, G, N, (double*)out));
     else
-      k_sum_cols<double><<<(unsigned)((N + 31) / 32), dim3(32, 32), 0, s>>>(part, G, N, (double*)out);
+      SG_CUDA_TRY(launch_pdl_ew(k_sum_cols<double>, gc, dim3(32, 32), s, part, G, N, (double*)out));
   }
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
