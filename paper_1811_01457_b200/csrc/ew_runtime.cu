@@ -809,6 +809,7 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
     pr.p.part[i] = pp;
   }
   if ((rc = launch(v->grad, L, pr.p, st))) return rc;
+  SumJobs jobs;
   for (int i = 0; i < k; ++i) {
     const int kind = s.kinds[i];
     if (kind == SG_FULL) {
@@ -844,8 +845,18 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
     }
     long long G = kind == SG_ROW ? G_row : kind == SG_COL ? G_col : G_blk;
     long long N = kind == SG_ROW ? s.C : kind == SG_COL ? s.R : 1;
-    if ((rc = launch_sum_partials(pr.p.part[i], G, N, argbars[i].ptr, kern->dtype, st))) return rc;
+    if (jobs.n == SUM_JOBS_MAX) {
+      if ((rc = launch_sum_partials_multi(jobs, kern->dtype, st))) return rc;
+      jobs.n = 0;
+    }
+    jobs.part[jobs.n] = pr.p.part[i];
+    jobs.out[jobs.n] = argbars[i].ptr;
+    jobs.G[jobs.n] = G;
+    jobs.N[jobs.n] = N;
+    ++jobs.n;
   }
+  // every broadcast operand's cotangent finalised in one launch
+  if (jobs.n && (rc = launch_sum_partials_multi(jobs, kern->dtype, st))) return rc;
   return release(pr, st);
 }
 

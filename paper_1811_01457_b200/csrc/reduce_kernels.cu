@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "common.h"
+#include <algorithm>
 #include <cstdlib>
 
 #include "reduce_kernels.h"
@@ -39,6 +40,32 @@ __global__ void __launch_bounds__(1024) k_sum_cols(const double* __restrict__ pa
 #pragma unroll
     for (int y = 1; y < 32; ++y) s += red[y][threadIdx.x];
     out[j] = (T)s;
+  }
+}
+
+// k_sum_cols for several jobs (blockIdx.y): identical arithmetic per column.
+template <class T>
+__global__ void __launch_bounds__(1024) k_sum_cols_multi(const __grid_constant__ SumJobs jobs) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ double red[32][33];
+  const int b = blockIdx.y;
+  const long long N = jobs.N[b], G = jobs.G[b];
+  if (blockIdx.x * 32ll >= N) return;  // block-uniform
+  const double* __restrict__ part = jobs.part[b];
+  const long long j = blockIdx.x * 32ll + threadIdx.x;
+  double acc = 0.0;
+  if (j < N) {
+#pragma unroll 4
+    for (long long g = threadIdx.y; g < G; g += 32) acc += part[g * N + j];
+  }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < N) {
+    double s = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 32; ++y) s += red[y][threadIdx.x];
+    reinterpret_cast<T*>(jobs.out[b])[j] = (T)s;
   }
 }
 
@@ -185,6 +212,28 @@ int launch_sum_partials(const double* part, long long G, long long N, void* out,
       SG_CUDA_TRY(launch_pdl_ew(k_sum_cols<double>, gc, dim3(32, 32), s, part, G, N, (double*)out));
   }
   SG_CUDA_TRY(cudaGetLastError());
+  return SG_OK;
+}
+
+int launch_sum_partials_multi(const SumJobs& jobs, int dtype, cudaStream_t s) {
+  SumJobs cols;
+  long long nmax = 1;
+  for (int i = 0; i < jobs.n; ++i) {
+    if (jobs.N[i] < 256 && jobs.G[i] >= 256) {  // full-reduction shape: the blockwise kernel
+      if (int rc = launch_sum_partials(jobs.part[i], jobs.G[i], jobs.N[i], jobs.out[i], dtype, s)) return rc;
+      continue;
+    }
+    cols.part[cols.n] = jobs.part[i];
+    cols.out[cols.n] = jobs.out[i];
+    cols.G[cols.n] = jobs.G[i];
+    cols.N[cols.n] = jobs.N[i];
+    nmax = std::max(nmax, jobs.N[i]);
+    ++cols.n;
+  }
+  if (cols.n == 0) return SG_OK;
+  const dim3 grid((unsigned)((nmax + 31) / 32), (unsigned)cols.n);
+  if (dtype == SG_F32) SG_CUDA_TRY(launch_pdl_ew(k_sum_cols_multi<float>, grid, dim3(32, 32), s, cols));
+  else SG_CUDA_TRY(launch_pdl_ew(k_sum_cols_multi<double>, grid, dim3(32, 32), s, cols));
   return SG_OK;
 }
 
