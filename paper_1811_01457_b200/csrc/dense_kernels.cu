@@ -10,10 +10,41 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <utility>
 #include <string>
 
 #include "common.h"
 #include "gemm.h"
+
+// Programmatic dependent launch for the step's memory-bound kernels (launched
+// through pdl_launch): wait until the previous grid in the stream completed
+// (its writes visible) before touching memory; signal the next grid once this
+// block's work is issued, so its launch and prologue overlap our tail.
+#define SG_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define SG_GRID_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+
+namespace sg {
+template <class... KArgs, class... Args>
+cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("SGB200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace sg
 
 namespace sg {
 namespace dk {
@@ -51,6 +82,7 @@ __global__ void __launch_bounds__(256) k_act_grad(const void* ybar, int yd, long
                                                   long long ldh, long long M, long long N, int act, void* dz,
                                                   int dzd, long long lddz, void* dz2, int dz2d, long long lddz2,
                                                   float* colsum, long long ldc) {
+  SG_GRID_WAIT();
   const long long c = blockIdx.x * 32ll + threadIdx.x;
   const long long g = blockIdx.y * 8ll + threadIdx.y;  // 32-row group
   const long long r0 = g * 32;
@@ -68,6 +100,7 @@ __global__ void __launch_bounds__(256) k_act_grad(const void* ybar, int yd, long
     }
     if (colsum) colsum[g * ldc + c] = (float)acc;
   }
+  SG_GRID_TRIGGER();
 }
 
 // --- vectorised fast paths (fp32 seed/logits, bf16 activations and dZ):
@@ -139,6 +172,7 @@ __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long lon
                                                      long long ldh, long long M, long long N, int act,
                                                      DT* dz, long long lddz, float* colsum,
                                                      long long ldc) {
+  SG_GRID_WAIT();
   const long long c = (blockIdx.x * 64ll + threadIdx.x) * 8;
   const bool ok = c < N;
   const long long g = blockIdx.y, r0 = g * 32 + threadIdx.y * 8;
@@ -159,12 +193,14 @@ __global__ void __launch_bounds__(256) k_act_grad_v8(const float* ybar, long lon
     }
   }
   quarter_colsum(acc, colsum, ldc, g, c, ok);
+  SG_GRID_TRIGGER();
 }
 
 template <class DT>
 __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, const float* y, long long ldy,
                                                 long long M, long long N, float scale, DT* dz,
                                                 long long lddz, float* colsum, long long ldc, double* loss_part) {
+  SG_GRID_WAIT();
   // block (64, 4) as k_act_grad_v8
   __shared__ double red[256];
   const long long c = (blockIdx.x * 64ll + threadIdx.x) * 8;
@@ -200,6 +236,7 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
     __syncthreads();
   }
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+  SG_GRID_TRIGGER();
 }
 
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
@@ -207,6 +244,7 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
 // for narrow layers, each thread folds g = ty, ty+32, ... then a fixed fold over ty.
 __global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
                                                           float* out) {
+  SG_GRID_WAIT();
   constexpr int RG = 128;  // row groups per block (1024 threads = 8 columns x 128)
   __shared__ double red[RG][9];
   const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
@@ -223,6 +261,7 @@ __global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, lon
     __syncthreads();
   }
   if (ty == 0 && j < N) out[j] = (float)red[0][tx];
+  SG_GRID_TRIGGER();
 }
 
 // The same finalize for several bias gradients in one launch (blockIdx.y =
@@ -234,6 +273,7 @@ struct ColsumJobs {
   long long G[MAX_COLSUM_JOBS], ldp[MAX_COLSUM_JOBS], N[MAX_COLSUM_JOBS];
 };
 __global__ void __launch_bounds__(1024) k_colsum_finalize_multi(const __grid_constant__ ColsumJobs jobs) {
+  SG_GRID_WAIT();
   constexpr int RG = 128;
   __shared__ double red[RG][9];
   const int b = blockIdx.y;
@@ -254,29 +294,34 @@ __global__ void __launch_bounds__(1024) k_colsum_finalize_multi(const __grid_con
     __syncthreads();
   }
   if (ty == 0 && j < N) jobs.out[b][j] = (float)red[0][tx];
+  SG_GRID_TRIGGER();
 }
 
 // --- reduce_to over rows in the reference's order: sequential ascending fold
 //     (tensor.py:287-292, 337-338) — STRICT precision bias gradients
 template <class T>
 __global__ void k_colsum_strict(const T* x, long long ld, long long M, long long N, T* out) {
+  SG_GRID_WAIT();
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= N) return;
   T acc = x[j];
   for (long long r = 1; r < M; ++r) acc = acc + x[r * ld + j];
   out[j] = acc;
+  SG_GRID_TRIGGER();
 }
 
 // --- per-32-row column sums of x (bias-gradient stage 1 when no producer fused it)
 template <class T>
 __global__ void __launch_bounds__(256) k_colsum_part(const T* x, long long ld, long long M, long long N, float* part,
                                                      long long ldp) {
+  SG_GRID_WAIT();
   const long long c = blockIdx.x * 256ll + threadIdx.x;
   if (c >= N) return;
   const long long g = blockIdx.y, r0 = g * 32, r1 = r0 + 32 < M ? r0 + 32 : M;
   float acc = 0.0f;
   for (long long r = r0; r < r1; ++r) acc += (float)x[r * ld + c];
   part[g * ldp + c] = acc;
+  SG_GRID_TRIGGER();
 }
 
 // --- losses.  Per-block loss partial sums (fixed order) -> loss_part[block]
@@ -286,6 +331,7 @@ __global__ void __launch_bounds__(256) k_mse(const T* z, long long ldz, const T*
                                              long long N, T scale, void* dz, int dzd, long long lddz, void* dz2,
                                              int dz2d, long long lddz2, float* colsum, long long ldc,
                                              double* loss_part) {
+  SG_GRID_WAIT();
   __shared__ double red[256];
   const long long c = blockIdx.x * 32ll + threadIdx.x;
   const long long g = blockIdx.y * 8ll + threadIdx.y;
@@ -312,6 +358,7 @@ __global__ void __launch_bounds__(256) k_mse(const T* z, long long ldz, const T*
     __syncthreads();
   }
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
+  SG_GRID_TRIGGER();
 }
 
 // clamped binary cross-entropy on logits (nn_train.py:209-227):
@@ -327,6 +374,7 @@ __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T*
                                              long long N, T scale, void* dz, int dzd, long long lddz, void* dz2,
                                              int dz2d, long long lddz2, float* colsum, long long ldc,
                                              double* loss_part, unsigned* dom) {
+  SG_GRID_WAIT();
   __shared__ double red[256];
   const long long c = blockIdx.x * 32ll + threadIdx.x;
   const long long g = blockIdx.y * 8ll + threadIdx.y;
@@ -365,6 +413,7 @@ __global__ void __launch_bounds__(256) k_bce(const T* z, long long ldz, const T*
     __syncthreads();
   }
   if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * -(double)scale;
+  SG_GRID_TRIGGER();
 }
 
 // The c1 loss IR's float64 domain conditions for one softmax row, checked
@@ -414,6 +463,7 @@ __global__ void __launch_bounds__(1024) k_softmax_xent_rows(const T* z, long lon
                                                             long long lddz, void* dz2, int dz2d, long long lddz2,
                                                             float* colsum, long long ldc, double* loss_part,
                                                             unsigned* dom) {
+  SG_GRID_WAIT();
   __shared__ float cs[32][129];
   __shared__ double red[32];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
@@ -481,6 +531,7 @@ __global__ void __launch_bounds__(1024) k_softmax_xent_rows(const T* z, long lon
     for (int i = 0; i < 32; ++i) s2 += red[i];
     loss_part[blockIdx.x] = s2 * (double)scale;
   }
+  SG_GRID_TRIGGER();
 }
 
 // softmax cross-entropy, warp per row (N <= 1024):
@@ -493,6 +544,7 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const T* z, long long ldz,
                                                       long long lddz, void* dz2, int dz2d, long long lddz2,
                                                       float* colsum, long long ldc, double* loss_part,
                                                       unsigned* dom) {
+  SG_GRID_WAIT();
   __shared__ double red[8];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const long long g = blockIdx.x * 8ll + w;  // 32-row group
@@ -568,9 +620,11 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const T* z, long long ldz,
     for (int i = 0; i < 8; ++i) s += red[i];
     loss_part[blockIdx.x] = s * (double)scale;
   }
+  SG_GRID_TRIGGER();
 }
 
 __global__ void k_sum_loss(const double* part, long long n, double* out) {
+  SG_GRID_WAIT();
   __shared__ double red[256];
   double acc = 0.0;
   for (long long i = threadIdx.x; i < n; i += 256) acc += part[i];
@@ -581,18 +635,22 @@ __global__ void k_sum_loss(const double* part, long long n, double* out) {
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = red[0];
+  SG_GRID_TRIGGER();
 }
 
 // --- SGD over the flat parameter buffer + bf16 shadow copy for the next GEMMs
 template <class T>
 __global__ void k_sgd(T* p, const T* g, long long n, T lr, __nv_bfloat16* shadow) {
+  SG_GRID_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const T v = p[i] - lr * g[i];
     p[i] = v;
     if (shadow) shadow[i] = __float2bfloat16_rn((float)v);
   }
+  SG_GRID_TRIGGER();
 }
 __global__ void k_sgd_vec(float4* p, const float4* g, long long n4, float lr, uint2* shadow) {
+  SG_GRID_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 v = p[i];
     const float4 d = __ldcs(g + i);
@@ -606,11 +664,14 @@ __global__ void k_sgd_vec(float4* p, const float4* g, long long n4, float lr, ui
       shadow[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
     }
   }
+  SG_GRID_TRIGGER();
 }
 
 __global__ void k_cast(const void* src, int sd, void* dst, int dd, long long n) {
+  SG_GRID_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     st_as(dst, dd, i, ld_as<double>(src, sd, i));
+  SG_GRID_TRIGGER();
 }
 
 // 2-D cast of a row-strided block; fp32 -> bf16 (the minibatch load) with
@@ -618,6 +679,7 @@ __global__ void k_cast(const void* src, int sd, void* dst, int dd, long long n) 
 // Blocks walk rows (grid-stride), threads the 8-column vectors of a row.
 __global__ void k_cast2d_f32_bf16(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
                                   long long ldd, long long rows, long long vecs) {
+  SG_GRID_WAIT();
   for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     const float4* s4 = reinterpret_cast<const float4*>(src + r * lds);
     uint4* d4 = reinterpret_cast<uint4*>(dst + r * ldd);
@@ -629,12 +691,15 @@ __global__ void k_cast2d_f32_bf16(const float* __restrict__ src, long long lds, 
                          *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
     }
   }
+  SG_GRID_TRIGGER();
 }
 __global__ void k_cast2d(const void* src, int sd, long long lds, void* dst, int dd, long long ldd, long long rows,
                          long long cols) {
+  SG_GRID_WAIT();
   for (long long r = blockIdx.x; r < rows; r += gridDim.x)
     for (long long c = threadIdx.x; c < cols; c += blockDim.x)
       st_as(dst, dd, r * ldd + c, ld_as<double>(src, sd, r * lds + c));
+  SG_GRID_TRIGGER();
 }
 
 }  // namespace dk
@@ -660,7 +725,7 @@ namespace sg {
 int colsum_finalize_launch(const float* part, long long G, long long ld, long long N, float* out, int,
                            cudaStream_t st) {
   if (N <= 0) return SG_OK;
-  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 1024, 0, st>>>(part, G, ld, N, out);
+  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 7) / 8)), dim3(1024), 0, st, part, G, ld, N, out));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -670,9 +735,9 @@ int colsum_partials(const void* x, int dtype, long long ld, long long M, long lo
   const dim3 grid((unsigned)((N + 255) / 256), (unsigned)((M + 31) / 32));
   if (grid.y > 65535) return fail(SG_EINVAL, "colsum: M too large");
   if (dtype == SG_BF16)
-    dk::k_colsum_part<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, ld, M, N, part, ldp);
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_part<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, (const __nv_bfloat16*)x, ld, M, N, part, ldp));
   else if (dtype == SG_F32)
-    dk::k_colsum_part<float><<<grid, 256, 0, st>>>((const float*)x, ld, M, N, part, ldp);
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_part<float>, dim3(grid), dim3(256), 0, st, (const float*)x, ld, M, N, part, ldp));
   else
     return fail(SG_EINVAL, "colsum: bf16/f32 only");
   SG_CUDA_TRY(cudaGetLastError());
@@ -695,12 +760,12 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
     dim3 g8((unsigned)((N + 511) / 512), (unsigned)((M + 31) / 32));
     if (h_dtype == SG_BF16)
-      dk::k_act_grad_v8<<<g8, dim3(64, 4), 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const __nv_bfloat16*)h,
+      SG_CUDA_TRY(pdl_launch(dk::k_act_grad_v8<__nv_bfloat16, __nv_bfloat16>, dim3(g8), dim3(dim3(64, 4)), 0, (cudaStream_t)stream, (const float*)ybar, ld_y, (const __nv_bfloat16*)h,
                                                               ld_h, M, N, act, (__nv_bfloat16*)dz, ld_dz, colsum,
-                                                              ld_colsum);
+                                                              ld_colsum));
     else
-      dk::k_act_grad_v8<<<g8, dim3(64, 4), 0, (cudaStream_t)stream>>>((const float*)ybar, ld_y, (const float*)h, ld_h, M,
-                                                              N, act, (float*)dz, ld_dz, colsum, ld_colsum);
+      SG_CUDA_TRY(pdl_launch(dk::k_act_grad_v8<float, float>, dim3(g8), dim3(dim3(64, 4)), 0, (cudaStream_t)stream, (const float*)ybar, ld_y, (const float*)h, ld_h, M,
+                                                              N, act, (float*)dz, ld_dz, colsum, ld_colsum));
     SG_CUDA_TRY(cudaGetLastError());
     return SG_OK;
   }
@@ -708,13 +773,13 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
   if (grid.y > 65535) return fail(SG_EINVAL, "act_grad: M too large");
   const bool f64 = ybar_dtype == SG_F64;
   if (f64)
-    dk::k_act_grad<double><<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
+    SG_CUDA_TRY(pdl_launch(dk::k_act_grad<double>, dim3(grid), dim3(dim3(32, 8)), 0, (cudaStream_t)stream, 
         ybar, ybar_dtype, ld_y, h, h_dtype, ld_h, M, N, act, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
-        ld_colsum);
+        ld_colsum));
   else
-    dk::k_act_grad<float><<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
+    SG_CUDA_TRY(pdl_launch(dk::k_act_grad<float>, dim3(grid), dim3(dim3(32, 8)), 0, (cudaStream_t)stream, 
         ybar, ybar_dtype, ld_y, h, h_dtype, ld_h, M, N, act, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
-        ld_colsum);
+        ld_colsum));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -725,8 +790,8 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
   if (N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
-  dk::k_colsum_finalize<<<(unsigned)((N + 7) / 8), 1024, 0, (cudaStream_t)stream>>>(part, G, ld_part, N,
-                                                                                             out);
+  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 7) / 8)), dim3(1024), 0, (cudaStream_t)stream, part, G, ld_part, N,
+                                                                                             out));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -750,8 +815,8 @@ int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, 
       jobs.N[i] = N[b0 + i];
       nmax = std::max(nmax, (long long)N[b0 + i]);
     }
-    dk::k_colsum_finalize_multi<<<dim3((unsigned)((nmax + 7) / 8), (unsigned)nb), 1024, 0, (cudaStream_t)stream>>>(
-        jobs);
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize_multi, dim3(dim3((unsigned)((nmax + 7) / 8), (unsigned)nb)), dim3(1024), 0, (cudaStream_t)stream, 
+        jobs));
     SG_CUDA_TRY(cudaGetLastError());
   }
   return SG_OK;
@@ -765,11 +830,11 @@ int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t ld, int6
   int rc = ctx_activate(ctx);
   if (rc) return rc;
   if (dtype == SG_F64)
-    dk::k_colsum_strict<double><<<cap_grid(N, 128, 1 << 20), 128, 0, (cudaStream_t)stream>>>(
-        (const double*)x, ld, M, N, (double*)out);
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_strict<double>, dim3(cap_grid(N, 128, 1 << 20)), dim3(128), 0, (cudaStream_t)stream, 
+        (const double*)x, ld, M, N, (double*)out));
   else
-    dk::k_colsum_strict<float><<<cap_grid(N, 128, 1 << 20), 128, 0, (cudaStream_t)stream>>>(
-        (const float*)x, ld, M, N, (float*)out);
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_strict<float>, dim3(cap_grid(N, 128, 1 << 20)), dim3(128), 0, (cudaStream_t)stream, 
+        (const float*)x, ld, M, N, (float*)out));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -795,65 +860,65 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
     blocks = (long long)g8.x * g8.y;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dz_dtype == SG_BF16)
-      dk::k_mse_v8<<<g8, dim3(64, 4), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
-                                       (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part);
+      SG_CUDA_TRY(pdl_launch(dk::k_mse_v8<__nv_bfloat16>, dim3(g8), dim3(dim3(64, 4)), 0, st, (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                       (__nv_bfloat16*)dz, ld_dz, colsum, ld_colsum, loss_part));
     else
-      dk::k_mse_v8<<<g8, dim3(64, 4), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
-                                               (float*)dz, ld_dz, colsum, ld_colsum, loss_part);
+      SG_CUDA_TRY(pdl_launch(dk::k_mse_v8<float>, dim3(g8), dim3(dim3(64, 4)), 0, st, (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,
+                                               (float*)dz, ld_dz, colsum, ld_colsum, loss_part));
   } else if (kind == SG_LOSS_MSE) {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
     if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
     blocks = (long long)grid.x * grid.y;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dtype == SG_F64)
-      dk::k_mse<double><<<grid, dim3(32, 8), 0, st>>>((const double*)z, ld_z, (const double*)y, ld_y, M, N,
+      SG_CUDA_TRY(pdl_launch(dk::k_mse<double>, dim3(grid), dim3(dim3(32, 8)), 0, st, (const double*)z, ld_z, (const double*)y, ld_y, M, N,
                                                        scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
-                                                       ld_colsum, loss_part);
+                                                       ld_colsum, loss_part));
     else
-      dk::k_mse<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
+      SG_CUDA_TRY(pdl_launch(dk::k_mse<float>, dim3(grid), dim3(dim3(32, 8)), 0, st, (const float*)z, ld_z, (const float*)y, ld_y, M, N,
                                                       (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-                                                      colsum, ld_colsum, loss_part);
+                                                      colsum, ld_colsum, loss_part));
   } else if (kind == SG_LOSS_BCE) {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 255) / 256));
     if (grid.y > 65535) return fail(SG_EINVAL, "loss: M too large");
     blocks = (long long)grid.x * grid.y;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dtype == SG_F64)
-      dk::k_bce<double><<<grid, dim3(32, 8), 0, st>>>((const double*)z, ld_z, (const double*)y, ld_y, M, N,
+      SG_CUDA_TRY(pdl_launch(dk::k_bce<double>, dim3(grid), dim3(dim3(32, 8)), 0, st, (const double*)z, ld_z, (const double*)y, ld_y, M, N,
                                                        scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2, colsum,
-                                                       ld_colsum, loss_part, dom);
+                                                       ld_colsum, loss_part, dom));
     else
-      dk::k_bce<float><<<grid, dim3(32, 8), 0, st>>>((const float*)z, ld_z, (const float*)y, ld_y, M, N,
+      SG_CUDA_TRY(pdl_launch(dk::k_bce<float>, dim3(grid), dim3(dim3(32, 8)), 0, st, (const float*)z, ld_z, (const float*)y, ld_y, M, N,
                                                       (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-                                                      colsum, ld_colsum, loss_part, dom);
+                                                      colsum, ld_colsum, loss_part, dom));
   } else if (kind == SG_LOSS_SOFTMAX_XENT && N <= 128) {
     blocks = (M + 31) / 32;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dtype == SG_F64)
-      dk::k_softmax_xent_rows<double><<<(unsigned)blocks, 1024, 0, st>>>(
+      SG_CUDA_TRY(pdl_launch(dk::k_softmax_xent_rows<double>, dim3((unsigned)blocks), dim3(1024), 0, st, 
           (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-          colsum, ld_colsum, loss_part, dom);
+          colsum, ld_colsum, loss_part, dom));
     else
-      dk::k_softmax_xent_rows<float><<<(unsigned)blocks, 1024, 0, st>>>(
+      SG_CUDA_TRY(pdl_launch(dk::k_softmax_xent_rows<float>, dim3((unsigned)blocks), dim3(1024), 0, st, 
           (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
-          ld_dz2, colsum, ld_colsum, loss_part, dom);
+          ld_dz2, colsum, ld_colsum, loss_part, dom));
   } else if (kind == SG_LOSS_SOFTMAX_XENT) {
     if (N > 1024) return fail(SG_EINVAL, "softmax_xent: at most 1024 classes");
     blocks = (M + 255) / 256;
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dtype == SG_F64)
-      dk::k_softmax_xent<double><<<(unsigned)blocks, 256, 0, st>>>(
+      SG_CUDA_TRY(pdl_launch(dk::k_softmax_xent<double>, dim3((unsigned)blocks), dim3(256), 0, st, 
           (const double*)z, ld_z, (const double*)y, ld_y, M, N, scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype, ld_dz2,
-          colsum, ld_colsum, loss_part, dom);
+          colsum, ld_colsum, loss_part, dom));
     else
-      dk::k_softmax_xent<float><<<(unsigned)blocks, 256, 0, st>>>(
+      SG_CUDA_TRY(pdl_launch(dk::k_softmax_xent<float>, dim3((unsigned)blocks), dim3(256), 0, st, 
           (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale, dz, dz_dtype, ld_dz, dz2, dz2_dtype,
-          ld_dz2, colsum, ld_colsum, loss_part, dom);
+          ld_dz2, colsum, ld_colsum, loss_part, dom));
   } else {
     return fail(SG_EINVAL, "loss: unknown kind");
   }
   SG_CUDA_TRY(cudaGetLastError());
-  dk::k_sum_loss<<<1, 256, 0, st>>>(loss_part, blocks, loss);
+  SG_CUDA_TRY(pdl_launch(dk::k_sum_loss, dim3(1), dim3(256), 0, st, loss_part, blocks, loss));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -870,14 +935,14 @@ int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t 
   const bool vec = dtype == SG_F32 && n % 4 == 0 && ((uintptr_t)params % 16) == 0 &&
                    ((uintptr_t)grads % 16) == 0 && (!shadow_bf16 || ((uintptr_t)shadow_bf16 % 8) == 0);
   if (vec)
-    dk::k_sgd_vec<<<cap_grid(n / 4, 256, cap), 256, 0, st>>>((float4*)params, (const float4*)grads, n / 4,
-                                                              (float)lr, (uint2*)shadow_bf16);
+    SG_CUDA_TRY(pdl_launch(dk::k_sgd_vec, dim3(cap_grid(n / 4, 256, cap)), dim3(256), 0, st, (float4*)params, (const float4*)grads, n / 4,
+                                                              (float)lr, (uint2*)shadow_bf16));
   else if (dtype == SG_F32)
-    dk::k_sgd<float><<<cap_grid(n, 256, cap), 256, 0, st>>>((float*)params, (const float*)grads, n, (float)lr,
-                                                             (__nv_bfloat16*)shadow_bf16);
+    SG_CUDA_TRY(pdl_launch(dk::k_sgd<float>, dim3(cap_grid(n, 256, cap)), dim3(256), 0, st, (float*)params, (const float*)grads, n, (float)lr,
+                                                             (__nv_bfloat16*)shadow_bf16));
   else
-    dk::k_sgd<double><<<cap_grid(n, 256, cap), 256, 0, st>>>((double*)params, (const double*)grads, n, lr,
-                                                              (__nv_bfloat16*)shadow_bf16);
+    SG_CUDA_TRY(pdl_launch(dk::k_sgd<double>, dim3(cap_grid(n, 256, cap)), dim3(256), 0, st, (double*)params, (const double*)grads, n, lr,
+                                                              (__nv_bfloat16*)shadow_bf16));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -887,8 +952,8 @@ int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t 
   if (n <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
-  dk::k_cast<<<cap_grid(n, 256, (long long)ctx_num_sms(ctx) * 16), 256, 0, (cudaStream_t)stream>>>(
-      src, src_dtype, dst, dst_dtype, n);
+  SG_CUDA_TRY(pdl_launch(dk::k_cast, dim3(cap_grid(n, 256, (long long)ctx_num_sms(ctx) * 16)), dim3(256), 0, (cudaStream_t)stream, 
+      src, src_dtype, dst, dst_dtype, n));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -909,11 +974,11 @@ int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, 
       a16(src) && a16(dst)) {
     const long long vecs = cols / 8;
     const int block = vecs >= 256 ? 256 : (int)((vecs + 31) / 32 * 32);
-    dk::k_cast2d_f32_bf16<<<grid, block, 0, st>>>((const float*)src, ld_src, (__nv_bfloat16*)dst, ld_dst, rows,
-                                                   vecs);
+    SG_CUDA_TRY(pdl_launch(dk::k_cast2d_f32_bf16, dim3(grid), dim3(block), 0, st, (const float*)src, ld_src, (__nv_bfloat16*)dst, ld_dst, rows,
+                                                   vecs));
   } else {
     const int block = cols >= 256 ? 256 : (int)((cols + 31) / 32 * 32);
-    dk::k_cast2d<<<grid, block, 0, st>>>(src, src_dtype, ld_src, dst, dst_dtype, ld_dst, rows, cols);
+    SG_CUDA_TRY(pdl_launch(dk::k_cast2d, dim3(grid), dim3(block), 0, st, src, src_dtype, ld_src, dst, dst_dtype, ld_dst, rows, cols));
   }
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;

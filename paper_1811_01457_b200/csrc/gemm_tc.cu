@@ -596,6 +596,7 @@ namespace {
 // blockIdx.y = row, threads over 4-column groups (no 64-bit divides, float4 loads)
 __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
                                 long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials come from the GEMM before us (PDL)
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (n >= N) return;
   const bool vec = n + 4 <= N && (ldp % 4) == 0;
@@ -650,8 +651,8 @@ static int launch_splitk_reduce(const float* part, int splits, const GemmArgs& g
                                 cudaStream_t st) {
   const unsigned gx = (unsigned)(((g.N + 3) / 4 + 255) / 256);
   const unsigned gy = (unsigned)(g.M < 65535 ? g.M : 65535);
-  k_splitk_reduce<<<dim3(gx, gy), 256, 0, st>>>(part, splits, g.M, g.N, ld_part, g.epi.out_f32, g.epi.ld_f32,
-                                                 g.epi.out_bf16, g.epi.ld_bf16);
+  SG_CUDA_TRY(launch_pdl(k_splitk_reduce, dim3(gx, gy), dim3(256), 0, st, part, splits, g.M, g.N, ld_part,
+                         g.epi.out_f32, g.epi.ld_f32, g.epi.out_bf16, g.epi.ld_bf16));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
