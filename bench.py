@@ -701,6 +701,15 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         tr2 = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", dp=world > 1, graph=False)
         no_graph_ms, _ = _timed(lambda ev: tr2.step(X, Y), steps, max(3, args.warmup), dist, stream)
         tr2.close()
+    chain_ms = None
+    if name == "c5" and world == 1:  # the persistent-GEMM-chain variant beside it (opt-in, bit-identical)
+        os.environ["SGB200_CHAIN"] = "1"
+        try:
+            trc = Trainer(chain, batch, loss=loss, lr=lr, precision="bf16", graph=True)
+            chain_ms, _ = _timed(lambda ev: trc.step(X, Y), steps, max(3, args.warmup), dist, stream)
+            trc.close()
+        finally:
+            del os.environ["SGB200_CHAIN"]
     flops = tr.engine.flops_per_step() * world
     tr.close()
     tflops = flops / (ms * 1e-3) / 1e12
@@ -724,6 +733,7 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         "gpu_launches_per_step": launches,
         "ms_per_step_without_graph": None if no_graph_ms is None else round(no_graph_ms, 4),
         "layer_path_ms_per_step": None if layer_ms is None else round(layer_ms, 4),
+        "gemm_chain_ms_per_step": None if chain_ms is None else round(chain_ms, 4),
         "replicas_identical": replicas_ok,
         "scaling": "strong (global batch fixed)",
     }

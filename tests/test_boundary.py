@@ -218,3 +218,36 @@ def test_leading_dimension_of_size_one_views():
     assert _ld(buf[:1, :]) == 8
     assert _ld(buf[:, :5]) == 8
     assert _ld(torch.zeros((1, 24))) == 24
+
+
+def test_ctypes_mirrors_match_the_c_header(tmp_path):
+    """Every ctypes mirror of an include/sgb200.h struct has the C layout:
+    the same size and field offsets as gcc computes from the header."""
+    import shutil
+    import subprocess
+
+    from paper_1811_01457_b200.dense import DenseDesc, DenseGrad, MlpSmallDesc
+    from paper_1811_01457_b200.gemm import ChainProblem, GemmDesc
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    mirrors = {"sg_tensor": rt.SgTensor, "sg_gemm_desc": GemmDesc, "sg_chain_problem": ChainProblem,
+               "sg_dense_desc": DenseDesc, "sg_dense_grad": DenseGrad, "sg_mlp_small_desc": MlpSmallDesc}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sgb200.h"', "int main(void) {"]
+    for cname, cls in mirrors.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        cname, field, value = line.split()
+        got[(cname, field)] = int(value)
+    for cname, cls in mirrors.items():
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
