@@ -285,14 +285,13 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
   };
   auto coord = [&](int t) {
     TileCoord c;
-    if (p.tail_split > 0) {  // tail mode: row-major tiles
-      const int tile = t < p.tail_full ? t : p.tail_full + ((t - p.tail_full) >> 1);
-      c.m0 = (tile / n_tiles) * PM;
-      c.n0 = (tile % n_tiles) * BN;
-      return c;
-    }
+    // tail mode: work unit t < tail_full is tile t, the rest are the two
+    // K-halves of the remaining tiles; tiles in the same grouped raster as below
+    // (row-major order read every B block once per wave: 2.3x the algorithmic
+    // DRAM traffic of the TF32 4096^2 dW)
     const int G = p.raster;  // grouped raster over 256-row pair tiles
-    const int u = (t % out_tiles) % tiles_pb;
+    const int u = p.tail_split > 0 ? (t < p.tail_full ? t : p.tail_full + ((t - p.tail_full) >> 1))
+                                   : (t % out_tiles) % tiles_pb;
     const int per_group = G * n_tiles;
     const int group = u / per_group;
     const int first_m = group * G;
@@ -799,7 +798,17 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
       !g.epi.colsum && !g.epi.out_pre && num_kb >= 8 && tiles > pairs_avail && rem > 0 && 2 * rem <= pairs_avail) {
     p.tail_full = tiles - rem;
     p.tail_split = rem;
-    const long long row0 = (long long)(p.tail_full / n_tiles) * 256;  // first row of the first split tile
+    // the split tiles are the last `rem` of the grouped raster (coord() in the
+    // kernel): zero every row from the first of them on -- full tiles in those
+    // rows store over the zeros afterwards
+    const int m_tiles = (g.M + 255) / 256;
+    int first_m = m_tiles;
+    for (int u = p.tail_full; u < tiles; ++u) {
+      const int per_group = p.raster * n_tiles, group = u / per_group, fm = group * p.raster;
+      const int gsize = std::min(m_tiles - fm, p.raster);
+      first_m = std::min(first_m, fm + (u - group * per_group) % gsize);
+    }
+    const long long row0 = (long long)first_m * 256;
     SG_CUDA_TRY(cudaMemset2DAsync(g.epi.out_f32 + row0 * g.epi.ld_f32, (size_t)g.epi.ld_f32 * 4, 0,
                                   (size_t)g.N * 4, (size_t)(g.M - row0), st));
     work = p.tail_full + 2 * rem;

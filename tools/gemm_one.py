@@ -22,12 +22,25 @@ Hout = torch.empty((M, N), dtype=bf, device="cuda")
 dX = torch.empty((M, K), dtype=bf, device="cuda")
 dW = torch.empty((N, K), device="cuda")
 cs = torch.empty(((M + 31) // 32, max(N, K)), device="cuda")
+X32, dZ32 = X.float(), dZ.float()
 fn = {
     "fwd": lambda: gemm(X, W, epilogue="bias_act", act="tanh", bias=bias, out_lp=Hout),
     "dx": lambda: gemm(dZ, W, b_mn=True, epilogue="act_grad", act="tanh", aux=H, out_lp=dX, colsum=cs),
     "dxplain": lambda: gemm(dZ, W, b_mn=True, out_lp=dX),
     "dw": lambda: gemm(dZ, X, a_mn=True, b_mn=True, out=dW),
+    "dw32": lambda: gemm(dZ32, X32, a_mn=True, b_mn=True, precision="tf32", out=dW),
+    "dx32": lambda: gemm(dZ32, W.float(), b_mn=True, precision="tf32", out=torch.empty((M, K), device="cuda")),
 }[kind]
-for _ in range(reps):
+for _ in range(min(reps, 3)):
     fn()
 torch.cuda.synchronize()
+if reps > 3:
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) / reps * 1e3
+    K2 = M if kind.startswith("dw") else K
+    print(f"{kind} {M}x{N}x{K}: {us:.1f} us, {2 * M * N * K / us / 1e6:.1f} TF/s")
