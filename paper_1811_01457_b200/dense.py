@@ -446,9 +446,19 @@ class ChainEngine:
         # per-layer path but, measured on B200, not yet faster:
         # a chained unit's epilogue also waits for its TMA stores to land and
         # publishes them, and that is on the critical path at K = 1024.
+        # Modes: "full" (SGB200_CHAIN=1): forward and pullback as one chain each;
+        # "pairwise" (SGB200_CHAIN=2): per layer, the pullback's dW and dX -- two
+        # independent GEMMs -- in ONE persistent launch (the dW's K-splits and
+        # the dX tiles share the CTA pairs: no idle pairs beside the split-K
+        # dW, one fill / drain instead of two), every db finalised at the end.
         if gemm_chain is None:
-            gemm_chain = os.environ.get("SGB200_CHAIN", "0") == "1"
+            gemm_chain = {"1": "full", "2": "pairwise"}.get(os.environ.get("SGB200_CHAIN", "0"))
+        elif gemm_chain is True:
+            gemm_chain = "full"
+        if gemm_chain not in (None, False, "full", "pairwise"):
+            raise ValueError(f"unknown gemm_chain mode {gemm_chain!r}")
         self.chainable = bool(gemm_chain) and precision == "bf16" and self.L >= 2
+        self.chain_mode = gemm_chain if self.chainable else None
         self.chains = None
         if self.chainable:
             self.dZl = [torch.zeros((B, _ld(d)), dtype=self.adt, device=dev)[:, :d] for d in self.sizes[1:]]
@@ -520,13 +530,20 @@ class ChainEngine:
     def forward(self):
         """Record the forward pass on the tape; returns the top-layer outputs."""
         self.tape.clear()
-        if self._use_chain():
+        use_chain = self._use_chain()
+        if use_chain and self.chain_mode == "full":
             self.chains[0].run()
             # one tape entry for the whole chain: its pullback is the chained
             # dX / dW pass (the save set is every H[l] and W[l], as per layer)
             self.tape.push(TapeEntry("dense_chain", tuple(self.H) + tuple(self.W), self._chain_backward, None))
             return self.Zt
         L = self.L
+        if use_chain:  # pairwise: per-layer forward GEMMs, the pullback in L launches
+            for l in range(L):
+                last = l == L - 1
+                dense_forward(self.descs[l], H=None if last else self.H[l + 1], H_f32=self.Zt if last else None)
+            self.tape.push(TapeEntry("dense_pairwise", tuple(self.H) + tuple(self.W), self._chain_backward, None))
+            return self.Zt
         for l in range(L):
             last = l == L - 1
             if self.precision == "bf16":
@@ -555,13 +572,26 @@ class ChainEngine:
         from .gemm import GemmChain, gemm_desc
 
         L, B = self.L, self.B
+        pairs = max(1, torch.cuda.get_device_properties(self.P.device).multi_processor_count // 2)
+        if self.chain_mode == "pairwise":
+            per_layer = []
+            for l in range(L):
+                probs = [(gemm_desc(self.dz_of(l), self.H[l], a_mn=True, b_mn=True, out=self.gW[l]),
+                          _pair_splits(self.sizes[l + 1], self.sizes[l], B, pairs), [])]
+                if l > 0:  # the long dW K-splits are planned first, the dX tiles fill around them
+                    act_prev = self.acts[l - 1]
+                    probs.append((gemm_desc(self.dz_of(l), self.Ws[l], b_mn=True,
+                                            epilogue="store" if act_prev == "identity" else "act_grad",
+                                            act=act_prev, aux=self.H[l], out_lp=self.dz_of(l - 1),
+                                            colsum=self.cs_of(l - 1)), 1, []))
+                per_layer.append(GemmChain(probs))
+            return None, per_layer
         fwd = []
         for l in range(L):
             top = l == L - 1
             d = gemm_desc(self.H[l], self.Ws[l], epilogue="bias_act", act=self.acts[l], bias=self.b[l],
                           out_lp=None if top else self.H[l + 1], out=self.Zt if top else None)
             fwd.append((d, 1, [("rows", l - 1)] if l > 0 else []))
-        pairs = max(1, torch.cuda.get_device_properties(self.P.device).multi_processor_count // 2)
         # backward order: the dX chain is the critical path (each layer's dZ
         # feeds the next dX row block by row block); layer l's dW (which only
         # needs dZ_l) is placed one layer later so it fills the gaps
@@ -587,8 +617,13 @@ class ChainEngine:
 
     def _chain_backward(self, _ctx):
         """Chained pullback: every layer's dX (with the lower layer's act' and
-        bias-gradient partials fused) and dW in one launch, then every db."""
-        self.chains[1].run()
+        bias-gradient partials fused) and dW in one launch -- or, pairwise, one
+        launch per layer -- then every db."""
+        if self.chain_mode == "pairwise":
+            for l in range(self.L - 1, -1, -1):
+                self.chains[1][l].run()
+        else:
+            self.chains[1].run()
         lib = _lib()
         n = self.L
         parts = (ctypes.c_void_p * n)(*[_p(self.cs_of(l)) for l in range(n)])

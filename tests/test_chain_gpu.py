@@ -81,7 +81,7 @@ def test_chained_step_is_bit_identical_to_layer_path(sizes, acts, B):
     X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
     Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
     res = {}
-    for use in (False, True):
+    for use in (False, "full", "pairwise"):
         e = ChainEngine(chain, B, "mse", "bf16", small=False, gemm_chain=use)
         for _ in range(2):  # twice: the chain replays from reset counters
             e.load_batch(X, Y)
@@ -89,13 +89,15 @@ def test_chained_step_is_bit_identical_to_layer_path(sizes, acts, B):
             e.loss_and_seed()
             e.pullback()
         torch.cuda.synchronize()
-        assert (e.chains is not None) == use
+        assert (e.chains is not None) == bool(use)
         res[use] = (e.loss.clone(), e.G.clone(), e.Zt.clone(), [h.clone() for h in e.H])
-    (l0, g0, z0, h0), (l1, g1, z1, h1) = res[False], res[True]
-    assert torch.equal(z0, z1)
-    assert all(torch.equal(a, b) for a, b in zip(h0, h1))
-    assert torch.equal(l0, l1)
-    assert torch.equal(g0, g1)
+    l0, g0, z0, h0 = res[False]
+    for mode in ("full", "pairwise"):
+        l1, g1, z1, h1 = res[mode]
+        assert torch.equal(z0, z1), mode
+        assert all(torch.equal(a, b) for a, b in zip(h0, h1)), mode
+        assert torch.equal(l0, l1), mode
+        assert torch.equal(g0, g1), mode
 
 
 def test_chained_training_run_matches_layer_path():

@@ -20,7 +20,7 @@ chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(len(acts))
 X = torch.rand((B, sizes[0]), device="cuda")
 Y = torch.rand((B, sizes[-1]), device="cuda") * 2 - 1
 res = {}
-for use in (False, True):
+for use in (False, "full", "pairwise"):
     e = ChainEngine(chain, B, "mse", "bf16", small=False, gemm_chain=use)
 
     def step():
@@ -33,7 +33,7 @@ for use in (False, True):
     step()
     torch.cuda.synchronize()
     print("use_chain", use, "first step ok", round(time.time() - t0, 2), "s", flush=True)
-    if use:
+    if use == "full":
         print("  fwd units", e.chains[0].units, "est", round(e.chains[0].est_us, 1), "us; bwd units",
               e.chains[1].units, "est", round(e.chains[1].est_us, 1), "us", flush=True)
     for _ in range(3):
@@ -47,4 +47,5 @@ for use in (False, True):
     torch.cuda.synchronize()
     print("  ms/step (fwd+loss+pullback, eager issue)", round(s.elapsed_time(t) / 10, 4), flush=True)
     res[use] = (e.loss.clone(), e.G.clone(), e.Zt.clone())
-print("bit-identical loss/G/Zt:", [torch.equal(a, b) for a, b in zip(res[False], res[True])])
+for mode in ("full", "pairwise"):
+    print(mode, "bit-identical loss/G/Zt:", [torch.equal(a, b) for a, b in zip(res[False], res[mode])])
