@@ -43,7 +43,11 @@ namespace chain {
 using namespace tc;
 
 constexpr int PM = 256, PN = 256, HALF = 128, CBK = 64;  // pair tile, k-block (bf16)
-constexpr int CSTAGES = 5;  // + wide epilogue slots (see gemm_tc_dev.cuh)
+// SGB200_CHAIN_WIDE=1: wide epilogue slots + 5 operand stages; default: the
+// standalone kernels' narrow slots + 6 stages (2 % faster per chained unit)
+template <bool WIDE> struct ChainCfg {
+  static constexpr int STAGES = WIDE ? 5 : 6;
+};
 constexpr int SLOTS = 2 * EPI_WARPS;                     // epilogue warps per pair tile
 
 // A problem's tensor maps live in global memory (TMA reads them there); the
@@ -148,8 +152,10 @@ __device__ __forceinline__ void split_fixup(const Params& P, const Problem& pr, 
   }
 }
 
+template <bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_chain_kernel(const __grid_constant__ Params P) {
+  constexpr int CSTAGES = ChainCfg<WIDE>::STAGES;
   constexpr int A_BYTES = HALF * ROW_BYTES;
   constexpr int B_BYTES = HALF * ROW_BYTES;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -297,7 +303,7 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
     int acc = 0;
     uint32_t acc_phase = 0, aux_phase = 0;
     int next_buf = 0;
-    uint8_t* slot = stage_slots + ew * Slot<true>::BYTES;
+    uint8_t* slot = stage_slots + ew * Slot<WIDE>::BYTES;
     uint64_t* my_aux = &aux_bar[2 * ew];
     for (int i = u0; i < u1; ++i) {
       const Unit un = P.units[i];
@@ -308,11 +314,11 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
       const int c0 = half * CH_PER;
       const bool staged = p.aux_stage && row0 < p.M;
       const Maps* mp = &P.maps[un.prob];
-      epi_aux_prologue<true>(staged, lane, slot, &mp->aux, my_aux, n0t + c0 * 32, CH_PER, p.N, row0);
+      epi_aux_prologue<WIDE>(staged, lane, slot, &mp->aux, my_aux, n0t + c0 * 32, CH_PER, p.N, row0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane == 0) SG_TRACE(i - u0, 1);  // accumulator complete
-      epi_chunks<true>(p, tmem_base + acc * PN + ((uint32_t)(q * 32) << 16), n0t + c0 * 32, c0, CH_PER, row0, lane,
+      epi_chunks<WIDE>(p, tmem_base + acc * PN + ((uint32_t)(q * 32) << 16), n0t + c0 * 32, c0, CH_PER, row0, lane,
                        un.split, 0, false, slot, staged, &mp->aux, my_aux, aux_phase, &mp->lp, &mp->f32, next_buf);
       tc_fence_before();
       __syncwarp();
@@ -385,9 +391,19 @@ void chain_free(sg_chain* c) {
   delete c;
 }
 
-constexpr size_t CHAIN_SMEM = (size_t)chain::CSTAGES * 2 * 128 * tc::ROW_BYTES + 1024 + 1024 +
-                              tc::EPI_WARPS * tc::Slot<true>::BYTES;
-static_assert(CHAIN_SMEM <= 232448, "shared memory budget");
+template <bool WIDE>
+constexpr size_t chain_smem() {
+  return (size_t)chain::ChainCfg<WIDE>::STAGES * 2 * 128 * tc::ROW_BYTES + 1024 + 1024 +
+         tc::EPI_WARPS * tc::Slot<WIDE>::BYTES;
+}
+static_assert(chain_smem<true>() <= 232448 && chain_smem<false>() <= 232448, "shared memory budget");
+bool chain_wide() {
+  static const bool w = [] {
+    const char* e = std::getenv("SGB200_CHAIN_WIDE");
+    return e && e[0] == '1';
+  }();
+  return w;
+}
 
 }  // namespace
 
@@ -617,8 +633,11 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
   c->params.n_cnt = (int)n_cnt;
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
-    e = cudaFuncSetAttribute(chain::gemm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)CHAIN_SMEM);
+    e = cudaFuncSetAttribute(chain::gemm_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)chain_smem<true>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(chain::gemm_chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)chain_smem<false>());
     if (e != cudaSuccess) {
       chain_free(c);
       return cuda_fail(e, "chain: kernel attributes");
@@ -634,14 +653,16 @@ int sg_chain_run(sg_chain* c, void* stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c->grid);
   cfg.blockDim = dim3(tc::NUM_THREADS);
-  cfg.dynamicSmemBytes = CHAIN_SMEM;
+  const bool wide = chain_wide();
+  cfg.dynamicSmemBytes = wide ? chain_smem<true>() : chain_smem<false>();
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SG_CUDA_TRY(cudaLaunchKernelEx(&cfg, chain::gemm_chain_kernel, c->params));
+  if (wide) SG_CUDA_TRY(cudaLaunchKernelEx(&cfg, chain::gemm_chain_kernel<true>, c->params));
+  else SG_CUDA_TRY(cudaLaunchKernelEx(&cfg, chain::gemm_chain_kernel<false>, c->params));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
