@@ -202,20 +202,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         float v[32];
         tmem_ld32(tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
         if (n0 >= p.N) continue;  // warp-uniform
-        AuxSrc aux;
+        float h[32];
         if (staged) {
           mbar_wait(&aux_bar[ew], aux_phase);
           aux_phase ^= 1;
-          aux.smem = slot;
-          aux.issue_base = slot;
-          aux.map = &tma_aux;
-          aux.bar = &aux_bar[ew];
-          aux.next_n0 = n0 + 32;
-          aux.row0 = row0;
-          aux.issue = c + 1 < c1 && n0 + 32 < p.N;
+          aux_read(slot, h, lane);
+          fence_proxy_async();  // our reads precede the next async write of the buffer
+          __syncwarp();
+          if (lane == 0 && c + 1 < c1 && n0 + 32 < p.N) aux_issue(slot, &tma_aux, &aux_bar[ew], n0 + 32, row0);
         }
-        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, row0 < p.M, n0, lane, t / out_tiles, bidx, aux, slot, false,
-                  &tma_olp, &tma_of32);
+        epi_chunk(p, v, m, row_ok, (tc.m0 >> 5) + q, row0 < p.M, n0, lane, t / out_tiles, bidx, staged, h, slot,
+                  false, &tma_olp, &tma_of32);
       }
       tc_fence_before();
       __syncwarp();
@@ -236,11 +233,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   }
 }
 
-// EW epilogue warps per CTA: 8 (two per TMEM lane quadrant, each a half of the
-// tile's columns) or 16 (four per quadrant, a quarter each: twice the warps to
-// hide the epilogue's latencies, at 96 registers per thread)
-template <bool TF32, int STAGES, bool A_MN, bool B_MN, bool WIDE, int EW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((EPI_WARP0 + EW) * 32, 1)
+template <bool TF32, int STAGES, bool A_MN, bool B_MN, bool WIDE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_olp, const __grid_constant__ CUtensorMap tma_of32,
                       const __grid_constant__ CUtensorMap tma_aux,
@@ -319,9 +313,9 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 2 * EW);  // every epilogue warp of both CTAs
+      mbar_init(&acc_empty[a], 2 * EPI_WARPS);  // every epilogue warp of both CTAs
     }
-    for (int w = 0; w < 2 * EW; ++w) mbar_init(&aux_bar[w], 1);
+    for (int w = 0; w < 2 * EPI_WARPS; ++w) mbar_init(&aux_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -421,8 +415,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
     // ===================== epilogue (both CTAs, own 128 rows) =====================
     const int ew = warp - EPI_WARP0;
     const int q = ew % 4;
-    const int half = ew / 4;  // which part of the tile's columns
-    constexpr int CH_PER = (BN / 32) / (EW / 4);
+    const int half = ew / 4;
+    constexpr int CH_PER = (BN / 32) / 2;
     const uint32_t acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
     const uint32_t acc_empty_leader1 = mapa_shared(smem_u32(&acc_empty[1]), 0);
     int acc = 0;
@@ -449,18 +443,18 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
       if (p.splits > 1 && p.split_cnt) {  // in-kernel split-K fix-up of this warp's region of the tile
         const int tile = (tc.m0 / PM) * n_tiles + tc.n0 / BN;
-        split_region_fixup(p, p.split_cnt + tile * (2 * EW) + (int)rank * EW + ew, row0, tc.n0 + c0 * 32, CH_PER,
-                           lane);
+        split_region_fixup(p, p.split_cnt + tile * (2 * EPI_WARPS) + (int)rank * EPI_WARPS + ew, row0,
+                           tc.n0 + c0 * 32, CH_PER, lane);
       }
       if (lane == 0 && ew == 0) SG_TRACE(it, 2);  // epilogue warp 0 done with the tile
-      if (lane == 0 && ew == EW - 1) SG_TRACE(it, 3);  // last epilogue warp done
+      if (lane == 0 && ew == EPI_WARPS - 1) SG_TRACE(it, 3);  // last epilogue warp done
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
   }
-  if (EW == EPI_WARPS && warp >= EPI_WARP0 && p.fin_out) {
+  if (warp >= EPI_WARP0 && p.fin_out) {
     // bias-gradient finalize as the epilogue's tail job, in warp 0's staging slot
     if (lane == 0) bulk_wait_read0();
     epi_bar();
@@ -720,15 +714,15 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   return SG_OK;
 }
 
-template <bool TF32, bool A_MN, bool B_MN, bool WIDE, int EW = tc::EPI_WARPS>
+template <bool TF32, bool A_MN, bool B_MN, bool WIDE>
 int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   constexpr int BK = tc::Elem<TF32>::BK;
-  // wide epilogue slots (double-buffered staging, aux two chunks ahead) or 16
-  // epilogue warps cost one operand stage of the 227 KB
-  constexpr int STAGES = (WIDE || EW > tc::EPI_WARPS) ? 5 : 6;
+  // wide epilogue slots (double-buffered staging, aux two chunks ahead) cost
+  // one operand stage of the 227 KB
+  constexpr int STAGES = WIDE ? 5 : 6;
   constexpr int STAGE = 128 * tc::ROW_BYTES * 2;
-  // operand ring + alignment + barriers (1 KB) + one epilogue staging slot per epilogue warp
-  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + EW * tc::Slot<WIDE>::BYTES;
+  // operand ring + alignment + barriers (1 KB) + 8 epilogue staging slots
+  constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1024 + tc::EPI_WARPS * tc::Slot<WIDE>::BYTES;
   static_assert(SMEM <= 232448, "shared memory budget");
   CUtensorMap ma, mb;
   int rc;
@@ -738,7 +732,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   if (B_MN) rc = make_map(&mb, g.B, g.N, g.K, g.ldb, BK, TF32, true, g.batch, g.sb);
   else rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 128, TF32, false, g.batch, g.sb);
   if (rc) return rc;
-  auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN, WIDE, EW>;
+  auto kern = tc::gemm_tc_pair_kernel<TF32, STAGES, A_MN, B_MN, WIDE>;
   static std::atomic<uint64_t> attr_set{0};  // per device
   if (first_on_device(attr_set))
     SG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -775,13 +769,13 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
     SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
     p.part = part;
     if (fixup) {  // the last split of each tile region sums the partials inside the kernel
-      const size_t ncnt = (size_t)tiles * 2 * EW;
+      const size_t ncnt = (size_t)tiles * 2 * tc::EPI_WARPS;
       SG_CUDA_TRY(cudaMallocAsync((void**)&cnt, ncnt * sizeof(unsigned), st));
       SG_CUDA_TRY(cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned), st));
       p.split_cnt = cnt;
     }
   }
-  if (g.fin.out && EW == tc::EPI_WARPS) {
+  if (g.fin.out) {
     p.fin_part = g.fin.part;
     p.fin_G = g.fin.G;
     p.fin_ld = g.fin.ld;
@@ -820,7 +814,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
     work = p.tail_full + 2 * rem;
   }
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
-  SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3((tc::EPI_WARP0 + EW) * 32), SMEM, st, ma, mb, mlp, mf32, maux, p));
+  SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
   if (splits > 1) {
     if (!cnt)
@@ -828,8 +822,6 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
     SG_CUDA_TRY(cudaFreeAsync(part, st));
     if (cnt) SG_CUDA_TRY(cudaFreeAsync(cnt, st));
   }
-  if (g.fin.out && !p.fin_out)
-    return colsum_finalize_launch(g.fin.part, g.fin.G, g.fin.ld, g.fin.N, g.fin.out, num_sms, st);
   return SG_OK;
 }
 
@@ -862,18 +854,7 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
     const char* e = std::getenv("SGB200_GEMM_WIDE");
     return e && e[0] == '1';
   }();
-  // 16 epilogue warps per CTA (SGB200_GEMM_EPI16=1)
-  static const bool epi16 = [] {
-    const char* e = std::getenv("SGB200_GEMM_EPI16");
-    return e && e[0] == '1';
-  }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
-    if (epi16) {
-      if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, false, 16>(g, num_sms, st);
-      if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, false, 16>(g, num_sms, st);
-      if (g.a_mn && g.b_mn) return run_pair<TF32, true, true, false, 16>(g, num_sms, st);
-      return run_pair<TF32, true, false, false, 16>(g, num_sms, st);
-    }
     if (wide) {
       if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, true>(g, num_sms, st);
       if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, true>(g, num_sms, st);

@@ -422,92 +422,15 @@ __device__ __forceinline__ uint8_t* stage_buf(uint8_t* slot, int b) {
   return slot + b * (BF16 ? 2048 : 4096);
 }
 
-// The saved activation of an ACT_GRAD chunk: a TMA-staged 32 x 32 bf16 block
-// in shared memory (read in place, 8 columns at a time, then released: the
-// block's buffer is re-filled with the next chunk's) or, without staging,
-// the row in global memory.
-struct AuxSrc {
-  const uint8_t* smem = nullptr;  // staged block, aux_read's layout (base + AUX_OFF)
-  uint8_t* issue_base = nullptr;  // release: refill this buffer ...
-  const CUtensorMap* map = nullptr;
-  uint64_t* bar = nullptr;
-  int next_n0 = 0, row0 = 0;      // ... with the block at (next_n0, row0)
-  bool issue = false;
-};
-// v[c0 .. c0+7] *= act'(h), act' from the saved output (rules.py:82-94)
-__device__ __forceinline__ void act_grad8(float (&v)[32], int c0, const float (&h)[8], int act) {
-  if (act == SG_ACT_SIGMOID) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[c0 + j] *= h[j] * (1.0f - h[j]);
-  } else if (act == SG_ACT_TANH) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[c0 + j] *= 1.0f - h[j] * h[j];
-  } else if (act == SG_ACT_RELU) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[c0 + j] = h[j] > 0.0f ? v[c0 + j] : 0.0f * v[c0 + j];
-  }
-}
-__device__ __forceinline__ void unpack_bf16x8(const uint4& w, float (&h)[8]) {
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2 f = __bfloat1622float2(b[j]);
-    h[2 * j] = f.x;
-    h[2 * j + 1] = f.y;
-  }
-}
-// act' applied from the aux source without materialising the 32-value row
-__device__ __forceinline__ void act_grad_from(float (&v)[32], const GemmEpilogue& e, const AuxSrc& aux, long long m,
-                                              int n0, int nn, int lane) {
-  if (aux.smem) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float h[8];
-      unpack_bf16x8(*reinterpret_cast<const uint4*>(aux.smem + AUX_OFF + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)),
-                    h);
-      act_grad8(v, 8 * c, h, e.act);
-    }
-  } else if (e.aux_f32) {
-    const float* src = e.aux_f32 + m * e.ld_aux + n0;
-    const bool vec = nn == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float h[8];
-      if (vec) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(src + 8 * c));
-        const float4 b = __ldg(reinterpret_cast<const float4*>(src + 8 * c + 4));
-        h[0] = a.x, h[1] = a.y, h[2] = a.z, h[3] = a.w, h[4] = b.x, h[5] = b.y, h[6] = b.z, h[7] = b.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) h[j] = 8 * c + j < nn ? __ldg(src + 8 * c + j) : 0.0f;
-      }
-      act_grad8(v, 8 * c, h, e.act);
-    }
-  } else {
-    const __nv_bfloat16* src = e.aux + m * e.ld_aux + n0;
-    const bool vec = nn == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float h[8];
-      if (vec) {
-        unpack_bf16x8(__ldg(reinterpret_cast<const uint4*>(src + 8 * c)), h);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) h[j] = 8 * c + j < nn ? __bfloat162float(src[8 * c + j]) : 0.0f;
-      }
-      act_grad8(v, 8 * c, h, e.act);
-    }
-  }
-}
-
 // One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
 template <bool WIDE = false>
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
-                                          bool grp_ok, int n0, int lane, int split, int bidx, const AuxSrc& aux,
-                                          uint8_t* slot, bool radd, const CUtensorMap* map_lp,
-                                          const CUtensorMap* map_f32, int* next_buf = nullptr) {
+                                          bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
+                                          const float (&hs)[32], uint8_t* slot, bool radd,
+                                          const CUtensorMap* map_lp, const CUtensorMap* map_f32,
+                                          int* next_buf = nullptr) {
   SG_CPROF_START();
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -523,18 +446,20 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0.0f;
   } else if (e.mode == SG_EPI_BIAS_ACT) {
-    if (e.bias) {  // added in place, four columns at a time
+    if (e.bias) {
+      float bv[32];
       if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + i));
-          v[i] += b4.x, v[i + 1] += b4.y, v[i + 2] += b4.z, v[i + 3] += b4.w;
+          bv[i] = b4.x, bv[i + 1] = b4.y, bv[i + 2] = b4.z, bv[i + 3] = b4.w;
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (n0 + i < p.N) v[i] += __ldg(e.bias + n0 + i);
+        for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += bv[i];
     }
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
     if (e.act == SG_ACT_SIGMOID) {
@@ -545,12 +470,14 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     }
     act_fwd_chunk(v, e.act);
   } else if (e.mode == SG_EPI_ACT_GRAD) {
-    act_grad_from(v, e, aux, m, n0, nn, lane);
-  }
-  if (aux.smem) {  // warp-uniform: release the staged block, refill its buffer
-    fence_proxy_async();  // our reads precede the next async write of the buffer
-    __syncwarp();
-    if (lane == 0 && aux.issue) aux_issue(aux.issue_base, aux.map, aux.bar, aux.next_n0, aux.row0);
+    if (hstaged) {
+      act_grad_chunk(v, hs, e.act);
+    } else {
+      float h[32];
+      if (e.aux_f32) load_row_f32(e.aux_f32 + (long long)m * e.ld_aux + n0, h, nn);
+      else load_row_bf16(e.aux + (long long)m * e.ld_aux + n0, h, nn);
+      act_grad_chunk(v, h, e.act);
+    }
   }
   if (e.mode == SG_EPI_BIAS_ACT && e.act == SG_ACT_SIGMOID && e.dom) {  // warp-uniform
     if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
@@ -780,24 +707,22 @@ __device__ __forceinline__ void epi_chunks(const KParams& p, uint32_t tmem_row, 
     tmem_ld32(tmem_row + (c_first + j) * 32, v);
     SG_CPROF(0);  // TMEM load
     if (n0 >= p.N) continue;  // warp-uniform; later chunks are past N as well
-    AuxSrc aux;
+    float h[32];
     if (staged) {
       const int b = WIDE ? (j & 1) : 0;
       mbar_wait(&aux_bars[b], (aux_phase >> b) & 1);
       aux_phase ^= 1u << b;
       SG_CPROF(1);  // saved activation block arrived
       uint8_t* base = WIDE ? aux_base_wide(slot, b) : slot;
+      aux_read(base, h, lane);
+      fence_proxy_async();  // our reads precede the next async write of the buffer
+      __syncwarp();
       const int ahead = WIDE ? 2 : 1;
-      aux.smem = base;
-      aux.issue_base = base;
-      aux.map = map_aux;
-      aux.bar = &aux_bars[b];
-      aux.next_n0 = n0 + 32 * ahead;
-      aux.row0 = row0;
-      aux.issue = j + ahead < nch && n0 + 32 * ahead < p.N;
+      if (lane == 0 && j + ahead < nch && n0 + 32 * ahead < p.N)
+        aux_issue(base, map_aux, &aux_bars[b], n0 + 32 * ahead, row0);
     }
-    epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, aux, slot, radd, map_lp, map_f32,
-                    &next_buf);
+    epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, staged, h, slot, radd, map_lp,
+                    map_f32, &next_buf);
   }
 }
 
