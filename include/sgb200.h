@@ -136,6 +136,13 @@ SG_API int sg_ew_variant_count(sg_kernel* kern);
 #define SG_EPI_STORE 0
 #define SG_EPI_BIAS_ACT 1
 #define SG_EPI_ACT_GRAD 2
+/* BIAS_ACT with a known cotangent of the activation (a value-and-pullback
+ * call, reverse_ad.py:633-663 `grad` with seeds): out_lp = act(z + b) (bf16,
+ * the saved activation) and, in the same epilogue, out2_lp = seed .* act'(h)
+ * with h that bf16 activation (rules.py:82-94), column sums of it into colsum;
+ * seed is fp32 [M][ld_seed] passed in `aux`/`ld_aux`.  BF16 precision, no
+ * fp32 `out`; replaces a separate act' pass over the seed. */
+#define SG_EPI_BIAS_ACT_SEED 3
 
 #define SG_ACT_IDENTITY 0
 #define SG_ACT_SIGMOID 1
@@ -172,6 +179,8 @@ typedef struct sg_gemm_desc {
    * take the STORE / BIAS_ACT epilogues (bias shared) without colsum/out_pre. */
   int64_t batch;
   int64_t stride_a, stride_b, stride_out, stride_lp;
+  void* out2_lp; /* BIAS_ACT_SEED: bf16 [M][ld_out2] seed .* act'(out_lp) */
+  int64_t ld_out2;
 } sg_gemm_desc;
 
 SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);

@@ -25,6 +25,10 @@ struct GemmEpilogue {
   float* colsum;               // optional column sums of the result per 32-row group:
   long long ld_colsum;         //   colsum[(m / 32)][n], [ceil(M/32)][ld_colsum]
   unsigned* dom = nullptr;     // domain flags (SG_DOM_*): sigmoid pre-activations that overflow the reference
+  const float* seed = nullptr; // BIAS_ACT_SEED: cotangent of the activation, fp32 [M][ld_seed]
+  long long ld_seed = 0;
+  __nv_bfloat16* out2_bf16 = nullptr;  // BIAS_ACT_SEED: seed .* act'(h), bf16 [M][ld_out2]
+  long long ld_out2 = 0;
 };
 
 // Column sums of a 32x32 block held one row per lane (v[i] = column i):

@@ -578,12 +578,14 @@ void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& 
   }();
   std::memset(&mlp, 0, sizeof mlp);
   std::memset(&mf32, 0, sizeof mf32);
-  p.tma_lp = p.tma_f32 = 0;
+  p.tma_lp = p.tma_f32 = p.tma_o2 = 0;
   if (!enabled || p.splits > 1) return;
   if (g.epi.out_bf16)
     p.tma_lp = make_out_map(&mlp, g.epi.out_bf16, true, g.N, g.M, g.epi.ld_bf16, g.batch, g.so_lp);
   if (g.epi.out_f32)
     p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32, g.batch, g.so_f32);
+  else if (g.epi.mode == SG_EPI_BIAS_ACT_SEED && g.epi.out2_bf16)  // out2 (bf16) in the fp32 map's slot
+    p.tma_o2 = make_out_map(&mf32, g.epi.out2_bf16, true, g.N, g.M, g.epi.ld_out2, 1, 0);
 }
 
 }  // namespace tcmap

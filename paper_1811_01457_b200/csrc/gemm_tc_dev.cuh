@@ -301,6 +301,7 @@ struct KParams {
   int tail_full;        //   computed as two K-halves each, reduce-added into the zeroed fp32 output
   int batch;            // independent GEMMs (bmm lanes), >= 1
   long long so_f32, so_lp;  // batch strides of out_f32 / out_bf16 (elements)
+  int tma_o2 = 0;           // BIAS_ACT_SEED: out2 through TMA (its map in the fp32 output's slot)
   // CTA-pair kernel, splits > 1: per (tile, epilogue-warp region) arrival
   // counters (zeroed) -- the last split to arrive sums the partials in split
   // order and writes the output (no separate reduce launch)
@@ -445,7 +446,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     // rows past M: zeros for the column sums; TMA clips them on store
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-  } else if (e.mode == SG_EPI_BIAS_ACT) {
+  } else if (e.mode == SG_EPI_BIAS_ACT || e.mode == SG_EPI_BIAS_ACT_SEED) {
     if (e.bias) {
       float bv[32];
       if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
@@ -479,7 +480,8 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       act_grad_chunk(v, h, e.act);
     }
   }
-  if (e.mode == SG_EPI_BIAS_ACT && e.act == SG_ACT_SIGMOID && e.dom) {  // warp-uniform
+  if ((e.mode == SG_EPI_BIAS_ACT || e.mode == SG_EPI_BIAS_ACT_SEED) && e.act == SG_ACT_SIGMOID &&
+      e.dom) {  // warp-uniform
     if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(e.dom, (unsigned)SG_DOM_EXP_OVERFLOW);
   }
   SG_CPROF(2);  // epilogue math
@@ -509,6 +511,27 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   if (e.out_bf16) {
     if (p.tma_lp) warp_tma_store<true>(sbuf16, map_lp, v, lane, n0, row0, bidx, false, alt);
     else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
+  }
+  if (e.mode == SG_EPI_BIAS_ACT_SEED) {
+    // the activation's cotangent: dz = seed .* act'(h) with h the bf16
+    // activation just stored (the value the pullback reads back otherwise)
+    float sd[32];
+    if (row_ok) load_row_f32(e.seed + (long long)m * e.ld_seed + n0, sd, nn);
+    else
+#pragma unroll
+      for (int i = 0; i < 32; ++i) sd[i] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+    act_grad_chunk(sd, v, e.act);  // sd *= act'(h)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = sd[i];
+    // (the fp32 output slot is free in this mode: it carries out2's map)
+    if (p.tma_o2) {
+      warp_tma_store<true>(slot, map_f32, v, lane, n0, row0, bidx);  // buffer 0, after every read of it
+      if (WIDE) *next_buf = 1;
+    } else if (row_ok) {
+      store_row_bf16(e.out2_bf16 + (long long)m * e.ld_out2 + n0, v, nn);
+    }
   }
   SG_CPROF(3);  // stores issued
   // bias gradient: per-32-row column sums (rules.py:45-46 reduce_like); the

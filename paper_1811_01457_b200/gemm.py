@@ -17,7 +17,7 @@ import ctypes
 from . import runtime as rt
 
 PREC = {"bf16": 0, "strict_fp32": 1, "strict_fp64": 2, "tf32": 3}
-EPI = {"store": 0, "bias_act": 1, "act_grad": 2}
+EPI = {"store": 0, "bias_act": 1, "act_grad": 2, "bias_act_seed": 3}
 ACT = {"identity": 0, "sigmoid": 1, "tanh": 2, "relu": 3}
 
 
@@ -36,6 +36,7 @@ class GemmDesc(ctypes.Structure):
         ("batch", ctypes.c_int64),
         ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
         ("stride_out", ctypes.c_int64), ("stride_lp", ctypes.c_int64),
+        ("out2_lp", ctypes.c_void_p), ("ld_out2", ctypes.c_int64),
     ]
 
 
@@ -111,20 +112,23 @@ def check_dtypes(precision: str, operands=(), fp32=(), lp=(), colsum=None) -> No
 
 def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
          epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-         out_pre=None, colsum=None, stream=None):
+         out_pre=None, colsum=None, seed=None, out2_lp=None, stream=None):
     """Launch one GEMM; outputs are written in place into the given tensors.
 
     ``colsum`` (fp32 ``[ceil(M/32)][>=N]``) receives per-32-row column sums of
-    the result (the first stage of a bias gradient).
+    the result (the first stage of a bias gradient).  ``epilogue="bias_act_seed"``
+    (a forward with a known cotangent ``seed`` of its activation, fp32): ``out_lp``
+    = act(z + b) and ``out2_lp`` = seed .* act'(out_lp), with ``colsum`` of the latter.
     """
     d = gemm_desc(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, precision=precision, epilogue=epilogue, act=act,
-                  bias=bias, aux=aux, out=out, out_lp=out_lp, out_pre=out_pre, colsum=colsum)
+                  bias=bias, aux=aux, out=out, out_lp=out_lp, out_pre=out_pre, colsum=colsum, seed=seed,
+                  out2_lp=out2_lp)
     rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
 
 
 def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
               epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-              out_pre=None, colsum=None) -> GemmDesc:
+              out_pre=None, colsum=None, seed=None, out2_lp=None) -> GemmDesc:
     """The validated ``sg_gemm_desc`` of a GEMM (see :func:`gemm`), without launching it."""
     if a_mn:
         Ka, Ma = A.shape
@@ -148,7 +152,20 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
         raise ValueError(f"gemm: bias has {bias.numel()} elements, {N} needed")
     if epilogue == "act_grad" and aux is None:
         raise ValueError("gemm: the act_grad epilogue needs aux (the saved activation)")
-    check_dtypes(precision, operands=(("A", A), ("B", B), ("aux", aux)),
+    if epilogue == "bias_act_seed":
+        import torch
+
+        if precision != "bf16" or seed is None or out_lp is None or out2_lp is None or out is not None:
+            raise ValueError("gemm: bias_act_seed needs bf16, seed, out_lp and out2_lp, and no fp32 out")
+        for name, t in (("seed", seed), ("out2_lp", out2_lp)):
+            if t.dim() != 2 or t.shape[0] < M or t.shape[1] < N:
+                raise ValueError(f"gemm: {name} of shape {tuple(t.shape)} cannot hold the {M} x {N} result")
+        if seed.dtype != torch.float32 or out2_lp.dtype != torch.bfloat16:
+            raise ValueError("gemm: seed must be float32 and out2_lp bfloat16")
+        aux = seed  # the descriptor carries the seed in aux
+    elif seed is not None or out2_lp is not None:
+        raise ValueError("gemm: seed / out2_lp belong to the bias_act_seed epilogue")
+    check_dtypes(precision, operands=(("A", A), ("B", B)) + ((("aux", aux),) if seed is None else ()),
                  fp32=(("out", out), ("out_pre", out_pre), ("bias", bias)), lp=(("out_lp", out_lp),),
                  colsum=colsum)
     if colsum is not None and (colsum.dim() != 2 or colsum.shape[0] < (M + 31) // 32 or colsum.shape[1] < N):
@@ -166,7 +183,8 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
     d.out, d.ld_out = _ptr(out), _ld(out)
     d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
     d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
-    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum)  # the buffers stay alive with the descriptor
+    d.out2_lp, d.ld_out2 = _ptr(out2_lp), _ld(out2_lp)
+    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum, out2_lp)  # the buffers stay alive with the descriptor
     return d
 
 

@@ -491,3 +491,41 @@ np.save(sys.argv[1], np.concatenate([e.G.double().cpu().numpy(), e.loss.cpu().nu
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
             outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520)])
+def test_value_and_pullback_fuses_the_seed(M, D):
+    """DenseLayer.value_and_pullback (the forward GEMM's epilogue also forms
+    dZ = ybar .* act'(H) and its column sums) against the same layer's
+    forward + separate act' + pullback and an fp64 evaluation: c3 at full size
+    and a ragged shape."""
+    g = torch.Generator(device="cuda").manual_seed(M)
+    W = ((torch.rand((D, D), generator=g, device="cuda") * 2 - 1) * (6.0 / (2 * D)) ** 0.5)
+    b = (torch.rand(D, generator=g, device="cuda") * 2 - 1) * 0.01
+    X = (torch.rand((M, D), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    ybar = torch.rand((M, D), generator=g, device="cuda") * 2 - 1
+    outs = []
+    for fused in (False, True):
+        layer = DenseLayer(M, D, D, "sigmoid", precision="bf16")
+        layer.set_params(W.cpu().numpy(), b.cpu().numpy())
+        if fused:
+            H, dX, dW, db = layer.value_and_pullback(ybar, X)
+        else:
+            H = layer.forward(X)
+            dX, dW, db = layer.pullback(ybar)
+        torch.cuda.synchronize()
+        outs.append((H.clone(), layer.dZ.clone(), dX.clone(), dW.clone(), db.clone()))
+    (H0, Z0, X0, W0, b0), (H1, Z1, X1, W1, b1) = outs
+    assert torch.equal(H0, H1)
+    assert torch.equal(Z0, Z1)  # dZ from the same bf16 H: identical values
+    x64, w64 = X.double(), layer.Wb.double()
+    s = torch.sigmoid(x64 @ w64.T + b.double())
+    dz = ybar.double() * s * (1 - s)
+
+    def nrel_t(u, v):
+        return float((u.double() - v).abs().max() / v.abs().max())
+
+    assert nrel_t(X1, dz @ w64) <= 1e-2
+    assert nrel_t(W1, dz.T @ x64) <= 1e-2
+    assert nrel_t(b1, dz.sum(0)) <= 1e-2
+    assert nrel_t(b1, b0.double()) <= 1e-5  # db: partial sums in another order only
