@@ -56,7 +56,7 @@ constexpr int SLOTS = 2 * EPI_WARPS;                     // epilogue warps per p
 struct Maps {
   CUtensorMap a, b, lp, f32, aux;
 };
-constexpr int MAX_PROBS = 96;
+constexpr int MAX_PROBS = 84;  // the problems live in the 32 KB kernel parameter space
 
 struct Problem {
   KParams p;
@@ -440,7 +440,7 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
   if (!ctx || !probs || !out || n <= 0) return fail(SG_EINVAL, "chain: null argument or empty chain");
   if (int rc = ctx_activate(ctx)) return rc;
   const int pairs = std::max(1, ctx_compute_sms(ctx) / 2);
-  if (n > chain::MAX_PROBS) return fail(SG_EINVAL, "chain: at most 96 GEMMs per chain");
+  if (n > chain::MAX_PROBS) return fail(SG_EINVAL, "chain: at most 84 GEMMs per chain");
   std::vector<chain::Problem> hp(n);
   std::vector<chain::Maps> hm(n);
   long long n_cnt = 0, n_split = 0, n_part = 0;
