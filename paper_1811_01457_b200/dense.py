@@ -484,6 +484,11 @@ class ChainEngine:
         else:
             self.dZ = [torch.zeros((B, _ld(dmax)), dtype=self.adt, device=dev) for _ in range(2)]
             self.colsum = torch.zeros(((B + 31) // 32, _ld(dmax)), dtype=torch.float32, device=dev)
+            if precision == "bf16" and self.L >= 2:
+                # per-layer bias-gradient partials: every db finalised in one
+                # launch after the pullback (deferred_db) instead of one per layer
+                self.csl = [torch.zeros(((B + 31) // 32, _ld(d)), dtype=torch.float32, device=dev)
+                            for d in self.sizes[1:]]
         self.dH = torch.zeros((B, _ld(dL)), dtype=self.mdt, device=dev)[:, :dL]
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         n_part = max(1, ((dmax + 31) // 32) * ((B + 31) // 32))
@@ -523,7 +528,18 @@ class ChainEngine:
         """Per-32-row column-sum partials of dz_of(l) (tensor-core precisions)."""
         if not self.tc:
             return None
-        return self.csl[l] if self.chainable else self.colsum
+        return self.csl[l] if hasattr(self, "csl") else self.colsum
+
+    def _deferred_db(self) -> bool:
+        """bf16 pullback without per-layer hooks: dW and dX per layer, every db
+        finalised at the end in one launch (sg_colsum_finalize_multi) -- the
+        same kernels and arithmetic as sg_dense_backward, 15 launches fewer on
+        c5.  Off under data parallelism: a bucket's db must be final when the
+        pullback readies it."""
+        import os
+
+        return (hasattr(self, "csl") and self.grad_ready is None and self.l0_slices <= 1
+                and os.environ.get("SGB200_DEFER_DB", "1") != "0")
 
     # ------------------------------------------------------------- inputs
     def load_batch(self, X, Y) -> None:
@@ -632,15 +648,8 @@ class ChainEngine:
         add_dw(0)
         return GemmChain(fwd), GemmChain(bwd)
 
-    def _chain_backward(self, _ctx):
-        """Chained pullback: every layer's dX (with the lower layer's act' and
-        bias-gradient partials fused) and dW in one launch -- or, pairwise, one
-        launch per layer -- then every db."""
-        if self.chain_mode == "pairwise":
-            for l in range(self.L - 1, -1, -1):
-                self.chains[1][l].run()
-        else:
-            self.chains[1].run()
+    def _finalize_all_db(self):
+        """db_l = sum of dz_l's per-32-row partials, every layer in one launch."""
         lib = _lib()
         n = self.L
         parts = (ctypes.c_void_p * n)(*[_p(self.cs_of(l)) for l in range(n)])
@@ -650,6 +659,17 @@ class ChainEngine:
         N = (ctypes.c_int64 * n)(*[self.sizes[l + 1] for l in range(n)])
         rt.check(lib.sg_colsum_finalize_multi(rt.context(), n, parts, G, ld, N, outs, rt.stream_ptr()),
                  "sg_colsum_finalize_multi")
+
+    def _chain_backward(self, _ctx):
+        """Chained pullback: every layer's dX (with the lower layer's act' and
+        bias-gradient partials fused) and dW in one launch -- or, pairwise, one
+        launch per layer -- then every db."""
+        if self.chain_mode == "pairwise":
+            for l in range(self.L - 1, -1, -1):
+                self.chains[1][l].run()
+        else:
+            self.chains[1].run()
+        self._finalize_all_db()
 
     def _ready(self, l):
         def cb(_entry):
@@ -723,6 +743,19 @@ class ChainEngine:
                                    colsum_in=None if cs is None else cs[:, r])
                     if self.grad_ready is not None:
                         self.grad_ready(bucket_of_layer(0, S, k))
+                return
+            if self._deferred_db():
+                # the two GEMMs of sg_dense_backward (rules.py:113-115, 82-94);
+                # db of every layer after layer 0's (rules.py:45-46)
+                from .gemm import gemm
+
+                gemm(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l])
+                if l > 0:
+                    act_prev = self.acts[l - 1]
+                    gemm(dz, self.Ws[l], b_mn=True, epilogue="store" if act_prev == "identity" else "act_grad",
+                         act=act_prev, aux=self.H[l], out_lp=self.dz_of(l - 1), colsum=self.cs_of(l - 1))
+                else:
+                    self._finalize_all_db()
                 return
             # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
             # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below
