@@ -143,6 +143,14 @@ SG_API int sg_ew_variant_count(sg_kernel* kern);
  * seed is fp32 [M][ld_seed] passed in `aux`/`ld_aux`.  BF16 precision, no
  * fp32 `out`; replaces a separate act' pass over the seed. */
 #define SG_EPI_BIAS_ACT_SEED 3
+/* The MSE loss of a linear top layer in its own epilogue (training step,
+ * loss = scale * sum (z - y)^2, z = x W^T + b): reads the
+ * targets y (fp32, in `aux`/`ld_aux`), writes dz = 2 (z - y) scale as bf16 to
+ * out2_lp (+ its column sums into colsum) and per-(32-row group, 32-column
+ * chunk) partial losses to loss_part[group * ceil(N/32) + chunk] (f64, summed
+ * in a fixed order by sg_sum_f64); z itself is written only if `out` is given.
+ * BF16 precision, identity activation; `colsum` ld = ld_colsum. */
+#define SG_EPI_BIAS_MSE 4
 
 #define SG_ACT_IDENTITY 0
 #define SG_ACT_SIGMOID 1
@@ -179,8 +187,10 @@ typedef struct sg_gemm_desc {
    * take the STORE / BIAS_ACT epilogues (bias shared) without colsum/out_pre. */
   int64_t batch;
   int64_t stride_a, stride_b, stride_out, stride_lp;
-  void* out2_lp; /* BIAS_ACT_SEED: bf16 [M][ld_out2] seed .* act'(out_lp) */
+  void* out2_lp; /* BIAS_ACT_SEED: bf16 [M][ld_out2] seed .* act'(out_lp); BIAS_MSE: dz */
   int64_t ld_out2;
+  double* loss_part; /* BIAS_MSE: [ceil(M/32)][ceil(N/32)] partial losses */
+  double loss_scale; /* BIAS_MSE: scale (1 / global batch) */
 } sg_gemm_desc;
 
 SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);
@@ -221,6 +231,8 @@ SG_API int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int6
                    int64_t ld_y, int64_t M, int64_t N, double scale, double* loss, double* loss_part,
                    int64_t n_part, void* dz, int32_t dz_dtype, int64_t ld_dz, void* dz2, int32_t dz2_dtype,
                    int64_t ld_dz2, float* colsum, int64_t ld_colsum, void* stream);
+/* *out = sum of part[0..n) in a fixed order (f64): the partial losses of BIAS_MSE. */
+SG_API int sg_sum_f64(sg_ctx* ctx, const double* part, int64_t n, double* out, void* stream);
 /* params -= lr * grads over the flat parameter buffer (nn_train.py:365-372);
  * optional bf16 shadow copy of the updated parameters for the next GEMMs. */
 SG_API int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t n, double lr,

@@ -986,4 +986,13 @@ int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, 
   return SG_OK;
 }
 
+int sg_sum_f64(sg_ctx* ctx, const double* part, int64_t n, double* out, void* stream) {
+  if (!ctx || !part || !out) return fail(SG_EINVAL, "null argument");
+  if (n <= 0) return fail(SG_EINVAL, "sum_f64: empty");
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  SG_CUDA_TRY(pdl_launch(dk::k_sum_loss, dim3(1), dim3(256), 0, (cudaStream_t)stream, part, (long long)n, out));
+  return SG_OK;
+}
+
 }  // extern "C"

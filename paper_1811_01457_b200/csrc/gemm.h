@@ -27,8 +27,10 @@ struct GemmEpilogue {
   unsigned* dom = nullptr;     // domain flags (SG_DOM_*): sigmoid pre-activations that overflow the reference
   const float* seed = nullptr; // BIAS_ACT_SEED: cotangent of the activation, fp32 [M][ld_seed]
   long long ld_seed = 0;
-  __nv_bfloat16* out2_bf16 = nullptr;  // BIAS_ACT_SEED: seed .* act'(h), bf16 [M][ld_out2]
+  __nv_bfloat16* out2_bf16 = nullptr;  // BIAS_ACT_SEED: seed .* act'(h); BIAS_MSE: dz; bf16 [M][ld_out2]
   long long ld_out2 = 0;
+  double* loss_part = nullptr;          // BIAS_MSE: [ceil(M/32)][ceil(N/32)] partial losses
+  float loss_scale = 0.0f;
 };
 
 // Column sums of a 32x32 block held one row per lane (v[i] = column i):

@@ -512,7 +512,7 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
     splits = (pr.num_kb + kb_per - 1) / kb_per;
     pr.p = tc::KParams{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, 1, 0, 0};
     tcmap::out_maps(g, pr.p, mp.lp, mp.f32);
-    tcmap::aux_map(g, pr.p, mp.aux);
+    tcmap::aux_map(g, pr.p, mp.aux, false);
     if (splits > 1) {
       pr.p.ld_part = (g.N + 3) / 4 * 4;
       part_off[i] = n_part;

@@ -18,7 +18,11 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
       d->K > (1ll << 31) - 1)
     return fail(SG_EINVAL, "gemm: bad extents");
   if (d->M == 0 || d->N == 0) return SG_OK;
-  if (d->epilogue < SG_EPI_STORE || d->epilogue > SG_EPI_BIAS_ACT_SEED) return fail(SG_EINVAL, "gemm: bad epilogue");
+  if (d->epilogue < SG_EPI_STORE || d->epilogue > SG_EPI_BIAS_MSE) return fail(SG_EINVAL, "gemm: bad epilogue");
+  if (d->epilogue == SG_EPI_BIAS_MSE &&
+      (d->precision != SG_PREC_BF16 || !d->aux || !d->out2_lp || !d->loss_part || d->act != SG_ACT_IDENTITY ||
+       d->out_lp || d->batch > 1))
+    return fail(SG_EINVAL, "gemm: BIAS_MSE needs BF16, identity, targets in aux, out2_lp and loss_part, no out_lp");
   if (d->epilogue == SG_EPI_BIAS_ACT_SEED &&
       (d->precision != SG_PREC_BF16 || !d->aux || !d->out_lp || !d->out2_lp || d->out || d->batch > 1))
     return fail(SG_EINVAL, "gemm: BIAS_ACT_SEED needs BF16, the seed in aux, out_lp and out2_lp, and no fp32 out");
@@ -78,6 +82,15 @@ void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g) {
   g.epi.colsum = d->colsum;
   g.epi.ld_colsum = d->ld_colsum;
   g.epi.dom = ctx_domain_word(ctx);
+  if (d->epilogue == SG_EPI_BIAS_MSE) {
+    g.epi.aux = nullptr;  // the targets travel in aux (fp32)
+    g.epi.seed = (const float*)d->aux;
+    g.epi.ld_seed = d->ld_aux;
+    g.epi.out2_bf16 = (__nv_bfloat16*)d->out2_lp;
+    g.epi.ld_out2 = d->ld_out2;
+    g.epi.loss_part = d->loss_part;
+    g.epi.loss_scale = (float)d->loss_scale;
+  }
   if (d->epilogue == SG_EPI_BIAS_ACT_SEED) {
     g.epi.aux = nullptr;  // the seed travels in aux: fp32, read per row in the epilogue
     g.epi.seed = (const float*)d->aux;

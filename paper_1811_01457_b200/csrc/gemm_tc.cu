@@ -431,7 +431,8 @@ gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_cons
       const int row0 = tc.m0 + (int)rank * HALF + q * 32;
       const int c0 = half * CH_PER;
       const bool staged = p.aux_stage && row0 < p.M;  // warp-uniform
-      epi_aux_prologue<WIDE>(staged, lane, slot, &tma_aux, my_aux, tc.n0 + c0 * 32, CH_PER, p.N, row0);
+      epi_aux_prologue<WIDE>(staged, lane, slot, &tma_aux, my_aux, tc.n0 + c0 * 32, CH_PER, p.N, row0,
+                             p.aux_stage == 2);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane == 0) SG_TRACE(it, 1);  // accumulator complete
@@ -548,7 +549,11 @@ bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, lon
 
 // ACT_GRAD with a bf16 saved activation and a bf16-only output: the aux
 // blocks are TMA-streamed through the free half of each staging slot.
-void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m) {
+// BIAS_MSE in the wide-slot kernel (wide = true): the fp32 targets, 4 KB
+// blocks through the slot's upper half, one chunk ahead (dz is staged in
+// the lower half; no fp32 output shares the slot).  Measured on B200: a
+// second target buffer with dz stored from registers instead is slower.
+void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m, bool wide) {
   std::memset(&m, 0, sizeof m);
   p.aux_stage = 0;
   static const bool enabled = [] {
@@ -556,6 +561,22 @@ void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m) {
     return !(e && e[0] == '0');
   }();
   const GemmEpilogue& e = g.epi;
+  if (e.mode == SG_EPI_BIAS_MSE) {
+    if (!enabled || !wide || e.out_f32 || !e.seed || p.splits > 1 || g.batch > 1 ||
+        (reinterpret_cast<uintptr_t>(e.seed) & 15) || (e.ld_seed * 4) % 16)
+      return;
+    EncodeTiled enc = encode_fn();
+    if (!enc) return;
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)(e.ld_seed * 4), (cuuint64_t)(e.ld_seed * 4 * g.M)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(e.seed), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    p.aux_stage = r == CUDA_SUCCESS ? 2 : 0;
+    return;
+  }
   if (!enabled || e.mode != SG_EPI_ACT_GRAD || !e.aux || e.aux_f32 || e.out_f32 || !p.tma_lp || p.splits > 1 ||
       g.batch > 1 || (reinterpret_cast<uintptr_t>(e.aux) & 15) || (e.ld_aux * 2) % 16)
     return;
@@ -584,8 +605,8 @@ void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& 
     p.tma_lp = make_out_map(&mlp, g.epi.out_bf16, true, g.N, g.M, g.epi.ld_bf16, g.batch, g.so_lp);
   if (g.epi.out_f32)
     p.tma_f32 = make_out_map(&mf32, g.epi.out_f32, false, g.N, g.M, g.epi.ld_f32, g.batch, g.so_f32);
-  else if (g.epi.mode == SG_EPI_BIAS_ACT_SEED && g.epi.out2_bf16)  // out2 (bf16) in the fp32 map's slot
-    p.tma_o2 = make_out_map(&mf32, g.epi.out2_bf16, true, g.N, g.M, g.epi.ld_out2, 1, 0);
+  else if ((g.epi.mode == SG_EPI_BIAS_ACT_SEED || g.epi.mode == SG_EPI_BIAS_MSE) && g.epi.out2_bf16)
+    p.tma_o2 = make_out_map(&mf32, g.epi.out2_bf16, true, g.N, g.M, g.epi.ld_out2, 1, 0);  // out2 in the fp32 slot
 }
 
 }  // namespace tcmap
@@ -696,7 +717,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
-  aux_map(g, p, maux);
+  aux_map(g, p, maux, false);
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
@@ -755,7 +776,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
   out_maps(g, p, mlp, mf32);
-  aux_map(g, p, maux);
+  aux_map(g, p, maux, WIDE);
   float* part = nullptr;
   unsigned* cnt = nullptr;
   // In-kernel split-K fix-up (SGB200_GEMM_SPLIT_FIXUP=1): measured slower on
@@ -857,7 +878,8 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
     return e && e[0] == '1';
   }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
-    if (wide) {
+    // the fused MSE loss streams its fp32 targets through the wide slots
+    if (wide || (g.epi.mode == SG_EPI_BIAS_MSE && !g.epi.out_f32)) {
       if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, true>(g, num_sms, st);
       if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, true>(g, num_sms, st);
       if (g.a_mn && g.b_mn) return run_pair<TF32, true, true, true>(g, num_sms, st);
@@ -882,6 +904,18 @@ extern "C" SG_API int sg_gemm_trace_buffer(void* buf, int iters, int launches) {
   SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_launches, &launches, sizeof launches));
   SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_seq, &zero, sizeof zero));
   SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_trace_done, &zero, sizeof zero));
+  return SG_OK;
+}
+// epilogue stage profile of the single-GEMM kernels (sg_chain_cprof's twin):
+// on != 0 clears and enables, on == 0 disables and reads out 8 counters
+extern "C" SG_API int sg_gemm_cprof(int on, unsigned long long* out8) {
+  if (on) {
+    unsigned long long z[8] = {};
+    SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_cprof, z, sizeof z));
+  } else if (out8) {
+    SG_CUDA_TRY(cudaMemcpyFromSymbol(out8, tc::g_cprof, 8 * sizeof(unsigned long long)));
+  }
+  SG_CUDA_TRY(cudaMemcpyToSymbol(tc::g_cprof_on, &on, sizeof on));
   return SG_OK;
 }
 #endif

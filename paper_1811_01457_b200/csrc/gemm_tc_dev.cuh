@@ -251,7 +251,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // 32 x 32 chunk, summed over the lane-0 threads of the first 8 CTAs.
 #ifdef SGB200_GEMM_TRACE
 __device__ unsigned long long g_cprof[8];
-__device__ int g_cprof_on = 0;
+__constant__ int g_cprof_on = 0;  // constant cache: the check adds no global-load latency
 #define SG_CPROF_START() long long cprof_t = clock64()
 #define SG_CPROF(k)                                                                  \
   do {                                                                               \
@@ -295,7 +295,8 @@ struct KParams {
   float* part;        // [splits][M][ld_part] when splits > 1
   long long ld_part;
   int tma_lp, tma_f32;  // outputs written through smem staging + TMA bulk stores
-  int aux_stage;        // ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot
+  int aux_stage;        // 1: ACT_GRAD bf16 aux streamed by TMA into the upper half of each staging slot;
+                        // 2: BIAS_MSE fp32 targets, 4 KB blocks in the wide slot's upper half
   int raster;           // CTA-pair kernel: M-tiles per raster group
   int tail_split;       // CTA-pair kernel, > 0: tiles are taken row-major; the last tail_split tiles are
   int tail_full;        //   computed as two K-halves each, reduce-added into the zeroed fp32 output
@@ -396,8 +397,9 @@ __device__ __forceinline__ void warp_tma_store(uint8_t* slot, const CUtensorMap*
 // staging slot, so the next chunk's block is in flight while this one is
 // processed (and the tile's first block while the accumulator is computed).
 constexpr int AUX_OFF = 2048;
-__device__ __forceinline__ void aux_issue(uint8_t* slot, const CUtensorMap* map, uint64_t* bar, int n0, int row0) {
-  mbar_expect_tx(bar, 2048);
+__device__ __forceinline__ void aux_issue(uint8_t* slot, const CUtensorMap* map, uint64_t* bar, int n0, int row0,
+                                          uint32_t bytes = 2048) {
+  mbar_expect_tx(bar, bytes);
   tma_load_3d(slot + AUX_OFF, map, bar, n0, row0, 0);
 }
 __device__ __forceinline__ void aux_read(const uint8_t* slot, float (&h)[32], int lane) {
@@ -426,12 +428,29 @@ __device__ __forceinline__ uint8_t* stage_buf(uint8_t* slot, int b) {
 // One 32x32 accumulator chunk (row m per lane, columns n0..n0+31) through the
 // fused epilogue.  `grp` is the 32-row group (bias-gradient partial row),
 // `grp_ok` whether that group has any row < M.  Warp-collective (shuffles).
+// BIAS_MSE targets staged in shared memory (aux_stage == 2): the block of
+// this chunk (shared-window address, 0: not staged) and what to issue into
+// the buffer once it has been read.  Passed by value (registers).
+struct YStage {
+  uint32_t sm;    // smem address of the 4 KB block (aux_base_wide(slot, 0) + AUX_OFF)
+  uint8_t* base;  // aux_base_wide(slot, 0), for aux_issue
+  const CUtensorMap* map;
+  uint64_t* bar;
+  int next_n0;  // < 0: no next block
+  int row0;
+};
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+  return r;
+}
+
 template <bool WIDE = false>
 __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int m, bool row_ok, int grp,
                                           bool grp_ok, int n0, int lane, int split, int bidx, bool hstaged,
                                           const float (&hs)[32], uint8_t* slot, bool radd,
                                           const CUtensorMap* map_lp, const CUtensorMap* map_f32,
-                                          int* next_buf = nullptr) {
+                                          int* next_buf = nullptr, YStage ys = YStage{}) {
   SG_CPROF_START();
   const GemmEpilogue& e = p.epi;
   const bool full = n0 + 32 <= p.N;
@@ -446,7 +465,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     // rows past M: zeros for the column sums; TMA clips them on store
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-  } else if (e.mode == SG_EPI_BIAS_ACT || e.mode == SG_EPI_BIAS_ACT_SEED) {
+  } else if (e.mode == SG_EPI_BIAS_ACT || e.mode == SG_EPI_BIAS_ACT_SEED || e.mode == SG_EPI_BIAS_MSE) {
     if (e.bias) {
       float bv[32];
       if (full && (reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0) {
@@ -461,6 +480,7 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] += bv[i];
+      SG_CPROF(6);  // bias loaded and added
     }
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
     if (e.act == SG_ACT_SIGMOID) {
@@ -511,6 +531,64 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
   if (e.out_bf16) {
     if (p.tma_lp) warp_tma_store<true>(sbuf16, map_lp, v, lane, n0, row0, bidx, false, alt);
     else if (row_ok) store_row_bf16(e.out_bf16 + bidx * p.so_lp + (long long)m * e.ld_bf16 + n0, v, nn);
+  }
+  if (e.mode == SG_EPI_BIAS_MSE) {
+    // the MSE loss of the linear top layer (k_mse's arithmetic): d = z - y,
+    // loss += d^2, dz = d scale + d scale
+    // (rules.py:53-58 on mul(d, d)).  Targets: the TMA-staged block, else
+    // this lane's row from global memory -- 4 at a time, so no second
+    // 32-float row is live beside the accumulator.
+    const float* yrow = e.seed + (long long)m * e.ld_seed + n0;
+    const bool yvec = full && (reinterpret_cast<uintptr_t>(yrow) & 15) == 0;
+    // loss: fp32 within the 32 x 32 block (a pairwise tree: sums of 8 per
+    // lane, then the warp butterfly), fp64 across blocks (sg_sum_f64) --
+    // fp64 arithmetic here would sit on the epilogue's critical path
+    float l = 0.0f, l8 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float4 y;
+      if (ys.sm) {  // SWIZZLE_128B: chunk c of row `lane` at c ^ (lane & 7)
+        y = lds_f4(ys.sm + lane * 128 + ((c ^ (lane & 7)) << 4));
+      } else if (row_ok && yvec) {
+        y = __ldg(reinterpret_cast<const float4*>(yrow + 4 * c));
+      } else {
+        y.x = row_ok && 4 * c < nn ? __ldg(yrow + 4 * c) : 0.0f;
+        y.y = row_ok && 4 * c + 1 < nn ? __ldg(yrow + 4 * c + 1) : 0.0f;
+        y.z = row_ok && 4 * c + 2 < nn ? __ldg(yrow + 4 * c + 2) : 0.0f;
+        y.w = row_ok && 4 * c + 3 < nn ? __ldg(yrow + 4 * c + 3) : 0.0f;
+      }
+      const float yy[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = 4 * c + k;
+        const float d = (row_ok && i < nn) ? v[i] - yy[k] : 0.0f;
+        l8 += d * d;
+        v[i] = d * e.loss_scale + d * e.loss_scale;
+      }
+      if (c & 1) {
+        l += l8;
+        l8 = 0.0f;
+      }
+    }
+    SG_CPROF(5);  // targets read, dz formed
+    if (ys.sm) {  // the block is read: the buffer takes the next one
+#ifndef SG_NO_AUX_FENCE
+      fence_proxy_async();
+#endif
+      __syncwarp();
+      if (lane == 0 && ys.next_n0 >= 0) aux_issue(ys.base, ys.map, ys.bar, ys.next_n0, ys.row0, 4096);
+    }
+    SG_CPROF(6);  // next block issued
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) e.loss_part[(long long)grp * ((p.N + 31) / 32) + n0 / 32] = (double)l * (double)e.loss_scale;
+    SG_CPROF(7);  // loss partial reduced and stored
+    if (p.tma_o2) {
+      warp_tma_store<true>(slot, map_f32, v, lane, n0, row0, bidx);
+      if (WIDE) *next_buf = 1;
+    } else if (row_ok) {
+      store_row_bf16(e.out2_bf16 + (long long)m * e.ld_out2 + n0, v, nn);
+    }
   }
   if (e.mode == SG_EPI_BIAS_ACT_SEED) {
     // the activation's cotangent: dz = seed .* act'(h) with h the bf16
@@ -708,8 +786,13 @@ __device__ __forceinline__ void colsum_finalize_tail(const KParams& p, double* r
 // parity bit per aux buffer.
 template <bool WIDE>
 __device__ __forceinline__ void epi_aux_prologue(bool staged, int lane, uint8_t* slot, const CUtensorMap* map_aux,
-                                                 uint64_t* aux_bars, int n_first, int nch, int N, int row0) {
+                                                 uint64_t* aux_bars, int n_first, int nch, int N, int row0,
+                                                 bool y32 = false) {
   if (!staged || lane != 0) return;
+  if (WIDE && y32) {  // one 4 KB fp32 buffer (the slot's upper half), one chunk ahead
+    if (n_first < N) aux_issue(aux_base_wide(slot, 0), map_aux, &aux_bars[0], n_first, row0, 4096);
+    return;
+  }
   if (n_first < N) aux_issue(WIDE ? aux_base_wide(slot, 0) : slot, map_aux, &aux_bars[0], n_first, row0);
   if (WIDE && nch > 1 && n_first + 32 < N) aux_issue(aux_base_wide(slot, 1), map_aux, &aux_bars[1], n_first + 32, row0);
 }
@@ -731,21 +814,32 @@ __device__ __forceinline__ void epi_chunks(const KParams& p, uint32_t tmem_row, 
     SG_CPROF(0);  // TMEM load
     if (n0 >= p.N) continue;  // warp-uniform; later chunks are past N as well
     float h[32];
-    if (staged) {
+    const bool y32 = WIDE && staged && p.aux_stage == 2;  // fp32 targets (warp-uniform)
+    YStage ys{};
+    if (y32) {  // the epilogue reads the block itself and re-issues the buffer
+      mbar_wait(&aux_bars[0], aux_phase & 1);
+      aux_phase ^= 1u;
+      SG_CPROF(1);
+      uint8_t* base = aux_base_wide(slot, 0);
+      ys = {smem_u32(base + AUX_OFF), base, map_aux, &aux_bars[0], (j + 1 < nch && n0 + 32 < p.N) ? n0 + 32 : -1,
+            row0};
+    } else if (staged) {
       const int b = WIDE ? (j & 1) : 0;
       mbar_wait(&aux_bars[b], (aux_phase >> b) & 1);
       aux_phase ^= 1u << b;
       SG_CPROF(1);  // saved activation block arrived
       uint8_t* base = WIDE ? aux_base_wide(slot, b) : slot;
       aux_read(base, h, lane);
+#ifndef SG_NO_AUX_FENCE
       fence_proxy_async();  // our reads precede the next async write of the buffer
+#endif
       __syncwarp();
       const int ahead = WIDE ? 2 : 1;
       if (lane == 0 && j + ahead < nch && n0 + 32 * ahead < p.N)
         aux_issue(base, map_aux, &aux_bars[b], n0 + 32 * ahead, row0);
     }
-    epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, staged, h, slot, radd, map_lp,
-                    map_f32, &next_buf);
+    epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, staged && !y32, h, slot, radd,
+                    map_lp, map_f32, &next_buf, ys);
   }
 }
 
@@ -757,7 +851,7 @@ int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer
              bool tf32, bool mn_major, int batch, long long sbatch);
 bool make_out_map(CUtensorMap* map, const void* ptr, bool bf16, long long N, long long M, long long ld, int batch,
                   long long sbatch);
-void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m);
+void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m, bool wide);
 void out_maps(const GemmArgs& g, tc::KParams& p, CUtensorMap& mlp, CUtensorMap& mf32);
 }  // namespace tcmap
 

@@ -141,10 +141,11 @@ def _lib():
         lib.sg_mlp_small_step.argtypes = [P, P, P, P, P, P, I64, P, I64, P, I64, P, P, I64, P]
         lib.sg_cast.argtypes = [P, P, I32, P, I32, I64, P]
         lib.sg_cast_2d.argtypes = [P, P, I32, I64, P, I32, I64, I64, I64, P]
+        lib.sg_sum_f64.argtypes = [P, P, I64, P, P]
         lib.sg_dense_forward.argtypes = [P, ctypes.POINTER(DenseDesc), P, I64, P, I64, P, I64, P]
         lib.sg_dense_backward.argtypes = [P, ctypes.POINTER(DenseDesc), ctypes.POINTER(DenseGrad), P]
         for n in ("sg_act_grad", "sg_colsum_finalize", "sg_colsum_finalize_multi", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d",
-                  "sg_dense_forward", "sg_dense_backward"):
+                  "sg_sum_f64", "sg_dense_forward", "sg_dense_backward"):
             getattr(lib, n).restype = ctypes.c_int
         _bound = True
     return lib
@@ -495,6 +496,13 @@ class ChainEngine:
         self.loss_part = torch.zeros(n_part, dtype=torch.float64, device=dev)
         self.descs = [dense_desc(self.H[l], self.Ws[l] if precision == "bf16" else self.W[l], self.b[l],
                                  self.acts[l], precision) for l in range(self.L)]
+        # bf16 + MSE + linear top layer: the training step computes the loss and
+        # its seed dz in the top GEMM's epilogue (SG_EPI_BIAS_MSE) -- the fp32
+        # top outputs are neither written nor read back (forward(fuse_loss=True));
+        # SGB200_FUSED_LOSS=0 keeps the separate loss kernel
+        self.fused_mse = (precision == "bf16" and loss == "mse" and self.acts[-1] == "identity"
+                          and os.environ.get("SGB200_FUSED_LOSS", "1") != "0")
+        self._loss_fused = False
         self.tape = Tape()
         self.grad_ready = None  # optional callback(bucket_index) when a bucket's gradients are written
         self.l0_slices = 1      # data parallel: layer 0's dW in row slices (enable_first_layer_slices)
@@ -560,9 +568,28 @@ class ChainEngine:
             self.Yin = self.Y
 
     # ------------------------------------------------------------ forward
-    def forward(self):
-        """Record the forward pass on the tape; returns the top-layer outputs."""
+    def _top_forward_mse(self):
+        """The top layer's forward GEMM with the MSE loss in its epilogue:
+        dz_top = 2 (z - y) scale and its bias-gradient partials, the loss as
+        per-block partials (summed by loss_and_seed).  z is not stored."""
+        from .gemm import gemm
+
+        top = self.L - 1
+        Y = getattr(self, "Yin", None)
+        Y = self.Y if Y is None else Y
+        gemm(self.H[top], self.Ws[top], epilogue="bias_mse", bias=self.b[top], seed=Y,
+             out2_lp=self.dz_of(top), colsum=self.cs_of(top), loss_part=self.loss_part, loss_scale=self.scale)
+        self._loss_fused = True
+
+    def forward(self, fuse_loss: bool = False):
+        """Record the forward pass on the tape; returns the top-layer outputs.
+        ``fuse_loss`` (training steps): when the engine fuses its loss
+        (``fused_mse``), the top layer computes the loss and its seed instead
+        of its outputs -- the return value is then None and loss_and_seed only
+        sums the loss partials."""
         self.tape.clear()
+        self._loss_fused = False
+        fuse = fuse_loss and self.fused_mse
         use_chain = self._use_chain()
         if use_chain and self.chain_mode == "full":
             self.chains[0].run()
@@ -574,18 +601,23 @@ class ChainEngine:
         if use_chain:  # pairwise: per-layer forward GEMMs, the pullback in L launches
             for l in range(L):
                 last = l == L - 1
-                dense_forward(self.descs[l], H=None if last else self.H[l + 1], H_f32=self.Zt if last else None)
+                if last and fuse:
+                    self._top_forward_mse()
+                else:
+                    dense_forward(self.descs[l], H=None if last else self.H[l + 1], H_f32=self.Zt if last else None)
             self.tape.push(TapeEntry("dense_pairwise", tuple(self.H) + tuple(self.W), self._chain_backward, None))
-            return self.Zt
+            return None if fuse else self.Zt
         for l in range(L):
             last = l == L - 1
-            if self.precision == "bf16":
+            if last and fuse:
+                self._top_forward_mse()
+            elif self.precision == "bf16":
                 dense_forward(self.descs[l], H=None if last else self.H[l + 1], H_f32=self.Zt if last else None)
             else:
                 dense_forward(self.descs[l], H=self.Zt if last else self.H[l + 1])
             self.tape.push(TapeEntry(f"dense{l}", (self.H[l], self.W[l]),
                                      self._make_backward(l), self._ready(l)))
-        return self.Zt
+        return None if fuse else self.Zt
 
     def _use_chain(self) -> bool:
         """Chains run when this engine can use them and no per-layer hooks are
@@ -705,6 +737,10 @@ class ChainEngine:
         ctx, st = rt.context(), rt.stream_ptr()
         top = self.L - 1
         dL = self.sizes[-1]
+        if self._loss_fused:  # forward(fuse_loss=True) wrote dz and the loss partials
+            n = ((self.B + 31) // 32) * ((dL + 31) // 32)
+            rt.check(lib.sg_sum_f64(ctx, _p(self.loss_part), n, _p(self.loss), st), "sg_sum_f64")
+            return self.loss
         dz = self.dz_of(top)
         cs = self.cs_of(top)
         ident = self.acts[top] == "identity"
@@ -850,7 +886,7 @@ class ChainEngine:
 
     def step(self, lr: float):
         """forward + loss + pullback + SGD on the loaded batch (all device-side)."""
-        self.forward()
+        self.forward(fuse_loss=True)
         self.loss_and_seed()
         self.pullback()
         self.sgd(lr)

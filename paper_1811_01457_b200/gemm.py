@@ -17,7 +17,7 @@ import ctypes
 from . import runtime as rt
 
 PREC = {"bf16": 0, "strict_fp32": 1, "strict_fp64": 2, "tf32": 3}
-EPI = {"store": 0, "bias_act": 1, "act_grad": 2, "bias_act_seed": 3}
+EPI = {"store": 0, "bias_act": 1, "act_grad": 2, "bias_act_seed": 3, "bias_mse": 4}
 ACT = {"identity": 0, "sigmoid": 1, "tanh": 2, "relu": 3}
 
 
@@ -37,6 +37,7 @@ class GemmDesc(ctypes.Structure):
         ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
         ("stride_out", ctypes.c_int64), ("stride_lp", ctypes.c_int64),
         ("out2_lp", ctypes.c_void_p), ("ld_out2", ctypes.c_int64),
+        ("loss_part", ctypes.c_void_p), ("loss_scale", ctypes.c_double),
     ]
 
 
@@ -112,23 +113,26 @@ def check_dtypes(precision: str, operands=(), fp32=(), lp=(), colsum=None) -> No
 
 def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
          epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-         out_pre=None, colsum=None, seed=None, out2_lp=None, stream=None):
+         out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0, stream=None):
     """Launch one GEMM; outputs are written in place into the given tensors.
 
     ``colsum`` (fp32 ``[ceil(M/32)][>=N]``) receives per-32-row column sums of
     the result (the first stage of a bias gradient).  ``epilogue="bias_act_seed"``
     (a forward with a known cotangent ``seed`` of its activation, fp32): ``out_lp``
     = act(z + b) and ``out2_lp`` = seed .* act'(out_lp), with ``colsum`` of the latter.
+    ``epilogue="bias_mse"`` (a linear top layer with its MSE loss, targets
+    ``seed`` fp32): ``out2_lp`` = 2 (z - y) loss_scale (+ ``colsum``), ``loss_part``
+    (f64, ``ceil(M/32) * ceil(N/32)``) the per-block partial losses; ``out`` optional.
     """
     d = gemm_desc(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, precision=precision, epilogue=epilogue, act=act,
                   bias=bias, aux=aux, out=out, out_lp=out_lp, out_pre=out_pre, colsum=colsum, seed=seed,
-                  out2_lp=out2_lp)
+                  out2_lp=out2_lp, loss_part=loss_part, loss_scale=loss_scale)
     rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
 
 
 def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
               epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-              out_pre=None, colsum=None, seed=None, out2_lp=None) -> GemmDesc:
+              out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0) -> GemmDesc:
     """The validated ``sg_gemm_desc`` of a GEMM (see :func:`gemm`), without launching it."""
     if a_mn:
         Ka, Ma = A.shape
@@ -163,8 +167,24 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
         if seed.dtype != torch.float32 or out2_lp.dtype != torch.bfloat16:
             raise ValueError("gemm: seed must be float32 and out2_lp bfloat16")
         aux = seed  # the descriptor carries the seed in aux
+    elif epilogue == "bias_mse":
+        import torch
+
+        if (precision != "bf16" or seed is None or out2_lp is None or loss_part is None or out_lp is not None
+                or act != "identity"):
+            raise ValueError("gemm: bias_mse needs bf16, identity, seed (targets), out2_lp and loss_part, no out_lp")
+        for name, t in (("seed", seed), ("out2_lp", out2_lp)):
+            if t.dim() != 2 or t.shape[0] < M or t.shape[1] < N:
+                raise ValueError(f"gemm: {name} of shape {tuple(t.shape)} cannot hold the {M} x {N} result")
+        if seed.dtype != torch.float32 or out2_lp.dtype != torch.bfloat16 or loss_part.dtype != torch.float64:
+            raise ValueError("gemm: seed must be float32, out2_lp bfloat16 and loss_part float64")
+        if loss_part.numel() < ((M + 31) // 32) * ((N + 31) // 32):
+            raise ValueError(f"gemm: loss_part needs {((M + 31) // 32) * ((N + 31) // 32)} elements")
+        aux = seed
     elif seed is not None or out2_lp is not None:
-        raise ValueError("gemm: seed / out2_lp belong to the bias_act_seed epilogue")
+        raise ValueError("gemm: seed / out2_lp belong to the bias_act_seed / bias_mse epilogues")
+    if loss_part is not None and epilogue != "bias_mse":
+        raise ValueError("gemm: loss_part belongs to the bias_mse epilogue")
     check_dtypes(precision, operands=(("A", A), ("B", B)) + ((("aux", aux),) if seed is None else ()),
                  fp32=(("out", out), ("out_pre", out_pre), ("bias", bias)), lp=(("out_lp", out_lp),),
                  colsum=colsum)
@@ -184,7 +204,8 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
     d.out_lp, d.ld_lp = _ptr(out_lp), _ld(out_lp)
     d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
     d.out2_lp, d.ld_out2 = _ptr(out2_lp), _ld(out2_lp)
-    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum, out2_lp)  # the buffers stay alive with the descriptor
+    d.loss_part, d.loss_scale = _ptr(loss_part), float(loss_scale)
+    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum, out2_lp, loss_part)  # the buffers stay alive with the descriptor
     return d
 
 

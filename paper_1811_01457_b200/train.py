@@ -193,7 +193,7 @@ class Trainer:
 
     def _device_step(self):
         e = self.engine
-        e.forward()
+        e.forward(fuse_loss=True)
         e.loss_and_seed()
         e.pullback()
         if self.dp is not None:
@@ -292,7 +292,7 @@ class Trainer:
         """Loss and parameter gradients without the update (the pullback API)."""
         e = self.engine
         e.load_batch(X, Y)
-        e.forward()
+        e.forward(fuse_loss=True)
         e.loss_and_seed()
         e.pullback()
         if self.dp is not None:

@@ -529,3 +529,41 @@ def test_value_and_pullback_fuses_the_seed(M, D):
     assert nrel_t(W1, dz.T @ x64) <= 1e-2
     assert nrel_t(b1, dz.sum(0)) <= 1e-2
     assert nrel_t(b1, b0.double()) <= 1e-5  # db: partial sums in another order only
+
+
+@pytest.mark.parametrize("sizes,B", [((512, 768, 256), 2048), ((300, 200, 10), 1000), ((64, 96, 33), 70)])
+def test_fused_mse_loss_matches_separate_loss_kernel(sizes, B):
+    """forward(fuse_loss=True) (the MSE loss and its seed dz formed in the
+    top GEMM's epilogue, SG_EPI_BIAS_MSE) against forward() + the separate
+    loss kernel on the same engine and batch: dz is the same arithmetic on the
+    same fp32 z (bit-identical), the loss differs only in its summation order
+    (f64 partials), the bias gradient in the order of its per-32-row column
+    sums.  Ragged widths and batches included."""
+    rng = np.random.default_rng(B)
+    L = len(sizes) - 1
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], "tanh" if i < L - 1 else "identity")
+                    for i in range(L)]).init_params(rng)
+    e = ChainEngine(chain, B, "mse", "bf16", small=False)
+    assert e.fused_mse
+    X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+    outs = []
+    for fuse in (False, True):
+        e.G.zero_()
+        e.load_batch(X, Y)
+        z = e.forward(fuse_loss=fuse)
+        assert (z is None) == fuse
+        e.loss_and_seed()
+        dz = e.dz_of(L - 1).clone()
+        e.pullback()
+        torch.cuda.synchronize()
+        outs.append((float(e.loss.item()), dz, e.G.clone(), [g.clone() for g in e.gb]))
+    (l0, dz0, G0, gb0), (l1, dz1, G1, gb1) = outs
+    assert torch.equal(dz0, dz1)
+    assert abs(l1 - l0) <= 1e-6 * abs(l0)  # fp32 sums of 8 squares, fp64 beyond: summation order only
+    for a, b in zip(gb0, gb1):
+        assert float((a - b).abs().max()) <= 1e-5 * max(1e-30, float(a.abs().max()))
+    # the weight gradients only see dz: identical
+    for l in range(L):
+        wo, bo = e.seg[l]
+        assert torch.equal(G0[wo:bo], G1[wo:bo])
