@@ -204,20 +204,24 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
                                                 long long lddz, float* colsum, long long ldc, double* loss_part) {
   SG_GRID_WAIT();
   // block (64, 4) as k_act_grad_v8
-  __shared__ double red[256];
+  // Loss partials: one per 32 x 32 block, [row group][column block], with the
+  // arithmetic of the fused BIAS_MSE GEMM epilogue (gemm_tc_dev.cuh epi_chunk):
+  // per row, fp32 sums of 8 columns folded left to right, then the warp
+  // butterfly's tree over the 32 rows -- so the separate loss kernel and the
+  // fused one give bit-identical losses.
+  __shared__ float rs[32][65];  // per-row sums of 8 columns [row in group][8-column group]
   const long long c = (blockIdx.x * 64ll + threadIdx.x) * 8;
   const bool ok = c < N;
   const long long g = blockIdx.y, r0 = g * 32 + threadIdx.y * 8;
-  const long long r1 = r0 + 8 < M ? r0 + 8 : M;
-  double lsum = 0.0;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (ok) {
 #pragma unroll 4
-    for (long long r = r0; r < r1; ++r) {
+  for (int k = 0; k < 8; ++k) {
+    const long long r = r0 + k;
+    float l = 0.0f;
+    if (ok && r < M) {
       const V8 zv = ld8_f32(z + r * ldz + c);
       const V8 yv = ld8_f32(y + r * ldy + c);
       V8 o;
-      float l = 0.0f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float d = zv.v[j] - yv.v[j];
@@ -225,19 +229,25 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
         o.v[j] = d * scale + d * scale;
         acc[j] += o.v[j];
       }
-      lsum += (double)l;
       st8(dz + r * lddz + c, o);
     }
+    rs[threadIdx.y * 8 + k][threadIdx.x] = l;
   }
   quarter_colsum(acc, colsum, ldc, g, c, ok);
-  const int tid = threadIdx.y * 64 + threadIdx.x;
-  red[tid] = lsum;
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (tid < s) red[tid] += red[tid + s];
-    __syncthreads();
+  const int tid = threadIdx.y * 64 + threadIdx.x;
+  const long long n0 = blockIdx.x * 512ll + tid * 32;
+  if (tid < 16 && n0 < N) {
+    float lr[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      lr[i] = ((rs[i][4 * tid] + rs[i][4 * tid + 1]) + rs[i][4 * tid + 2]) + rs[i][4 * tid + 3];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < o; ++i) lr[i] = lr[i] + lr[i + o];
+    loss_part[g * ((N + 31) / 32) + n0 / 32] = (double)lr[0] * (double)scale;
   }
-  if (tid == 0) loss_part[blockIdx.y * gridDim.x + blockIdx.x] = red[0] * (double)scale;
   SG_GRID_TRIGGER();
 }
 
@@ -859,7 +869,7 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
       ld_y % 8 == 0 && ld_dz % 8 == 0 && a16(z) && a16(y) && a16(dz) &&
       (!colsum || (a16(colsum) && ld_colsum % 4 == 0)) && (M + 31) / 32 <= 65535) {
     dim3 g8((unsigned)((N + 511) / 512), (unsigned)((M + 31) / 32));
-    blocks = (long long)g8.x * g8.y;
+    blocks = ((M + 31) / 32) * ((N + 31) / 32);  // one partial per 32 x 32 block (k_mse_v8)
     if (blocks > n_part) return fail(SG_EINVAL, "loss: loss_part too small");
     if (dz_dtype == SG_BF16)
       SG_CUDA_TRY(pdl_launch(dk::k_mse_v8<__nv_bfloat16>, dim3(g8), dim3(dim3(64, 4)), 0, st, (const float*)z, ld_z, (const float*)y, ld_y, M, N, (float)scale,

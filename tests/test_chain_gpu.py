@@ -103,7 +103,10 @@ def test_chained_step_is_bit_identical_to_layer_path(sizes, acts, B):
 def test_chained_training_run_matches_layer_path():
     """CUDA-graph training (minibatch load, chained forward, loss, chained
     pullback, batched bias-gradient finalize, SGD): identical losses and
-    parameters to the per-layer path, step by step."""
+    parameters to the per-layer path, step by step.  Both arms take the
+    separate loss kernel (SGB200_FUSED_LOSS=0): the chained forward has no
+    loss-fused epilogue, and the fused one sums the bias-gradient partials in
+    another order (tests/test_dense_gpu.py::test_fused_mse_loss_matches_separate_loss_kernel)."""
     rng = np.random.default_rng(3)
     sizes, acts, B = (512,) * 5, ("tanh",) * 3 + ("identity",), 2048
     X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
@@ -113,6 +116,7 @@ def test_chained_training_run_matches_layer_path():
         import os
 
         os.environ["SGB200_CHAIN"] = "1" if use else "0"
+        os.environ["SGB200_FUSED_LOSS"] = "0"
         try:
             chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(4)]).init_params(
                 np.random.default_rng(1))
@@ -122,6 +126,7 @@ def test_chained_training_run_matches_layer_path():
             runs[use] = (losses, tr.engine.P.clone())
         finally:
             del os.environ["SGB200_CHAIN"]
+            del os.environ["SGB200_FUSED_LOSS"]
     assert runs[False][0] == runs[True][0]
     assert torch.equal(runs[False][1], runs[True][1])
     assert runs[True][0][-1] < runs[True][0][0]
