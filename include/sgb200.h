@@ -191,9 +191,24 @@ typedef struct sg_gemm_desc {
   int64_t ld_out2;
   double* loss_part; /* BIAS_MSE: [ceil(M/32)][ceil(N/32)] partial losses */
   double loss_scale; /* BIAS_MSE: scale (1 / global batch) */
+  /* deferred split-K (optional): when the launcher splits K (a STORE GEMM whose
+   * output tiles cannot fill the GPU, e.g. dW of a narrow layer), the fp32
+   * partials [splits][M][ld] (see sg_gemm_splits) are written here and NOT
+   * reduced: the caller reduces them later with sg_splitk_reduce_multi (several
+   * GEMMs in one launch).  Ignored when the GEMM does not split. */
+  float* split_part;
+  int64_t split_part_elems; /* capacity of split_part in floats */
 } sg_gemm_desc;
 
 SG_API int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* desc, void* stream);
+/* The split-K factor sg_gemm picks for desc (1: no split) and the partials'
+ * row pitch ld (floats): a deferred split needs splits * M * ld floats. */
+SG_API int sg_gemm_splits(sg_ctx* ctx, const sg_gemm_desc* desc, int32_t* splits, int64_t* ld_part);
+/* out_i[m][n] = sum_s part_i[s][m][n], s ascending (sg_gemm's own split-K
+ * reduce, bit-identical) for n deferred split-K GEMMs in one launch. */
+SG_API int sg_splitk_reduce_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int32_t* splits,
+                                  const int64_t* M, const int64_t* N, const int64_t* ld_part, float* const* outs,
+                                  const int64_t* ld_out, void* stream);
 
 /* ------------------------------------------------ Dense step, memory-bound
  * dz = ybar .* act'(h)  (rules.py:82-94 with the saved output h, reference

@@ -71,9 +71,14 @@ struct GemmArgs {
   long long sa = 0, sb = 0;  // operand batch strides (elements)
   long long so_f32 = 0, so_lp = 0;  // output batch strides (elements)
   FinalizeJob fin;            // run after the tiles (CTA-pair kernels) or as its own launch
+  float* split_part = nullptr;  // deferred split-K: partials land here, the caller reduces them
+  long long split_part_elems = 0;
 };
 
 int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st);
+void plan_gemm_splits(const GemmArgs& g, bool tf32, int num_sms, int* splits, long long* ld_part);
+int splitk_reduce_multi(int n, const float* const* parts, const int32_t* S, const int64_t* M, const int64_t* N,
+                        const int64_t* ld_part, float* const* outs, const int64_t* ld_out, cudaStream_t st);
 // sg_gemm_desc -> GemmArgs of the tensor-core kernels (validated by sg_gemm)
 void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g);
 int colsum_finalize_launch(const float* part, long long G, long long ld, long long N, float* out, int num_sms,

@@ -81,6 +81,7 @@ struct Params {
   unsigned* split_cnt;  // split-K arrival counters (reset by their last arriver)
   unsigned* done;       // CTAs finished; the last one clears cnt
   int n_cnt;
+  int defer;  // deferred row publishing (SGB200_CHAIN_DEFER, default on)
   Problem probs[MAX_PROBS];
 };
 
@@ -133,6 +134,30 @@ __device__ __forceinline__ void signal_rows(const Params& P, const Problem& pr, 
     bulk_wait0();                // this warp's TMA stores have landed
     fence_proxy_async_global();  // async-proxy writes ordered before the generic release
     if (!pr.p.tma_lp && !pr.p.tma_f32) __threadfence();  // direct stores of the warp (seen through __syncwarp)
+    red_release(P.cnt + pr.cnt_off + mb, 1u);
+  }
+}
+
+// Bulk store groups one chunk of a problem's epilogue commits (a chunk's
+// TMA stores: fp32 and / or bf16 output, or the second bf16 output).
+__device__ __forceinline__ int chunk_groups(const KParams& p) {
+  if (p.splits > 1) return 0;
+  const GemmEpilogue& e = p.epi;
+  return (e.out_f32 && p.tma_f32) + (e.out_bf16 && p.tma_lp) + (e.out2_bf16 && p.tma_o2);
+}
+// Deferred publish: called after the NEXT unit's first chunk, whose `newer`
+// store groups may still be in flight -- every older group (the published
+// unit's stores) has completed once at most `newer` are pending.
+__device__ __forceinline__ void signal_rows_deferred(const Params& P, const Problem& pr, int mb, int lane,
+                                                     int newer) {
+  __syncwarp();
+  if (lane == 0) {
+    if (newer <= 0) bulk_wait0();
+    else if (newer == 1) asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+    else if (newer == 2) asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group 3;" ::: "memory");
+    fence_proxy_async_global();
+    if (!pr.p.tma_lp && !pr.p.tma_f32) __threadfence();
     red_release(P.cnt + pr.cnt_off + mb, 1u);
   }
 }
@@ -305,6 +330,14 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
     int next_buf = 0;
     uint8_t* slot = stage_slots + ew * Slot<WIDE>::BYTES;
     uint64_t* my_aux = &aux_bar[2 * ew];
+    // A finished unit's rows are published once its TMA stores have landed.
+    // Waiting for them right after the unit costs the epilogue 1-1.5 us per
+    // unit; when the next unit's accumulator is already complete (its
+    // operands did not wait for these rows, so deferring cannot deadlock),
+    // the publish moves behind that unit's first chunk instead, by which time
+    // the stores have landed.  SGB200_CHAIN_DEFER=0 publishes at once.
+    int pend_mb = -1, pend_prob = 0;
+    const bool defer = P.defer;
     for (int i = u0; i < u1; ++i) {
       const Unit un = P.units[i];
       const Problem& pr = P.probs[un.prob];
@@ -318,8 +351,19 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane == 0) SG_TRACE(i - u0, 1);  // accumulator complete
+      auto publish_pending = [&]() {
+        if (pend_mb >= 0) {
+          signal_rows_deferred(P, P.probs[pend_prob], pend_mb, lane, chunk_groups(p));
+          pend_mb = -1;
+        }
+      };
       epi_chunks<WIDE>(p, tmem_base + acc * PN + ((uint32_t)(q * 32) << 16), n0t + c0 * 32, c0, CH_PER, row0, lane,
-                       un.split, 0, false, slot, staged, &mp->aux, my_aux, aux_phase, &mp->lp, &mp->f32, next_buf);
+                       un.split, 0, false, slot, staged, &mp->aux, my_aux, aux_phase, &mp->lp, &mp->f32, next_buf,
+                       publish_pending);
+      if (pend_mb >= 0) {  // no chunk of this warp's half was inside N: nothing newer in flight
+        signal_rows_deferred(P, P.probs[pend_prob], pend_mb, lane, 0);
+        pend_mb = -1;
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc == 0 ? acc_empty_leader0 : acc_empty_leader1);
@@ -328,10 +372,19 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
         acc = 0;
         acc_phase ^= 1;
       }
-      if (p.splits > 1)
+      if (p.splits > 1) {
         split_fixup(P, pr, un, (int)rank * EPI_WARPS + ew, row0, n0t + c0 * 32, CH_PER, lane);
-      else if (pr.signal)
-        signal_rows(P, pr, un.mb, lane);
+      } else if (pr.signal) {
+        int ready = 0;  // the next unit's accumulator is complete (warp-uniform via lane 0)
+        if (defer && i + 1 < u1 && lane == 0) ready = mbar_test(&acc_full[acc], acc_phase);
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready) {
+          pend_mb = un.mb;
+          pend_prob = un.prob;
+        } else {
+          signal_rows(P, pr, un.mb, lane);
+        }
+      }
       if (lane == 0 && ew == 0) SG_TRACE(i - u0, 3);  // warp 0 done (signal / split fix-up included)
     }
   }
@@ -631,6 +684,10 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
   c->params.split_cnt = c->d_split;
   c->params.done = c->d_done;
   c->params.n_cnt = (int)n_cnt;
+  {
+    const char* e = std::getenv("SGB200_CHAIN_DEFER");
+    c->params.defer = !(e && e[0] == '0');
+  }
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     e = cudaFuncSetAttribute(chain::gemm_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

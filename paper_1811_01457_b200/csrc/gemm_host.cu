@@ -98,6 +98,8 @@ void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g) {
     g.epi.out2_bf16 = (__nv_bfloat16*)d->out2_lp;
     g.epi.ld_out2 = d->ld_out2;
   }
+  g.split_part = d->split_part;
+  g.split_part_elems = d->split_part_elems;
   g.batch = (int)batch;
   g.sa = d->stride_a;
   g.sb = d->stride_b;
@@ -105,3 +107,32 @@ void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g) {
   g.so_lp = d->stride_lp;
 }
 }  // namespace sg
+
+extern "C" int sg_gemm_splits(sg_ctx* ctx, const sg_gemm_desc* d, int32_t* splits, int64_t* ld_part) {
+  if (!ctx || !d || !splits || !ld_part) return fail(SG_EINVAL, "null argument");
+  *splits = 1;
+  *ld_part = (d->N + 3) / 4 * 4;
+  if (d->precision != SG_PREC_BF16 && d->precision != SG_PREC_TF32) return SG_OK;  // strict GEMMs never split
+  if (d->M <= 0 || d->N <= 0 || d->K <= 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  GemmArgs g{};
+  gemm_args_from_desc(ctx, d, g);
+  int s = 1;
+  long long ld = 0;
+  plan_gemm_splits(g, d->precision == SG_PREC_TF32, ctx_compute_sms(ctx), &s, &ld);
+  *splits = s;
+  *ld_part = ld;
+  return SG_OK;
+}
+
+extern "C" int sg_splitk_reduce_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int32_t* splits,
+                                      const int64_t* M, const int64_t* N, const int64_t* ld_part,
+                                      float* const* outs, const int64_t* ld_out, void* stream) {
+  if (!ctx || n < 0 || (n && (!parts || !splits || !M || !N || !ld_part || !outs || !ld_out)))
+    return fail(SG_EINVAL, "null argument");
+  if (n == 0) return SG_OK;
+  int rc = ctx_activate(ctx);
+  if (rc) return rc;
+  return splitk_reduce_multi(n, parts, splits, M, N, ld_part, outs, ld_out, (cudaStream_t)stream);
+}

@@ -616,10 +616,9 @@ namespace {
 
 // split-K finalize: out = sum_s part[s] in ascending s (deterministic)
 // blockIdx.y = row, threads over 4-column groups (no 64-bit divides, float4 loads)
-__global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
-                                long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials come from the GEMM before us (PDL)
-  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+__device__ __forceinline__ void splitk_reduce_cols(const float* __restrict__ part, int S, int M, int N, long long ldp,
+                                                   float* out, long long ld_out, __nv_bfloat16* out_lp,
+                                                   long long ld_lp, int n) {
   if (n >= N) return;
   const bool vec = n + 4 <= N && (ldp % 4) == 0;
   for (long long m = blockIdx.y; m < M; m += gridDim.y) {
@@ -646,6 +645,26 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, in
   }
   }
 }
+__global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, long long ldp, float* out,
+                                long long ld_out, __nv_bfloat16* out_lp, long long ld_lp) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials come from the GEMM before us (PDL)
+  splitk_reduce_cols(part, S, M, N, ldp, out, ld_out, out_lp, ld_lp, (blockIdx.x * blockDim.x + threadIdx.x) * 4);
+}
+// Deferred split-K: several GEMMs' partials reduced in one launch (blockIdx.z
+// = job), with k_splitk_reduce's arithmetic (bit-identical results).
+constexpr int MAX_SPLITK_JOBS = 32;
+struct SplitkJobs {
+  const float* part[MAX_SPLITK_JOBS];
+  float* out[MAX_SPLITK_JOBS];
+  long long ldp[MAX_SPLITK_JOBS], ld_out[MAX_SPLITK_JOBS];
+  int S[MAX_SPLITK_JOBS], M[MAX_SPLITK_JOBS], N[MAX_SPLITK_JOBS];
+};
+__global__ void k_splitk_reduce_multi(const __grid_constant__ SplitkJobs jobs) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int b = blockIdx.z;
+  splitk_reduce_cols(jobs.part[b], jobs.S[b], jobs.M[b], jobs.N[b], jobs.ldp[b], jobs.out[b], jobs.ld_out[b], nullptr,
+                     0, (blockIdx.x * blockDim.x + threadIdx.x) * 4);
+}
 
 // Launch with a programmatic dependency on the previous kernel in the stream
 // (SGB200_GEMM_PDL=0 disables): the kernel's own griddepcontrol.wait orders
@@ -667,6 +686,38 @@ cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
+// layer: M = N = 1024, K = batch): plain-store epilogues only.  `units` =
+// SMs (1-SM kernels) or CTA pairs.
+void choose_splits(const GemmArgs& g, int tiles, int units, int num_kb, int& splits, int& kb_per) {
+  splits = 1;
+  kb_per = num_kb;
+  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && g.batch == 1 && tiles * 2 <= units && num_kb >= 8) {
+    int s = units / tiles;
+    if (s > num_kb / 4) s = num_kb / 4;
+    if (s > 16) s = 16;
+    if (s >= 2) {
+      kb_per = (num_kb + s - 1) / s;
+      splits = (num_kb + kb_per - 1) / kb_per;
+    }
+  }
+}
+
+// The partial buffer of a split-K launch: the caller's (deferred reduce,
+// GemmArgs::split_part) or a stream-ordered temporary.
+static int split_part_buffer(const GemmArgs& g, int splits, long long ld_part, float** part, cudaStream_t st) {
+  const long long need = (long long)splits * g.M * ld_part;
+  if (g.split_part) {
+    if (g.split_part_elems < need) return fail(SG_EINVAL, "gemm: split_part holds " +
+                                               std::to_string(g.split_part_elems) + " floats, " +
+                                               std::to_string(need) + " needed");
+    *part = g.split_part;
+    return SG_OK;
+  }
+  SG_CUDA_TRY(cudaMallocAsync((void**)part, (size_t)need * sizeof(float), st));
+  return SG_OK;
 }
 
 static int launch_splitk_reduce(const float* part, int splits, const GemmArgs& g, long long ld_part,
@@ -704,15 +755,7 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   // split-K when the output tiles cannot fill the machine (e.g. dW of a narrow
   // layer: M = N = 1024, K = batch): plain-store epilogues only
   int splits = 1, kb_per = num_kb;
-  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && g.batch == 1 && tiles * 2 <= num_sms && num_kb >= 8) {
-    int s = num_sms / tiles;
-    if (s > num_kb / 4) s = num_kb / 4;
-    if (s > 16) s = 16;
-    if (s >= 2) {
-      kb_per = (num_kb + s - 1) / s;
-      splits = (num_kb + kb_per - 1) / kb_per;
-    }
-  }
+  choose_splits(g, tiles, num_sms, num_kb, splits, kb_per);
   tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, g.batch, g.so_f32, g.so_lp};
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
@@ -721,14 +764,14 @@ int run(const GemmArgs& g, int num_sms, cudaStream_t st) {
   float* part = nullptr;
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
-    SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
+    if ((rc = split_part_buffer(g, splits, p.ld_part, &part, st))) return rc;
     p.part = part;
   }
   const int work = tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
   SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
-  if (splits > 1) {
+  if (splits > 1 && !g.split_part) {  // deferred: the caller reduces (sg_splitk_reduce_multi)
     if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
   }
@@ -763,15 +806,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256) * g.batch;
   const int num_kb = (g.K + BK - 1) / BK;
   int splits = 1, kb_per = num_kb;
-  if (g.epi.mode == SG_EPI_STORE && !g.epi.colsum && g.batch == 1 && tiles * 2 <= pairs_avail && num_kb >= 8) {
-    int s = pairs_avail / tiles;
-    if (s > num_kb / 4) s = num_kb / 4;
-    if (s > 16) s = 16;
-    if (s >= 2) {
-      kb_per = (num_kb + s - 1) / s;
-      splits = (num_kb + kb_per - 1) / kb_per;
-    }
-  }
+  choose_splits(g, tiles, pairs_avail, num_kb, splits, kb_per);
   tc::KParams p{g.M, g.N, g.K, g.epi, splits, kb_per, nullptr, 0, 0, 0, 0, 8, 0, 0, g.batch, g.so_f32, g.so_lp};
   if (const char* e = std::getenv("SGB200_GEMM_RASTER")) p.raster = std::max(1, std::atoi(e));
   CUtensorMap mlp, mf32, maux;
@@ -789,9 +824,9 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   }();
   if (splits > 1) {
     p.ld_part = (g.N + 3) / 4 * 4;
-    SG_CUDA_TRY(cudaMallocAsync((void**)&part, (size_t)splits * g.M * p.ld_part * sizeof(float), st));
+    if ((rc = split_part_buffer(g, splits, p.ld_part, &part, st))) return rc;
     p.part = part;
-    if (fixup) {  // the last split of each tile region sums the partials inside the kernel
+    if (fixup && !g.split_part) {  // the last split of each tile region sums the partials inside the kernel
       const size_t ncnt = (size_t)tiles * 2 * tc::EPI_WARPS;
       SG_CUDA_TRY(cudaMallocAsync((void**)&cnt, ncnt * sizeof(unsigned), st));
       SG_CUDA_TRY(cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned), st));
@@ -839,7 +874,7 @@ int run_pair(const GemmArgs& g, int num_sms, cudaStream_t st) {
   const int grid = 2 * (work < pairs_avail ? work : pairs_avail);
   SG_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(tc::NUM_THREADS), SMEM, st, ma, mb, mlp, mf32, maux, p));
   SG_CUDA_TRY(cudaGetLastError());
-  if (splits > 1) {
+  if (splits > 1 && !g.split_part) {  // deferred: the caller reduces (sg_splitk_reduce_multi)
     if (!cnt)
       if (int rc2 = launch_splitk_reduce(part, splits, g, p.ld_part, st)) return rc2;
     SG_CUDA_TRY(cudaFreeAsync(part, st));
@@ -919,6 +954,57 @@ extern "C" SG_API int sg_gemm_cprof(int on, unsigned long long* out8) {
   return SG_OK;
 }
 #endif
+
+// The split-K factor launch_gemm_tc would pick for g (dispatch's kernel choice
+// and choose_splits), and the partials' row pitch.
+void plan_gemm_splits(const GemmArgs& g, bool tf32, int num_sms, int* splits, long long* ld_part) {
+  const int BK = tf32 ? tc::Elem<true>::BK : tc::Elem<false>::BK;
+  const int num_kb = (g.K + BK - 1) / BK;
+  const char* fe = std::getenv("SGB200_GEMM_FORCE_BN");
+  const int force_bn = fe ? std::atoi(fe) : 0;
+  const char* pe = std::getenv("SGB200_GEMM_PAIR");
+  const bool pair_ok = !(pe && pe[0] == '0');
+  int s = 1, kb_per = num_kb;
+  if (!force_bn && g.N > 128 && pair_ok && g.M >= 256 && num_sms >= 2) {
+    const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256) * g.batch;
+    choose_splits(g, tiles, num_sms / 2, num_kb, s, kb_per);
+  } else {
+    const int bn = force_bn ? force_bn : (g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256));
+    const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + bn - 1) / bn) * g.batch;
+    choose_splits(g, tiles, num_sms, num_kb, s, kb_per);
+  }
+  *splits = s;
+  *ld_part = (g.N + 3) / 4 * 4;
+}
+
+int splitk_reduce_multi(int n, const float* const* parts, const int32_t* S, const int64_t* M, const int64_t* N,
+                        const int64_t* ld_part, float* const* outs, const int64_t* ld_out, cudaStream_t st) {
+  for (int b0 = 0; b0 < n; b0 += MAX_SPLITK_JOBS) {
+    SplitkJobs jobs{};
+    const int nb = std::min(n - b0, MAX_SPLITK_JOBS);
+    long long nmax = 1, mmax = 1;
+    for (int i = 0; i < nb; ++i) {
+      const int k = b0 + i;
+      if (!parts[k] || !outs[k] || S[k] < 1 || M[k] < 1 || N[k] < 1 || M[k] > INT32_MAX || N[k] > INT32_MAX ||
+          ld_part[k] < N[k] || ld_out[k] < N[k])
+        return fail(SG_EINVAL, "splitk_reduce_multi: bad job " + std::to_string(k));
+      jobs.part[i] = parts[k];
+      jobs.out[i] = outs[k];
+      jobs.S[i] = S[k];
+      jobs.M[i] = (int)M[k];
+      jobs.N[i] = (int)N[k];
+      jobs.ldp[i] = ld_part[k];
+      jobs.ld_out[i] = ld_out[k];
+      nmax = std::max(nmax, (long long)N[k]);
+      mmax = std::max(mmax, (long long)M[k]);
+    }
+    const unsigned gx = (unsigned)(((nmax + 3) / 4 + 255) / 256);
+    const unsigned gy = (unsigned)(mmax < 65535 ? mmax : 65535);
+    SG_CUDA_TRY(launch_pdl(k_splitk_reduce_multi, dim3(gx, gy, nb), dim3(256), 0, st, jobs));
+    SG_CUDA_TRY(cudaGetLastError());
+  }
+  return SG_OK;
+}
 
 int launch_gemm_tc(const GemmArgs& g, bool tf32, int num_sms, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return fail(SG_EINVAL, "gemm: empty problem");

@@ -71,6 +71,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// non-blocking: has the barrier completed the phase with this parity?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -797,12 +809,17 @@ __device__ __forceinline__ void epi_aux_prologue(bool staged, int lane, uint8_t*
   if (WIDE && nch > 1 && n_first + 32 < N) aux_issue(aux_base_wide(slot, 1), map_aux, &aux_bars[1], n_first + 32, row0);
 }
 
-template <bool WIDE>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// `after0` runs once the first chunk's stores are issued (the GEMM chain
+// publishes the previous unit's rows there, its stores long landed).
+template <bool WIDE, class After0 = NoHook>
 __device__ __forceinline__ void epi_chunks(const KParams& p, uint32_t tmem_row, int n_first, int c_first, int nch,
                                            int row0, int lane, int split, int bidx, bool radd, uint8_t* slot,
                                            bool staged, const CUtensorMap* map_aux, uint64_t* aux_bars,
                                            uint32_t& aux_phase, const CUtensorMap* map_lp,
-                                           const CUtensorMap* map_f32, int& next_buf) {
+                                           const CUtensorMap* map_f32, int& next_buf, After0 after0 = After0{}) {
   const int m = row0 + lane;
   const bool row_ok = m < p.M;
 #pragma unroll 1
@@ -840,6 +857,7 @@ __device__ __forceinline__ void epi_chunks(const KParams& p, uint32_t tmem_row, 
     }
     epi_chunk<WIDE>(p, v, m, row_ok, row0 >> 5, row0 < p.M, n0, lane, split, bidx, staged && !y32, h, slot, radd,
                     map_lp, map_f32, &next_buf, ys);
+    if (j == 0) after0();
   }
 }
 

@@ -507,6 +507,20 @@ class ChainEngine:
         self.grad_ready = None  # optional callback(bucket_index) when a bucket's gradients are written
         self.l0_slices = 1      # data parallel: layer 0's dW in row slices (enable_first_layer_slices)
         self.small = self._plan_small() if small else None
+        # deferred split-K (bf16 pullback without per-layer hooks): a dW GEMM
+        # that splits K leaves its partials in its own buffer and every layer's
+        # are reduced in ONE launch after the pullback (sg_splitk_reduce_multi,
+        # the same ordered sum) -- the per-layer reduce launch sat between the
+        # layer's dW and the next dX.  SGB200_DEFER_SPLITK=0 reduces per GEMM.
+        self.dw_split = [None] * self.L
+        if hasattr(self, "csl") and os.environ.get("SGB200_DEFER_SPLITK", "1") != "0":
+            from .gemm import gemm_desc, gemm_splits
+
+            for l in range(self.L):
+                splits, ld = gemm_splits(gemm_desc(self.dz_of(l), self.H[l], a_mn=True, b_mn=True, out=self.gW[l]))
+                if splits > 1:
+                    part = torch.empty(splits * self.sizes[l + 1] * ld, dtype=torch.float32, device=dev)
+                    self.dw_split[l] = (part, splits, ld)
         if chain.layers[0].W is not None:
             self.set_params([(l.W, l.b) for l in chain.layers])
 
@@ -692,6 +706,13 @@ class ChainEngine:
         rt.check(lib.sg_colsum_finalize_multi(rt.context(), n, parts, G, ld, N, outs, rt.stream_ptr()),
                  "sg_colsum_finalize_multi")
 
+    def _reduce_all_dw(self):
+        """dW_l = sum of its deferred split-K partials, every split layer in one launch."""
+        from .gemm import splitk_reduce
+
+        splitk_reduce([(sp[0], sp[1], self.sizes[l + 1], self.sizes[l], sp[2], self.gW[l])
+                       for l, sp in enumerate(self.dw_split) if sp is not None])
+
     def _chain_backward(self, _ctx):
         """Chained pullback: every layer's dX (with the lower layer's act' and
         bias-gradient partials fused) and dW in one launch -- or, pairwise, one
@@ -785,13 +806,15 @@ class ChainEngine:
                 # db of every layer after layer 0's (rules.py:45-46)
                 from .gemm import gemm
 
-                gemm(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l])
+                sp = self.dw_split[l]
+                gemm(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l], split_part=None if sp is None else sp[0])
                 if l > 0:
                     act_prev = self.acts[l - 1]
                     gemm(dz, self.Ws[l], b_mn=True, epilogue="store" if act_prev == "identity" else "act_grad",
                          act=act_prev, aux=self.H[l], out_lp=self.dz_of(l - 1), colsum=self.cs_of(l - 1))
                 else:
                     self._finalize_all_db()
+                    self._reduce_all_dw()
                 return
             # dW = dZ^T H[l]; db = colsum(dZ) (partials fused upstream on the
             # tensor-core paths); dZ[l-1] = (dZ W) .* act'(H[l]) of the layer below

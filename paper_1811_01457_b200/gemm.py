@@ -38,6 +38,7 @@ class GemmDesc(ctypes.Structure):
         ("stride_out", ctypes.c_int64), ("stride_lp", ctypes.c_int64),
         ("out2_lp", ctypes.c_void_p), ("ld_out2", ctypes.c_int64),
         ("loss_part", ctypes.c_void_p), ("loss_scale", ctypes.c_double),
+        ("split_part", ctypes.c_void_p), ("split_part_elems", ctypes.c_int64),
     ]
 
 
@@ -50,6 +51,12 @@ def _lib():
     if not _bound:
         lib.sg_gemm.argtypes = [ctypes.c_void_p, ctypes.POINTER(GemmDesc), ctypes.c_void_p]
         lib.sg_gemm.restype = ctypes.c_int
+        lib.sg_gemm_splits.argtypes = [ctypes.c_void_p, ctypes.POINTER(GemmDesc), ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_int64)]
+        lib.sg_gemm_splits.restype = ctypes.c_int
+        P, I64 = ctypes.c_void_p, ctypes.c_int64
+        lib.sg_splitk_reduce_multi.argtypes = [P, ctypes.c_int32, P, P, P, P, P, P, P, P]
+        lib.sg_splitk_reduce_multi.restype = ctypes.c_int
         _bound = True
     return lib
 
@@ -113,8 +120,13 @@ def check_dtypes(precision: str, operands=(), fp32=(), lp=(), colsum=None) -> No
 
 def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
          epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-         out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0, stream=None):
+         out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0, split_part=None,
+         stream=None):
     """Launch one GEMM; outputs are written in place into the given tensors.
+
+    ``split_part`` (fp32, contiguous): deferred split-K -- when the GEMM splits
+    K (see :func:`gemm_splits`) its partials land there unreduced and ``out``
+    is left untouched until :func:`splitk_reduce` runs.
 
     ``colsum`` (fp32 ``[ceil(M/32)][>=N]``) receives per-32-row column sums of
     the result (the first stage of a bias gradient).  ``epilogue="bias_act_seed"``
@@ -126,13 +138,43 @@ def gemm(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf1
     """
     d = gemm_desc(A, B, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, precision=precision, epilogue=epilogue, act=act,
                   bias=bias, aux=aux, out=out, out_lp=out_lp, out_pre=out_pre, colsum=colsum, seed=seed,
-                  out2_lp=out2_lp, loss_part=loss_part, loss_scale=loss_scale)
+                  out2_lp=out2_lp, loss_part=loss_part, loss_scale=loss_scale, split_part=split_part)
     rt.check(_lib().sg_gemm(rt.context(), ctypes.byref(d), rt.stream_ptr(stream)), "sg_gemm")
+
+
+def gemm_splits(desc: "GemmDesc") -> tuple:
+    """(splits, ld) sg_gemm picks for a descriptor: a deferred split-K needs
+    ``splits * M * ld`` fp32 partials (splits == 1: no split)."""
+    s, ld = ctypes.c_int32(1), ctypes.c_int64(0)
+    rt.check(_lib().sg_gemm_splits(rt.context(), ctypes.byref(desc), ctypes.byref(s), ctypes.byref(ld)),
+             "sg_gemm_splits")
+    return int(s.value), int(ld.value)
+
+
+def splitk_reduce(jobs, stream=None) -> None:
+    """Reduce deferred split-K partials, several GEMMs in one launch:
+    ``jobs`` = [(part, splits, M, N, ld_part, out)], out fp32 2-D (unit column
+    stride); out = sum over splits in ascending order (sg_gemm's own reduce)."""
+    n = len(jobs)
+    if n == 0:
+        return
+    for part, splits, M, N, ld, out in jobs:
+        if part.dtype.itemsize != 4 or out.dim() != 2 or out.shape[0] < M or out.shape[1] < N:
+            raise ValueError("splitk_reduce: fp32 partials and an M x N fp32 output")
+        if part.numel() < splits * M * ld:
+            raise ValueError(f"splitk_reduce: {part.numel()} partials, {splits * M * ld} needed")
+    A = ctypes.c_void_p * n
+    I32, I64 = ctypes.c_int32 * n, ctypes.c_int64 * n
+    rt.check(_lib().sg_splitk_reduce_multi(
+        rt.context(), n, A(*[j[0].data_ptr() for j in jobs]), I32(*[j[1] for j in jobs]), I64(*[j[2] for j in jobs]),
+        I64(*[j[3] for j in jobs]), I64(*[j[4] for j in jobs]), A(*[j[5].data_ptr() for j in jobs]),
+        I64(*[_ld(j[5]) for j in jobs]), rt.stream_ptr(stream)), "sg_splitk_reduce_multi")
 
 
 def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision="bf16",
               epilogue="store", act="identity", bias=None, aux=None, out=None, out_lp=None,
-              out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0) -> GemmDesc:
+              out_pre=None, colsum=None, seed=None, out2_lp=None, loss_part=None, loss_scale=1.0,
+              split_part=None) -> GemmDesc:
     """The validated ``sg_gemm_desc`` of a GEMM (see :func:`gemm`), without launching it."""
     if a_mn:
         Ka, Ma = A.shape
@@ -205,7 +247,13 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
     d.colsum, d.ld_colsum = _ptr(colsum), _ld(colsum)
     d.out2_lp, d.ld_out2 = _ptr(out2_lp), _ld(out2_lp)
     d.loss_part, d.loss_scale = _ptr(loss_part), float(loss_scale)
-    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum, out2_lp, loss_part)  # the buffers stay alive with the descriptor
+    if split_part is not None:
+        import torch
+
+        if split_part.dtype != torch.float32 or not split_part.is_contiguous():
+            raise ValueError("gemm: split_part must be a contiguous float32 buffer")
+    d.split_part, d.split_part_elems = _ptr(split_part), 0 if split_part is None else split_part.numel()
+    d.keep = (A, B, bias, aux, out, out_lp, out_pre, colsum, out2_lp, loss_part, split_part)  # the buffers stay alive with the descriptor
     return d
 
 

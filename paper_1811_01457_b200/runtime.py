@@ -27,7 +27,7 @@ EXPORTS = (
     "sg_version", "sg_create", "sg_destroy", "sg_last_error",
     "sg_ew_compile", "sg_ew_forward", "sg_ew_grad", "sg_ew_pack", "sg_ew_check",
     "sg_ew_set_step_limit", "sg_ew_compile_only", "sg_ew_variant_count", "sg_reduce_to",
-    "sg_gemm", "sg_act_grad", "sg_colsum_finalize", "sg_colsum_finalize_multi", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d", "sg_sum_f64",
+    "sg_gemm", "sg_gemm_splits", "sg_splitk_reduce_multi", "sg_act_grad", "sg_colsum_finalize", "sg_colsum_finalize_multi", "sg_colsum_strict", "sg_loss", "sg_sgd", "sg_cast", "sg_cast_2d", "sg_sum_f64",
     "sg_dense_forward", "sg_dense_backward", "sg_mlp_small_scratch_bytes", "sg_mlp_small_step",
     "sg_dp_available", "sg_dp_unique_id", "sg_dp_init", "sg_dp_allreduce", "sg_dp_wait", "sg_dp_finalize",
     "sg_domain_check", "sg_chain_create", "sg_chain_run", "sg_chain_info", "sg_chain_destroy",

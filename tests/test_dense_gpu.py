@@ -569,3 +569,49 @@ def test_fused_mse_loss_matches_separate_loss_kernel(sizes, B):
     for l in range(L):
         wo, bo = e.seg[l]
         assert torch.equal(G0[wo:bo], G1[wo:bo])
+
+
+def test_deferred_splitk_is_bit_identical():
+    """Deferred split-K (a dW GEMM's partials left in its own buffer, every
+    layer's reduced in one sg_splitk_reduce_multi launch after the pullback)
+    against the per-GEMM reduce: identical dW and db, and the split actually
+    happens for these narrow layers (K = batch >> M = N)."""
+    import os
+
+    from paper_1811_01457_b200.gemm import gemm, gemm_splits, gemm_desc, splitk_reduce
+
+    rng = np.random.default_rng(11)
+    sizes, acts, B = (256, 384, 256, 128), ("tanh", "tanh", "identity"), 16384
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(3)]).init_params(rng)
+    X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+    grads = []
+    for defer in ("0", "1"):
+        os.environ["SGB200_DEFER_SPLITK"] = defer
+        try:
+            e = ChainEngine(chain, B, "mse", "bf16", small=False)
+        finally:
+            del os.environ["SGB200_DEFER_SPLITK"]
+        assert (sum(sp is not None for sp in e.dw_split) > 0) == (defer == "1")
+        e.load_batch(X, Y)
+        e.forward(fuse_loss=True)
+        e.loss_and_seed()
+        e.pullback()
+        torch.cuda.synchronize()
+        grads.append(e.G.clone())
+    assert torch.equal(grads[0], grads[1])
+    # the binding alone: partials + one multi-job reduce == the GEMM's own reduce
+    A = (torch.rand((B, 320), device="cuda") - 0.5).to(torch.bfloat16)
+    Bm = (torch.rand((B, 192), device="cuda") - 0.5).to(torch.bfloat16)
+    ref = torch.empty((320, 192), device="cuda")
+    gemm(A, Bm, a_mn=True, b_mn=True, out=ref)
+    splits, ld = gemm_splits(gemm_desc(A, Bm, a_mn=True, b_mn=True, out=ref))
+    assert splits > 1
+    part = torch.empty(splits * 320 * ld, device="cuda")
+    out = torch.full((320, 192), float("nan"), device="cuda")
+    gemm(A, Bm, a_mn=True, b_mn=True, out=out, split_part=part)
+    splitk_reduce([(part, splits, 320, 192, ld, out)])
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    with pytest.raises(Exception):
+        gemm(A, Bm, a_mn=True, b_mn=True, out=out, split_part=part[:10])
