@@ -8,9 +8,22 @@
 #include <cstdint>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/sgb200.h"
 
 namespace sg {
+
+// NVTX range over one C-ABI call (ranges for nsys / ncu --nvtx
+// filtering).  NVTX3 is header-only: without an attached tool the push/pop
+// are a null-check each.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define SG_NVTX(name) ::sg::NvtxRange sg_nvtx_range_(name)
 
 // Last error message of the calling thread (sg_last_error).
 void set_error(const std::string& msg);

@@ -53,6 +53,7 @@ extern "C" {
 
 int sg_dense_forward(sg_ctx* ctx, const sg_dense_desc* d, void* H, int64_t ldh, void* H_f32, int64_t ld_hf, void* Z,
                      int64_t ldz, void* stream) {
+  SG_NVTX("sg_dense_forward");
   if (!ctx) return fail(SG_EINVAL, "null argument");
   if (int rc = check_desc(d)) return rc;
   if (d->batch == 0) return SG_OK;
@@ -85,6 +86,7 @@ int sg_dense_forward(sg_ctx* ctx, const sg_dense_desc* d, void* H, int64_t ldh, 
 }
 
 int sg_dense_backward(sg_ctx* ctx, const sg_dense_desc* d, const sg_dense_grad* gr, void* stream) {
+  SG_NVTX("sg_dense_backward");
   if (!ctx || !gr) return fail(SG_EINVAL, "null argument");
   if (int rc = check_desc(d)) return rc;
   if (!gr->dZ || !gr->dW || !gr->db) return fail(SG_EINVAL, "dense: dZ, dW and db are required");

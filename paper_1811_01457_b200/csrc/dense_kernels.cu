@@ -765,6 +765,7 @@ extern "C" {
 int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y, const void* h, int32_t h_dtype,
                 int64_t ld_h, int64_t M, int64_t N, int32_t act, void* dz, int32_t dz_dtype, int64_t ld_dz,
                 void* dz2, int32_t dz2_dtype, int64_t ld_dz2, float* colsum, int64_t ld_colsum, void* stream) {
+  SG_NVTX("sg_act_grad");
   if (!ctx || !ybar || !h || !dz) return fail(SG_EINVAL, "null argument");
   if (M <= 0 || N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
@@ -801,6 +802,7 @@ int sg_act_grad(sg_ctx* ctx, const void* ybar, int32_t ybar_dtype, int64_t ld_y,
 
 int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_part, int64_t N, float* out,
                        void* stream) {
+  SG_NVTX("sg_colsum_finalize");
   if (!ctx || !part || !out) return fail(SG_EINVAL, "null argument");
   if (N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
@@ -813,6 +815,7 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
 
 int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int64_t* G,
                              const int64_t* ld_part, const int64_t* N, float* const* outs, void* stream) {
+  SG_NVTX("sg_colsum_finalize_multi");
   if (!ctx || n < 0 || (n && (!parts || !G || !ld_part || !N || !outs))) return fail(SG_EINVAL, "null argument");
   int rc = ctx_activate(ctx);
   if (rc) return rc;
@@ -839,6 +842,7 @@ int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, 
 
 int sg_colsum_strict(sg_ctx* ctx, const void* x, int32_t dtype, int64_t ld, int64_t M, int64_t N, void* out,
                      void* stream) {
+  SG_NVTX("sg_colsum_strict");
   if (!ctx || !x || !out) return fail(SG_EINVAL, "null argument");
   if (!fdt(dtype)) return fail(SG_EINVAL, "colsum_strict: f32/f64 only");
   if (M <= 0 || N <= 0) return SG_OK;
@@ -858,6 +862,7 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
             int64_t M, int64_t N, double scale, double* loss, double* loss_part, int64_t n_part, void* dz,
             int32_t dz_dtype, int64_t ld_dz, void* dz2, int32_t dz2_dtype, int64_t ld_dz2, float* colsum,
             int64_t ld_colsum, void* stream) {
+  SG_NVTX("sg_loss");
   if (!ctx || !z || !y || !dz || !loss || !loss_part) return fail(SG_EINVAL, "null argument");
   if (!fdt(dtype)) return fail(SG_EINVAL, "loss: logits must be f32/f64");
   if (M <= 0 || N <= 0) return fail(SG_EINVAL, "loss: empty batch");
@@ -940,6 +945,7 @@ int sg_loss(sg_ctx* ctx, int32_t kind, const void* z, int32_t dtype, int64_t ld_
 
 int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t n, double lr, void* shadow_bf16,
            void* stream) {
+  SG_NVTX("sg_sgd");
   if (!ctx || !params || !grads) return fail(SG_EINVAL, "null argument");
   if (!fdt(dtype)) return fail(SG_EINVAL, "sgd: f32/f64 parameters");
   if (n <= 0) return SG_OK;
@@ -963,6 +969,7 @@ int sg_sgd(sg_ctx* ctx, void* params, const void* grads, int32_t dtype, int64_t 
 }
 
 int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n, void* stream) {
+  SG_NVTX("sg_cast");
   if (!ctx || !src || !dst) return fail(SG_EINVAL, "null argument");
   if (n <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
@@ -975,6 +982,7 @@ int sg_cast(sg_ctx* ctx, const void* src, int32_t src_dtype, void* dst, int32_t 
 
 int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, void* dst, int32_t dst_dtype,
                int64_t ld_dst, int64_t rows, int64_t cols, void* stream) {
+  SG_NVTX("sg_cast_2d");
   if (!ctx || !src || !dst) return fail(SG_EINVAL, "null argument");
   if (rows <= 0 || cols <= 0) return SG_OK;
   if (ld_src < cols || ld_dst < cols) return fail(SG_EINVAL, "cast_2d: leading dimension smaller than the row");
@@ -1000,6 +1008,7 @@ int sg_cast_2d(sg_ctx* ctx, const void* src, int32_t src_dtype, int64_t ld_src, 
 }
 
 int sg_sum_f64(sg_ctx* ctx, const double* part, int64_t n, double* out, void* stream) {
+  SG_NVTX("sg_sum_f64");
   if (!ctx || !part || !out) return fail(SG_EINVAL, "null argument");
   if (n <= 0) return fail(SG_EINVAL, "sum_f64: empty");
   int rc = ctx_activate(ctx);

@@ -144,6 +144,7 @@ int sg_dp_init(sg_ctx* ctx, const uint8_t* unique_id, size_t n, int rank, int wo
 }
 
 int sg_dp_allreduce(sg_dp* dp, void* buf, int64_t n, int32_t dtype, void* stream) {
+  SG_NVTX("sg_dp_allreduce");
   if (!dp || (!buf && n > 0) || n < 0) return fail(SG_EINVAL, "null argument");
   ncclDataType_t t;
   if (!nccl_dtype(dtype, &t)) return fail(SG_EINVAL, "dp: dtype must be f32, f64 or bf16");

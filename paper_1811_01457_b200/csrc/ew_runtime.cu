@@ -655,6 +655,7 @@ int sg_ew_set_step_limit(sg_ctx* ctx, int64_t limit) {
 
 int sg_ew_compile(sg_ctx* ctx, const char* user_src, const char* key, int k, int dtype,
                   sg_kernel** out) {
+  SG_NVTX("sg_ew_compile");
   if (!ctx || !user_src || !out) return fail(SG_EINVAL, "null argument");
   if (k < 0 || k > SG_MAXK) return fail(SG_EINVAL, "fused_map supports at most 16 operands");
   if (dtype != SG_F32 && dtype != SG_F64) return fail(SG_EINVAL, "fused kernels compute in f32 or f64");
@@ -689,6 +690,7 @@ int sg_ew_compile_only(const char* user_src, int k, int dtype, const int* kinds,
 }
 
 int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_tensor* y, void* stream) {
+  SG_NVTX("sg_ew_forward");
   int rc = check_args(kern, k, args);
   if (rc) return rc;
   std::vector<long long> out;
@@ -720,6 +722,7 @@ int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg
 }
 
 int sg_ew_pack(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_tensor* pack, void* stream) {
+  SG_NVTX("sg_ew_pack");
   int rc = check_args(kern, k, args);
   if (rc) return rc;
   std::vector<long long> out;
@@ -741,6 +744,7 @@ int sg_ew_pack(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_te
 
 int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const sg_tensor* ybar,
                sg_tensor* y, sg_tensor* argbars, void* stream) {
+  SG_NVTX("sg_ew_grad");
   int rc = check_args(kern, k, args);
   if (rc) return rc;
   std::vector<long long> out;
@@ -890,6 +894,7 @@ int sg_domain_check(sg_ctx* ctx, void* stream, int32_t* flags) {
 }
 
 int sg_reduce_to(sg_ctx* ctx, const sg_tensor* a, const sg_tensor* b, sg_tensor* out, void* stream) {
+  SG_NVTX("sg_reduce_to");
   if (!ctx || !a || !out) return fail(SG_EINVAL, "null argument");
   if (a->dtype != SG_F32 && a->dtype != SG_F64) return fail(SG_EINVAL, "reduce_to computes in f32/f64");
   if (b && (b->dtype != a->dtype || b->ndim != a->ndim)) return fail(SG_EINVAL, "b must match a");

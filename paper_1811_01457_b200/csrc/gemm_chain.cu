@@ -490,6 +490,7 @@ extern "C" SG_API int sg_chain_cprof(int on, unsigned long long* out8) {
 extern "C" {
 
 int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_chain** out) {
+  SG_NVTX("sg_chain_create");
   if (!ctx || !probs || !out || n <= 0) return fail(SG_EINVAL, "chain: null argument or empty chain");
   if (int rc = ctx_activate(ctx)) return rc;
   const int pairs = std::max(1, ctx_compute_sms(ctx) / 2);
@@ -705,6 +706,7 @@ int sg_chain_create(sg_ctx* ctx, const sg_chain_problem* probs, int32_t n, sg_ch
 }
 
 int sg_chain_run(sg_chain* c, void* stream) {
+  SG_NVTX("sg_chain_run");
   if (!c) return fail(SG_EINVAL, "null chain");
   SG_CUDA_TRY(cudaSetDevice(c->device));
   cudaLaunchConfig_t cfg = {};

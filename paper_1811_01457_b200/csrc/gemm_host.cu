@@ -13,6 +13,7 @@ int ctx_activate(sg_ctx* ctx);
 using namespace sg;
 
 extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
+  SG_NVTX("sg_gemm");
   if (!ctx || !d) return fail(SG_EINVAL, "null argument");
   if (d->M < 0 || d->N < 0 || d->K < 0 || d->M > (1ll << 31) - 1 || d->N > (1ll << 31) - 1 ||
       d->K > (1ll << 31) - 1)
@@ -129,6 +130,7 @@ extern "C" int sg_gemm_splits(sg_ctx* ctx, const sg_gemm_desc* d, int32_t* split
 extern "C" int sg_splitk_reduce_multi(sg_ctx* ctx, int32_t n, const float* const* parts, const int32_t* splits,
                                       const int64_t* M, const int64_t* N, const int64_t* ld_part,
                                       float* const* outs, const int64_t* ld_out, void* stream) {
+  SG_NVTX("sg_splitk_reduce_multi");
   if (!ctx || n < 0 || (n && (!parts || !splits || !M || !N || !ld_part || !outs || !ld_out)))
     return fail(SG_EINVAL, "null argument");
   if (n == 0) return SG_OK;

@@ -617,6 +617,7 @@ int sg_mlp_small_scratch_bytes(const sg_mlp_small_desc* d, int64_t* bytes) {
 int sg_mlp_small_step(sg_ctx* ctx, const sg_mlp_small_desc* d, float* P, float* G, void* S_bf16, const float* X,
                       int64_t ldx, const float* Y, int64_t ldy, float* Z, int64_t ldz, double* loss, void* scratch,
                       int64_t scratch_bytes, void* stream) {
+  SG_NVTX("sg_mlp_small_step");
   if (!ctx || !P || !G || !X || !Y || !loss || !scratch) return fail(SG_EINVAL, "null argument");
   ms::Params p;
   size_t smem = 0, need = 0;

@@ -192,13 +192,21 @@ class Trainer:
         self._small_key = self._small_graph = None  # one-launch step: replayed graph per (X, Y, lr)
 
     def _device_step(self):
+        # NVTX ranges per phase (the C-ABI calls inside carry their own)
+        from torch.cuda import nvtx
+
         e = self.engine
-        e.forward(fuse_loss=True)
-        e.loss_and_seed()
-        e.pullback()
+        with nvtx.range("sgb200.forward"):
+            e.forward(fuse_loss=True)
+        with nvtx.range("sgb200.loss"):
+            e.loss_and_seed()
+        with nvtx.range("sgb200.pullback"):
+            e.pullback()
         if self.dp is not None:
-            self.dp.finish()
-        e.sgd(self.lr)
+            with nvtx.range("sgb200.allreduce_wait"):
+                self.dp.finish()
+        with nvtx.range("sgb200.sgd"):
+            e.sgd(self.lr)
 
     def step(self, X, Y):
         """One training step on (X, Y) already on the device; returns the loss (device)."""
