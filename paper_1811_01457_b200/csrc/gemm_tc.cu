@@ -561,7 +561,7 @@ void aux_map(const GemmArgs& g, tc::KParams& p, CUtensorMap& m, bool wide) {
     return !(e && e[0] == '0');
   }();
   const GemmEpilogue& e = g.epi;
-  if (e.mode == SG_EPI_BIAS_MSE) {
+  if (e.mode == SG_EPI_BIAS_MSE || e.mode == SG_EPI_BIAS_ACT_SEED) {  // fp32 targets / seed
     if (!enabled || !wide || e.out_f32 || !e.seed || p.splits > 1 || g.batch > 1 ||
         (reinterpret_cast<uintptr_t>(e.seed) & 15) || (e.ld_seed * 4) % 16)
       return;
@@ -912,9 +912,16 @@ int dispatch(const GemmArgs& g, int num_sms, cudaStream_t st) {
     const char* e = std::getenv("SGB200_GEMM_WIDE");
     return e && e[0] == '1';
   }();
+  // the seeded forward streams its fp32 seed through the wide slots as well
+  // (SGB200_SEED_TMA=0: read per row from global memory in the narrow kernel)
+  static const bool seed_tma = [] {
+    const char* e = std::getenv("SGB200_SEED_TMA");
+    return !(e && e[0] == '0');
+  }();
   if (pair_ok && g.M >= 256 && num_sms >= 2) {
     // the fused MSE loss streams its fp32 targets through the wide slots
-    if (wide || (g.epi.mode == SG_EPI_BIAS_MSE && !g.epi.out_f32)) {
+    if (wide || ((g.epi.mode == SG_EPI_BIAS_MSE || (g.epi.mode == SG_EPI_BIAS_ACT_SEED && seed_tma)) &&
+                 !g.epi.out_f32)) {
       if (!g.a_mn && !g.b_mn) return run_pair<TF32, false, false, true>(g, num_sms, st);
       if (!g.a_mn && g.b_mn) return run_pair<TF32, false, true, true>(g, num_sms, st);
       if (g.a_mn && g.b_mn) return run_pair<TF32, true, true, true>(g, num_sms, st);

@@ -606,10 +606,26 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
     // the activation's cotangent: dz = seed .* act'(h) with h the bf16
     // activation just stored (the value the pullback reads back otherwise)
     float sd[32];
-    if (row_ok) load_row_f32(e.seed + (long long)m * e.ld_seed + n0, sd, nn);
-    else
+    if (ys.sm) {  // the TMA-staged seed block (SWIZZLE_128B: chunk c of row `lane` at c ^ (lane & 7))
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 y = lds_f4(ys.sm + lane * 128 + ((c ^ (lane & 7)) << 4));
+        sd[4 * c] = y.x, sd[4 * c + 1] = y.y, sd[4 * c + 2] = y.z, sd[4 * c + 3] = y.w;
+      }
+#ifndef SG_NO_AUX_FENCE
+      fence_proxy_async();
+#endif
+      __syncwarp();
+      if (lane == 0 && ys.next_n0 >= 0) aux_issue(ys.base, ys.map, ys.bar, ys.next_n0, ys.row0, 4096);
+      if (!row_ok)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sd[i] = 0.0f;
+    } else if (row_ok) {
+      load_row_f32(e.seed + (long long)m * e.ld_seed + n0, sd, nn);
+    } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) sd[i] = 0.0f;
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
     act_grad_chunk(sd, v, e.act);  // sd *= act'(h)
