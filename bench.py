@@ -113,8 +113,8 @@ class ClockSampler:
         0x0000000000000080: "hw_power_brake_slowdown",
     }
 
-    def __init__(self, device_index: int, period_s: float = 0.002):
-        self.samples, self.reasons = [], set()
+    def __init__(self, device_index: int, period_s: float = float(os.environ.get("SGB200_CLOCK_PERIOD", "0.002"))):
+        self.samples, self.reasons, self.watts = [], set(), []
         self.max_mhz = None
         self.period = period_s
         self._stop = threading.Event()
@@ -135,6 +135,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.watts.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if mask & bit:
@@ -159,7 +160,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "power_w": round(statistics.median(self.watts), 1) if self.watts else None}
 
 
 # --------------------------------------------------------- broadcast (c2)
@@ -688,7 +690,10 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         Y = torch.rand((lb, sizes[-1]), generator=g, device="cuda") * 2 - 1
     stream = torch.cuda.current_stream()
     steps = args.mlp_steps if name != "c1" else max(args.mlp_steps, 50)
-    ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
+    # clocks and power during the timed steps: c4 / c5 run at the power limit
+    # (profiles/r02c_power_probe.log)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
     loss_v = float(tr.engine.loss.item())
     replicas_ok = tr.replicas_identical() if world > 1 else True
     small = tr.engine.small is not None  # the whole step in one cooperative launch
@@ -732,6 +737,7 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         "value": round(batch / (ms * 1e-3), 1), "unit": "samples/s", "ms_per_step": round(ms, 4),
         "flops_per_step": flops, "TFLOPs": round(tflops, 1),
         "roofline": roof,
+        "compute_precision": tr.compute_precision, "clocks": clk.summary(),
         "cuda_graph": bool(tr.use_graph) and not small, "loss_last": loss_v, "n_gpus": world,
         "gpu_launches_per_step": launches,
         "ms_per_step_without_graph": None if no_graph_ms is None else round(no_graph_ms, 4),

@@ -552,6 +552,14 @@ class ChainEngine:
             return None
         return self.csl[l] if hasattr(self, "csl") else self.colsum
 
+    @property
+    def compute_precision(self) -> str:
+        """The arithmetic the training step actually runs: the requested
+        precision, except that a chain small enough for the one-launch step
+        (``small``: c1-sized) computes in fp32 on the CUDA cores -- more
+        accurate than a bf16 / tf32 request, and the tensor cores are not used."""
+        return "fp32" if self.small is not None else self.precision
+
     def _deferred_db(self) -> bool:
         """bf16 pullback without per-layer hooks: dW and dX per layer, every db
         finalised at the end in one launch (sg_colsum_finalize_multi) -- the

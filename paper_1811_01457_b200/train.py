@@ -152,6 +152,12 @@ class Trainer:
 
     MAX_GRAPHS = 4
 
+    @property
+    def compute_precision(self) -> str:
+        """What the step computes in (``ChainEngine.compute_precision``): a
+        c1-sized chain runs its one-launch step in fp32 whatever the request."""
+        return self.engine.compute_precision
+
     def __init__(self, chain: Chain, batch: int, loss: str = "mse", lr: float = 0.05,
                  precision: str = "bf16", dp: bool = False, group=None, graph: bool = False,
                  dp_backend: str | None = None, small: bool = True):

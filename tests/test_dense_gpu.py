@@ -366,6 +366,7 @@ def test_small_chain_step_equals_layer_path_and_trains():
             np.random.default_rng(1))
         tr = Trainer(chain, B, loss="softmax_xent", lr=0.5, precision="bf16", small=small, graph=not small)
         assert (tr.engine.small is not None) == small
+        assert tr.compute_precision == ("fp32" if small else "bf16")  # the API says what runs
         return [float(tr.step(X, Y).item()) for _ in range(20)], tr
 
     ls, trs = run(True)
