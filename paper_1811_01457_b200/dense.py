@@ -30,6 +30,7 @@ fold order, everything in fp32/fp64).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass
 
@@ -512,15 +513,9 @@ class ChainEngine:
         # are reduced in ONE launch after the pullback (sg_splitk_reduce_multi,
         # the same ordered sum) -- the per-layer reduce launch sat between the
         # layer's dW and the next dX.  SGB200_DEFER_SPLITK=0 reduces per GEMM.
-        self.dw_split = [None] * self.L
-        if hasattr(self, "csl") and os.environ.get("SGB200_DEFER_SPLITK", "1") != "0":
-            from .gemm import gemm_desc, gemm_splits
-
-            for l in range(self.L):
-                splits, ld = gemm_splits(gemm_desc(self.dz_of(l), self.H[l], a_mn=True, b_mn=True, out=self.gW[l]))
-                if splits > 1:
-                    part = torch.empty(splits * self.sizes[l + 1] * ld, dtype=torch.float32, device=dev)
-                    self.dw_split[l] = (part, splits, ld)
+        # (planned on the first deferred pullback -- an eager step, before any
+        # graph capture -- so a data-parallel engine never allocates them)
+        self.dw_split = None
         if chain.layers[0].W is not None:
             self.set_params([(l.W, l.b) for l in chain.layers])
 
@@ -714,12 +709,30 @@ class ChainEngine:
         rt.check(lib.sg_colsum_finalize_multi(rt.context(), n, parts, G, ld, N, outs, rt.stream_ptr()),
                  "sg_colsum_finalize_multi")
 
+    def _dw_split_plan(self):
+        """Per layer (partials, splits, ld) of a dW GEMM that splits K, else None."""
+        if self.dw_split is None:
+            import torch
+
+            from .gemm import gemm_desc, gemm_splits
+
+            self.dw_split = [None] * self.L
+            if os.environ.get("SGB200_DEFER_SPLITK", "1") != "0":
+                for l in range(self.L):
+                    splits, ld = gemm_splits(gemm_desc(self.dz_of(l), self.H[l], a_mn=True, b_mn=True,
+                                                       out=self.gW[l]))
+                    if splits > 1:
+                        part = torch.empty(splits * self.sizes[l + 1] * ld, dtype=torch.float32,
+                                           device=self.P.device)
+                        self.dw_split[l] = (part, splits, ld)
+        return self.dw_split
+
     def _reduce_all_dw(self):
         """dW_l = sum of its deferred split-K partials, every split layer in one launch."""
         from .gemm import splitk_reduce
 
         splitk_reduce([(sp[0], sp[1], self.sizes[l + 1], self.sizes[l], sp[2], self.gW[l])
-                       for l, sp in enumerate(self.dw_split) if sp is not None])
+                       for l, sp in enumerate(self._dw_split_plan()) if sp is not None])
 
     def _chain_backward(self, _ctx):
         """Chained pullback: every layer's dX (with the lower layer's act' and
@@ -814,7 +827,7 @@ class ChainEngine:
                 # db of every layer after layer 0's (rules.py:45-46)
                 from .gemm import gemm
 
-                sp = self.dw_split[l]
+                sp = self._dw_split_plan()[l]
                 gemm(dz, self.H[l], a_mn=True, b_mn=True, out=self.gW[l], split_part=None if sp is None else sp[0])
                 if l > 0:
                     act_prev = self.acts[l - 1]

@@ -591,14 +591,15 @@ def test_deferred_splitk_is_bit_identical():
         os.environ["SGB200_DEFER_SPLITK"] = defer
         try:
             e = ChainEngine(chain, B, "mse", "bf16", small=False)
+            e._dw_split_plan()  # planned while the knob is set
         finally:
             del os.environ["SGB200_DEFER_SPLITK"]
-        assert (sum(sp is not None for sp in e.dw_split) > 0) == (defer == "1")
         e.load_batch(X, Y)
         e.forward(fuse_loss=True)
         e.loss_and_seed()
         e.pullback()
         torch.cuda.synchronize()
+        assert (sum(sp is not None for sp in e.dw_split) > 0) == (defer == "1")
         grads.append(e.G.clone())
     assert torch.equal(grads[0], grads[1])
     # the binding alone: partials + one multi-job reduce == the GEMM's own reduce
