@@ -254,25 +254,36 @@ __global__ void __launch_bounds__(256) k_mse_v8(const float* z, long long ldz, c
 // --- out[n] = sum_g part[g][n], fixed order, fp64 accumulation
 // 8 columns (one 32-byte sector) x 32 row groups per block: many blocks even
 // for narrow layers, each thread folds g = ty, ty+32, ... then a fixed fold over ty.
-__global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
-                                                          float* out) {
-  SG_GRID_WAIT();
-  constexpr int RG = 128;  // row groups per block (1024 threads = 8 columns x 128)
-  __shared__ double red[RG][9];
-  const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
-  const long long j = blockIdx.x * 8ll + tx;
-  double acc = 0.0;
-  if (j < N) {
+// Block = 32 columns x 32 threads; thread ty folds the 128 slices ty, ty+32,
+// ty+64, ty+96 (slice s: row groups g = s, s+128, ..., ascending), then a
+// fixed tree over the 128 slices -- the order of a 128-thread-per-column
+// fold, with coalesced 128-byte rows and a quarter of the blocks of one.
+__device__ __forceinline__ void colsum_finalize_block(const float* part, long long G, long long ldp, long long N,
+                                                      float* out, long long j0) {
+  constexpr int RG = 128;  // slices per column
+  __shared__ double red[RG][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const long long j = j0 + tx;
+#pragma unroll
+  for (int i = 0; i < RG / 32; ++i) {
+    double acc = 0.0;
+    if (j < N) {
 #pragma unroll 4
-    for (long long g = ty; g < G; g += RG) acc += (double)part[g * ldp + j];
+      for (long long g = ty + 32 * i; g < G; g += RG) acc += (double)part[g * ldp + j];
+    }
+    red[ty + 32 * i][tx] = acc;
   }
-  red[ty][tx] = acc;
   __syncthreads();
-  for (int s = RG / 2; s > 0; s >>= 1) {  // fixed-order tree over the row groups
-    if (ty < s) red[ty][tx] += red[ty + s][tx];
+  for (int s = RG / 2; s > 0; s >>= 1) {  // fixed-order tree over the slices
+    for (int r = ty; r < s; r += 32) red[r][tx] += red[r + s][tx];
     __syncthreads();
   }
   if (ty == 0 && j < N) out[j] = (float)red[0][tx];
+}
+__global__ void __launch_bounds__(1024) k_colsum_finalize(const float* part, long long G, long long ldp, long long N,
+                                                          float* out) {
+  SG_GRID_WAIT();
+  colsum_finalize_block(part, G, ldp, N, out, blockIdx.x * 32ll);
   SG_GRID_TRIGGER();
 }
 
@@ -286,26 +297,9 @@ struct ColsumJobs {
 };
 __global__ void __launch_bounds__(1024) k_colsum_finalize_multi(const __grid_constant__ ColsumJobs jobs) {
   SG_GRID_WAIT();
-  constexpr int RG = 128;
-  __shared__ double red[RG][9];
   const int b = blockIdx.y;
-  const long long N = jobs.N[b], G = jobs.G[b], ldp = jobs.ldp[b];
-  if (blockIdx.x * 8ll >= N) return;  // block-uniform
-  const float* part = jobs.part[b];
-  const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
-  const long long j = blockIdx.x * 8ll + tx;
-  double acc = 0.0;
-  if (j < N) {
-#pragma unroll 4
-    for (long long g = ty; g < G; g += RG) acc += (double)part[g * ldp + j];
-  }
-  red[ty][tx] = acc;
-  __syncthreads();
-  for (int s = RG / 2; s > 0; s >>= 1) {
-    if (ty < s) red[ty][tx] += red[ty + s][tx];
-    __syncthreads();
-  }
-  if (ty == 0 && j < N) jobs.out[b][j] = (float)red[0][tx];
+  if (blockIdx.x * 32ll < jobs.N[b])  // block-uniform
+    colsum_finalize_block(jobs.part[b], jobs.G[b], jobs.ldp[b], jobs.N[b], jobs.out[b], blockIdx.x * 32ll);
   SG_GRID_TRIGGER();
 }
 
@@ -740,7 +734,7 @@ namespace sg {
 int colsum_finalize_launch(const float* part, long long G, long long ld, long long N, float* out, int,
                            cudaStream_t st) {
   if (N <= 0) return SG_OK;
-  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 7) / 8)), dim3(1024), 0, st, part, G, ld, N, out));
+  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 31) / 32)), dim3(1024), 0, st, part, G, ld, N, out));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
 }
@@ -807,7 +801,7 @@ int sg_colsum_finalize(sg_ctx* ctx, const float* part, int64_t G, int64_t ld_par
   if (N <= 0) return SG_OK;
   int rc = ctx_activate(ctx);
   if (rc) return rc;
-  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 7) / 8)), dim3(1024), 0, (cudaStream_t)stream, part, G, ld_part, N,
+  SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize, dim3((unsigned)((N + 31) / 32)), dim3(1024), 0, (cudaStream_t)stream, part, G, ld_part, N,
                                                                                              out));
   SG_CUDA_TRY(cudaGetLastError());
   return SG_OK;
@@ -833,7 +827,7 @@ int sg_colsum_finalize_multi(sg_ctx* ctx, int32_t n, const float* const* parts, 
       jobs.N[i] = N[b0 + i];
       nmax = std::max(nmax, (long long)N[b0 + i]);
     }
-    SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize_multi, dim3(dim3((unsigned)((nmax + 7) / 8), (unsigned)nb)), dim3(1024), 0, (cudaStream_t)stream, 
+    SG_CUDA_TRY(pdl_launch(dk::k_colsum_finalize_multi, dim3(dim3((unsigned)((nmax + 31) / 32), (unsigned)nb)), dim3(1024), 0, (cudaStream_t)stream, 
         jobs));
     SG_CUDA_TRY(cudaGetLastError());
   }
