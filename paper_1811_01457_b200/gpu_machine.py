@@ -523,6 +523,27 @@ def eval_function(module, name: str, args: tuple, step_limit: int = DEFAULT_STEP
     return GpuMachine(module, step_limit).call(name, args)
 
 
+def _reference_transforms():
+    """The reference's host-side IR transforms (``augment``, ``vectorize``:
+    reverse_ad.py:619-630, spmd_batch.py) -- out of this repo's scope (they
+    emit IR, they compute nothing).  Taken from an importable ``ssagrad``, else
+    from the reference install this repo's bench uses (``baseline/_ref``)."""
+    try:
+        import ssagrad
+    except ImportError:
+        import os
+        import sys
+
+        ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+        if not os.path.isdir(os.path.join(ref, "ssagrad")):
+            raise ImportError("grad / batched_grad need the reference's IR transform (ssagrad.augment / "
+                              "vectorize) for a module without {name}__aug / __pb: install the reference "
+                              "(baseline/_ref) or pass augment= / vectorize=, or parse a pre-augmented module")
+        sys.path.append(ref)
+        import ssagrad
+    return ssagrad.augment, ssagrad.vectorize
+
+
 def grad(module, name: str, args: tuple, seeds: tuple | None = None, step_limit: int = DEFAULT_STEP_LIMIT,
          augment=None) -> dict:
     """``reverse_ad.grad`` (reverse_ad.py:633-663) running the aug/pb pair on the GPU.
@@ -541,7 +562,7 @@ def grad(module, name: str, args: tuple, seeds: tuple | None = None, step_limit:
     aug, pb = f"{name}__aug", f"{name}__pb"
     if aug not in module.functions or pb not in module.functions:
         if augment is None:
-            from ssagrad import augment  # the reference transform (host-side IR)
+            augment = _reference_transforms()[0]  # the reference transform (host-side IR)
         augment(module, name)
     m = GpuMachine(module, step_limit)
     out = m.call(aug, tuple(args))
@@ -568,10 +589,8 @@ def batched_grad(module, name: str, lanes: int, stacked_args: tuple, seeds: tupl
     fn = module.get(name)
     vaug, vpb = f"{name}__aug__batched_B{lanes}", f"{name}__pb__batched_B{lanes}"
     if vaug not in module.functions or vpb not in module.functions:
-        if vectorize is None:
-            from ssagrad import augment, vectorize  # the reference transforms (host-side IR)
-        else:
-            from ssagrad import augment
+        augment, ref_vectorize = _reference_transforms()  # the reference transforms (host-side IR)
+        vectorize = vectorize or ref_vectorize
         a, p = augment(module, name)
         vectorize(module, a.name, lanes)
         vectorize(module, p.name, lanes)

@@ -228,3 +228,24 @@ def test_device_tape_backprop_matches_reference(golden, key):
         got = [g[pv] for pv, ty in fn.params if ty.kind in ("f64", "tensor")]
         for gv, want in zip(got, case["grads"]):
             assert max_rel(gv, decode(want)) <= 1e-12, case["fn"]
+
+
+def test_reference_transforms_come_from_the_installed_reference():
+    """grad / batched_grad take the reference's own IR transforms (augment,
+    vectorize: host-side IR, out of scope here) from an importable ssagrad or
+    the bench's reference install (baseline/_ref); without either they fail
+    with an ImportError that says what to do (no silent fallback)."""
+    from paper_1811_01457_b200 import gpu_machine as G
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    try:
+        import ssagrad  # noqa: F401
+        have = True
+    except ImportError:
+        have = os.path.isdir(os.path.join(ref, "ssagrad"))
+    if not have:
+        with pytest.raises(ImportError, match="reference's IR transform"):
+            G._reference_transforms()
+        return
+    augment, vectorize = G._reference_transforms()
+    assert callable(augment) and callable(vectorize)
