@@ -36,10 +36,25 @@ struct GemmEpilogue {
 // Column sums of a 32x32 block held one row per lane (v[i] = column i):
 // a 31-shuffle transpose-reduce leaves column L's sum in lane L, summed in a
 // fixed order (deterministic).  v is destroyed.
+// (the adds in packed fp32x2 pairs -- FADD2, the same roundings -- unless
+// SG_EPI_SCALAR_MATH)
 __device__ __forceinline__ void warp_colsum_store(float (&v)[32], float* dst, int lane, int n) {
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) {
     const bool upper = (lane & s) != 0;
+#if !defined(SG_EPI_SCALAR_MATH) || !SG_EPI_SCALAR_MATH
+    if (s >= 2) {
+#pragma unroll
+      for (int i = 0; i < s; i += 2) {
+        const float r0 = __shfl_xor_sync(0xffffffffu, upper ? v[i] : v[i + s], s);
+        const float r1 = __shfl_xor_sync(0xffffffffu, upper ? v[i + 1] : v[i + 1 + s], s);
+        const float2 k = make_float2(upper ? v[i + s] : v[i], upper ? v[i + 1 + s] : v[i + 1]);
+        const float2 r = __fadd2_rn(k, make_float2(r0, r1));
+        v[i] = r.x, v[i + 1] = r.y;
+      }
+      continue;
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < s; ++i) {
       const float send = upper ? v[i] : v[i + s];

@@ -201,7 +201,36 @@ __device__ __forceinline__ void act_fwd_chunk(float (&v)[32], int act) {
     for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
   }
 }
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100): two lanes of
+// work per instruction with the same per-element roundings as the scalar
+// forms (an FFMA2 rounds each half like an FFMA).  SG_EPI_SCALAR_MATH=1
+// compiles the scalar forms.
+#ifndef SG_EPI_SCALAR_MATH
+#define SG_EPI_SCALAR_MATH 0
+#endif
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ void act_grad_chunk(float (&v)[32], const float (&h)[32], int act) {
+#if !SG_EPI_SCALAR_MATH
+  if (act == SG_ACT_SIGMOID) {  // v * (h * (1 - h)), the scalar form's three roundings
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float2 hh = f2(h[i], h[i + 1]);
+      const float2 t = __fmul2_rn(hh, __fadd2_rn(f2(1.0f, 1.0f), f2(-h[i], -h[i + 1])));
+      const float2 r = __fmul2_rn(f2(v[i], v[i + 1]), t);
+      v[i] = r.x, v[i + 1] = r.y;
+    }
+    return;
+  }
+  if (act == SG_ACT_TANH) {  // v * fma(-h, h, 1): the contracted scalar form
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float2 t = __ffma2_rn(f2(-h[i], -h[i + 1]), f2(h[i], h[i + 1]), f2(1.0f, 1.0f));
+      const float2 r = __fmul2_rn(f2(v[i], v[i + 1]), t);
+      v[i] = r.x, v[i + 1] = r.y;
+    }
+    return;
+  }
+#endif
   if (act == SG_ACT_SIGMOID) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= h[i] * (1.0f - h[i]);
@@ -490,8 +519,16 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
 #pragma unroll
         for (int i = 0; i < 32; ++i) bv[i] = n0 + i < p.N ? __ldg(e.bias + n0 + i) : 0.0f;
       }
+#if !SG_EPI_SCALAR_MATH
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const float2 r = __fadd2_rn(f2(v[i], v[i + 1]), f2(bv[i], bv[i + 1]));
+        v[i] = r.x, v[i + 1] = r.y;
+      }
+#else
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] += bv[i];
+#endif
       SG_CPROF(6);  // bias loaded and added
     }
     if (e.out_pre) store_row_f32(e.out_pre + (long long)m * e.ld_pre + n0, v, nn);
