@@ -114,7 +114,7 @@ class ClockSampler:
     }
 
     def __init__(self, device_index: int, period_s: float = float(os.environ.get("SGB200_CLOCK_PERIOD", "0.002"))):
-        self.samples, self.reasons, self.watts = [], set(), []
+        self.samples, self.reasons = [], set()
         self.max_mhz = None
         self.period = period_s
         self._stop = threading.Event()
@@ -135,7 +135,6 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                self.watts.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if mask & bit:
@@ -160,8 +159,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples),
-                "power_w": round(statistics.median(self.watts), 1) if self.watts else None}
+                "samples": len(self.samples)}
 
 
 # --------------------------------------------------------- broadcast (c2)
@@ -690,8 +688,10 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         Y = torch.rand((lb, sizes[-1]), generator=g, device="cuda") * 2 - 1
     stream = torch.cuda.current_stream()
     steps = args.mlp_steps if name != "c1" else max(args.mlp_steps, 50)
-    # clocks and power during the timed steps: c4 / c5 run at the power limit
-    # (profiles/r02c_power_probe.log)
+    # SM clocks during the timed steps (the bench's short windows run at boost
+    # clocks; sustained, c4 / c5 sit at the power limit: DESIGN §4,
+    # profiles/r02c_power_probe.log -- NVML's power reading averages over ~1 s,
+    # too long for these windows, so it is not reported here)
     with ClockSampler(torch.cuda.current_device()) as clk:
         ms, _ = _timed(lambda ev: tr.step(X, Y), steps, max(3, args.warmup), dist, stream)
     loss_v = float(tr.engine.loss.item())

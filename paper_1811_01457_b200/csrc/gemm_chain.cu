@@ -232,6 +232,9 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
   grid_dep_launch();
   SG_TRACE_BEGIN();
 
+  if (warp < EPI_WARP0) {
+  // registers to the epilogue warpgroups (warpgroup-collective; as gemm_tc_kernel)
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
@@ -317,7 +320,9 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
         }
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     // ===================== epilogue (both CTAs, own 128 rows) =====================
     const int ew = warp - EPI_WARP0;
     const int q = ew % 4;

@@ -99,6 +99,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   grid_dep_wait();
   grid_dep_launch();
 
+  if (warp < EPI_WARP0) {
+  // The TMA / MMA / TMEM warpgroup hands registers to the epilogue warpgroups
+  // (warpgroup-collective setmaxnreg; ptxas allocates each branch to its own
+  // limit): the 32-column epilogue chunks no longer spill at the 168 cap.
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
@@ -175,7 +180,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");  // (65536 - 128 x 56) / 256, rounded to 8
     // ===================== epilogue =====================
     const int ew = warp - EPI_WARP0;
     const int q = ew % 4;   // TMEM lanes 32q..32q+31 (a warp may only touch lanes 32*(warp%4)..)
