@@ -494,7 +494,7 @@ np.save(sys.argv[1], np.concatenate([e.G.double().cpu().numpy(), e.loss.cpu().nu
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520)])
+@pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520), (777, 522)])
 def test_value_and_pullback_fuses_the_seed(M, D):
     """DenseLayer.value_and_pullback (the forward GEMM's epilogue also forms
     dZ = ybar .* act'(H) and its column sums) against the same layer's
@@ -572,17 +572,18 @@ def test_fused_mse_loss_matches_separate_loss_kernel(sizes, B):
         assert torch.equal(G0[wo:bo], G1[wo:bo])
 
 
-def test_deferred_splitk_is_bit_identical():
+@pytest.mark.parametrize("sizes", [(256, 384, 256, 128), (300, 333, 130, 72)])
+def test_deferred_splitk_is_bit_identical(sizes):
     """Deferred split-K (a dW GEMM's partials left in its own buffer, every
     layer's reduced in one sg_splitk_reduce_multi launch after the pullback)
     against the per-GEMM reduce: identical dW and db, and the split actually
-    happens for these narrow layers (K = batch >> M = N)."""
+    happens for these narrow layers (K = batch >> M = N); ragged widths too."""
     import os
 
     from paper_1811_01457_b200.gemm import gemm, gemm_splits, gemm_desc, splitk_reduce
 
     rng = np.random.default_rng(11)
-    sizes, acts, B = (256, 384, 256, 128), ("tanh", "tanh", "identity"), 16384
+    acts, B = ("tanh", "tanh", "identity"), 16384
     chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(3)]).init_params(rng)
     X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
     Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
