@@ -56,3 +56,19 @@ for i in range(20):
 torch.cuda.synchronize()
 print(f"  event-split: K1 {sum(e[0].elapsed_time(e[1]) for e in ev) / 20:.4f} ms, "
       f"K2 {sum(e[1].elapsed_time(e[2]) for e in ev) / 20:.4f} ms")
+
+# what precedes K2: another K2, K1, a read-only kernel, a write-heavy copy (event-split)
+scratch = torch.empty_like(x)
+for label, pre in (("K2", k2), ("K1", k1), ("sum(x) read-only", lambda: x.sum()),
+                   ("copy x->scratch", lambda: scratch.copy_(x)), ("fill scratch", lambda: scratch.fill_(1.0))):
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(10)]
+    for _ in range(3):
+        pre()
+        k2()
+    for i in range(10):
+        pre()
+        ev[i][0].record()
+        k2()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    print(f"  K2 after {label:18s} {sum(e[0].elapsed_time(e[1]) for e in ev) / 10:.4f} ms")
