@@ -464,25 +464,32 @@ def cpu_baseline_broadcast(rows=64):
 
 # ------------------------------------------------------- dense workloads
 def _timed(fn, steps, warmup, dist, stream, per_step_events=None):
-    """CUDA-event time of `steps` calls (max over ranks), after `warmup` calls."""
+    """CUDA-event time of `steps` calls (max over ranks), after `warmup` calls.
+    The timed loop records no events between kernels (they break the
+    programmatic-dependent-launch overlap and stretch the kernel after them);
+    with `per_step_events`, a SEPARATE run of `steps` calls records them for
+    the per-kernel split."""
     import torch
 
     for _ in range(warmup):
         fn(None)
     barrier(dist)
     s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    evs = []
     s.record(stream)
     for i in range(steps):
-        ev = None
-        if per_step_events:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(per_step_events)]
-            evs.append(ev)
-        fn(ev)
+        fn(None)
     t.record(stream)
     torch.cuda.synchronize()
     barrier(dist)
-    return max_over_ranks(dist, s.elapsed_time(t)) / steps, evs
+    ms = max_over_ranks(dist, s.elapsed_time(t)) / steps
+    evs = []
+    if per_step_events:
+        for i in range(steps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(per_step_events)]
+            evs.append(ev)
+            fn(ev)
+        torch.cuda.synchronize()
+    return ms, evs
 
 
 def broadcast_variant_bench(args, dist, peaks, variant):
