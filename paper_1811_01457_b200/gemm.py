@@ -158,9 +158,12 @@ def splitk_reduce(jobs, stream=None) -> None:
     n = len(jobs)
     if n == 0:
         return
+    import torch
+
     for part, splits, M, N, ld, out in jobs:
-        if part.dtype.itemsize != 4 or out.dim() != 2 or out.shape[0] < M or out.shape[1] < N:
-            raise ValueError("splitk_reduce: fp32 partials and an M x N fp32 output")
+        if (part.dtype != torch.float32 or out.dtype != torch.float32 or not part.is_contiguous()
+                or out.dim() != 2 or out.shape[0] < M or out.shape[1] < N or ld < N):
+            raise ValueError("splitk_reduce: contiguous fp32 partials (ld >= N) and an M x N fp32 output")
         if part.numel() < splits * M * ld:
             raise ValueError(f"splitk_reduce: {part.numel()} partials, {splits * M * ld} needed")
     A = ctypes.c_void_p * n
