@@ -470,11 +470,14 @@ class ChainEngine:
         # independent GEMMs -- in ONE persistent launch (the dW's K-splits and
         # the dX tiles share the CTA pairs: no idle pairs beside the split-K
         # dW, one fill / drain instead of two), every db finalised at the end.
+        # "forward" (SGB200_CHAIN=3): only the forward GEMMs below the top layer
+        # as one chain; the top layer (with its fused loss) and the pullback
+        # layer by layer.
         if gemm_chain is None:
-            gemm_chain = {"1": "full", "2": "pairwise"}.get(os.environ.get("SGB200_CHAIN", "0"))
+            gemm_chain = {"1": "full", "2": "pairwise", "3": "forward"}.get(os.environ.get("SGB200_CHAIN", "0"))
         elif gemm_chain is True:
             gemm_chain = "full"
-        if gemm_chain not in (None, False, "full", "pairwise"):
+        if gemm_chain not in (None, False, "full", "pairwise", "forward"):
             raise ValueError(f"unknown gemm_chain mode {gemm_chain!r}")
         self.chainable = bool(gemm_chain) and precision == "bf16" and self.L >= 2
         self.chain_mode = gemm_chain if self.chainable else None
@@ -615,6 +618,16 @@ class ChainEngine:
             self.tape.push(TapeEntry("dense_chain", tuple(self.H) + tuple(self.W), self._chain_backward, None))
             return self.Zt
         L = self.L
+        if use_chain and self.chain_mode == "forward":
+            self.chains[0].run()  # layers 0 .. L-2 in one launch
+            top = L - 1
+            if fuse:
+                self._top_forward_mse()
+            else:
+                dense_forward(self.descs[top], H=None, H_f32=self.Zt)
+            for l in range(L):  # the pullback layer by layer, as without chains
+                self.tape.push(TapeEntry(f"dense{l}", (self.H[l], self.W[l]), self._make_backward(l), self._ready(l)))
+            return None if fuse else self.Zt
         if use_chain:  # pairwise: per-layer forward GEMMs, the pullback in L launches
             for l in range(L):
                 last = l == L - 1
@@ -655,6 +668,11 @@ class ChainEngine:
 
         L, B = self.L, self.B
         pairs = max(1, torch.cuda.get_device_properties(self.P.device).multi_processor_count // 2)
+        if self.chain_mode == "forward":
+            fwd = [(gemm_desc(self.H[l], self.Ws[l], epilogue="bias_act", act=self.acts[l], bias=self.b[l],
+                              out_lp=self.H[l + 1]), 1, [("rows", l - 1)] if l > 0 else [])
+                   for l in range(L - 1)]
+            return GemmChain(fwd), None
         if self.chain_mode == "pairwise":
             per_layer = []
             for l in range(L):

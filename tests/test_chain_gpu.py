@@ -130,3 +130,29 @@ def test_chained_training_run_matches_layer_path():
     assert runs[False][0] == runs[True][0]
     assert torch.equal(runs[False][1], runs[True][1])
     assert runs[True][0][-1] < runs[True][0][0]
+
+
+def test_forward_chain_mode_matches_layer_path():
+    """SGB200_CHAIN=3: the forward GEMMs below the top layer as ONE chain, the
+    top layer (fused MSE) and the pullback layer by layer -- the same kernels'
+    arithmetic, so losses and parameters equal the per-layer path's."""
+    import os
+
+    rng = np.random.default_rng(5)
+    sizes, acts, B = (384, 512, 512, 640, 256), ("tanh", "relu", "tanh", "identity"), 3000
+    X = torch.from_numpy(rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)).cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)).cuda()
+    runs = {}
+    for mode in ("0", "3"):
+        os.environ["SGB200_CHAIN"] = mode
+        try:
+            chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(4)]).init_params(
+                np.random.default_rng(1))
+            tr = Trainer(chain, B, loss="mse", lr=1e-3, precision="bf16", graph=True)
+            assert tr.engine.chain_mode == (None if mode == "0" else "forward")
+            losses = [float(tr.step(X, Y).item()) for _ in range(5)]
+            runs[mode] = (losses, tr.engine.P.clone())
+        finally:
+            del os.environ["SGB200_CHAIN"]
+    assert runs["0"][0] == runs["3"][0]
+    assert torch.equal(runs["0"][1], runs["3"][1])
