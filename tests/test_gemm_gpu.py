@@ -40,7 +40,9 @@ def check_close(got, a, b, tol=1e-5):
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 200, 104), (1000, 520, 776), (7, 10, 32),
                                    (256, 64, 4096), (129, 257, 136),
                                    # CTA-pair (cta_group::2) tiles, partial pair tiles, split-K
-                                   (1024, 768, 512), (520, 300, 200), (256, 256, 8192), (768, 1024, 2048)])
+                                   (1024, 768, 512), (520, 300, 200), (256, 256, 8192), (768, 1024, 2048),
+                                   # degenerate extents: one row / column, K below one k-block
+                                   (1, 1, 8), (1, 300, 64), (300, 1, 64), (33, 17, 8), (2048, 16, 16)])
 @pytest.mark.parametrize("layout", ["kk", "k_mn", "mn_mn"])
 def test_bf16_tensor_core_gemm(M, N, K, layout):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
