@@ -213,6 +213,24 @@ int broadcast_shape(int k, const sg_tensor* args, std::vector<long long>& out) {
     }
     out = r;
   }
+  // Every operand must then expand to the result (tensor.py:124-132
+  // can_expand, raised by bcast_to from interp.py's _spread_flat): the
+  // reference's max() rule makes a zero extent against 1 (or against the
+  // scalar start) a result extent of 1, which a zero-extent operand cannot
+  // fill -- the reference raises ValueError for any empty tensor operand.
+  for (int i = 0; i < k; ++i) {
+    const sg_tensor& a = args[i];
+    if (a.ndim == 0) continue;
+    for (int j = 1; j <= a.ndim; ++j) {
+      const long long d = a.shape[a.ndim - j];
+      if (d != out[out.size() - j] && d != 1) {
+        std::ostringstream m;
+        m << "cannot broadcast operand " << i << " (extent " << d << ") to the result extent "
+          << out[out.size() - j];
+        return fail(SG_EINVAL, m.str());
+      }
+    }
+  }
   return SG_OK;
 }
 
@@ -230,6 +248,12 @@ void fold_rows(Shape2D& s) {
       s.C = w;
       return;
     }
+}
+
+long long elems(const std::vector<long long>& shape) {
+  long long n = 1;
+  for (long long d : shape) n *= d;
+  return n;
 }
 
 void canonicalise(int k, const sg_tensor* args, const std::vector<long long>& out, Shape2D& s) {
@@ -696,6 +720,7 @@ int sg_ew_forward(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg
   std::vector<long long> out;
   if ((rc = broadcast_shape(k, args, out))) return rc;
   if ((rc = check_out(y, out, kern->dtype, "y"))) return rc;
+  if (elems(out) == 0) return SG_OK;  // an empty broadcast: nothing to compute
   Shape2D s;
   canonicalise(k, args, out, s);
   const void* extra[] = {y->ptr};
@@ -728,6 +753,7 @@ int sg_ew_pack(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, sg_te
   std::vector<long long> out;
   if ((rc = broadcast_shape(k, args, out))) return rc;
   if ((rc = check_out(pack, out, kern->dtype, "pack", 1 + k))) return rc;
+  if (elems(out) == 0) return SG_OK;
   Shape2D s;
   canonicalise(k, args, out, s);
   const void* extra[] = {pack->ptr};
@@ -753,8 +779,18 @@ int sg_ew_grad(sg_ctx* ctx, sg_kernel* kern, int k, const sg_tensor* args, const
   if (y && y->ptr && (rc = check_out(y, out, kern->dtype, "y"))) return rc;
   for (int i = 0; i < k; ++i) {
     long long want = args[i].ndim == 0 ? 1 : numel(args[i]);
-    if (argbars[i].dtype != kern->dtype || numel(argbars[i]) != want || !argbars[i].ptr)
+    if (argbars[i].dtype != kern->dtype || numel(argbars[i]) != want || (!argbars[i].ptr && want))
       return fail(SG_EINVAL, "argbar " + std::to_string(i) + " does not match its operand");
+  }
+  if (elems(out) == 0) {
+    // an empty broadcast: every cotangent is a sum of zero terms (reduce_like,
+    // rules.py:302-311 / tensor.py:327-345) -- zeros
+    for (int i = 0; i < k; ++i) {
+      const long long want = args[i].ndim == 0 ? 1 : numel(args[i]);
+      if (want) SG_CUDA_TRY(cudaMemsetAsync(argbars[i].ptr, 0, (size_t)want * dtype_size(kern->dtype),
+                                            (cudaStream_t)stream));
+    }
+    return SG_OK;
   }
   Shape2D s;
   canonicalise(k, args, out, s);

@@ -169,6 +169,15 @@ def _broadcast(vals) -> tuple:
                 raise ValueError(f"shapes {shape} and {s} do not broadcast")
             out.append(max(a, b))
         shape = tuple(reversed(out))
+    # tensor.py:124-132 (can_expand, via bcast_to in interp.py's _spread_flat):
+    # with the max() rule above a zero extent meets 1 as 1, and an empty
+    # operand cannot fill it -- the reference raises ValueError
+    for v in vals:
+        if isinstance(v, float):
+            continue
+        s = tuple(v.shape)
+        if any(s[-i] != shape[-i] and s[-i] != 1 for i in range(1, len(s) + 1)):
+            raise ValueError(f"cannot broadcast {s} to {shape}")
     return shape
 
 

@@ -251,3 +251,21 @@ def test_ctypes_mirrors_match_the_c_header(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(cls), cname
         for fname, _ in cls._fields_:
             assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
+
+
+def test_broadcast_rule_rejects_empty_operands_like_the_reference():
+    """fused._broadcast: the reference's max() extents (tensor.py:108-121) and
+    its can_expand check (tensor.py:124-132): an empty operand raises the
+    reference's ValueError before anything reaches the device."""
+    import numpy as np
+
+    from paper_1811_01457_b200.fused import _broadcast
+
+    assert _broadcast([np.zeros((3, 1)), np.zeros((4,)), 0.5]) == (3, 4)
+    assert _broadcast([np.zeros((1,)), np.zeros((6, 1))]) == (6, 1)
+    for shapes, msg in (([(0,), (0,)], "(0,) to (1,)"), ([(5,), (0, 5)], "(0, 5) to (1, 5)"),
+                        ([(0,), (3, 0)], "(0,) to (3, 1)")):
+        with pytest.raises(ValueError, match=r"cannot broadcast " + re.escape(msg)):
+            _broadcast([np.zeros(s) for s in shapes])
+    with pytest.raises(ValueError, match="do not broadcast"):
+        _broadcast([np.zeros((3,)), np.zeros((4,))])

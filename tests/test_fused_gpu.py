@@ -8,6 +8,7 @@ the reference suite, pkg/tests/conftest.py:137-144):
 """
 
 import math
+import re
 
 import numpy as np
 import pytest
@@ -387,3 +388,44 @@ def test_random_broadcast_patterns_f32(fused_module):
             bound = OS.reduce_to(np.abs(terms), tgt)
             err = np.abs(np.asarray(bar.double().cpu().numpy()).reshape(np.shape(want)) - want)
             assert (err <= 1e-6 * np.maximum(1.0, bound) + 1e-7).all(), (case, i, out, shapes)
+
+
+@pytest.mark.parametrize("xshape,ashape,msg", [((0,), (0,), "(0,) to (1,)"), ((0, 5), (5,), "(0, 5) to (1, 5)"),
+                                               ((3, 0), (0,), "(0,) to (3, 1)")])
+def test_empty_operands_raise_like_the_reference(fused_module, xshape, ashape, msg):
+    """The reference broadcasts extents with max() (tensor.py:108-121), so an
+    empty operand meets a result extent of 1 it cannot fill, and bcast_to
+    raises ValueError("cannot broadcast ...") (tensor.py:124-140, from
+    interp.py's _spread_flat) -- for fused_map and fused_map_with_partials
+    alike (checked against the unmodified reference: the messages below are
+    its own).  The device path raises the same, before any launch."""
+    args = [torch.zeros(ashape, device="cuda", dtype=torch.float64) + 0.5,
+            torch.zeros(xshape, device="cuda", dtype=torch.float64) + 0.2,
+            torch.zeros(ashape, device="cuda", dtype=torch.float64) + 0.1]
+    yb = torch.zeros(xshape, device="cuda", dtype=torch.float64)
+    for call in (lambda: F.fused_map(fused_module, "affsig", args),
+                 lambda: F.fused_map_with_partials(fused_module, "affsig", args),
+                 lambda: F.fused_map_grad(fused_module, "affsig", args, yb)):
+        with pytest.raises(ValueError, match=r"cannot broadcast " + re.escape(msg)):
+            call()
+    torch.cuda.synchronize()  # and nothing faulted on the device
+
+
+@pytest.mark.parametrize("xshape,ashape", [((1,), (1,)), ((1, 1), (1,)), ((6, 1), (1,)), ((1, 7), (7,))])
+def test_single_element_extents(fused_module, xshape, ashape):
+    """One-element extents (the reference's broadcast algebra, tensor.py:108-140):
+    forward and gradient values against the oracle."""
+    rng = np.random.default_rng(len(xshape) * 10 + sum(xshape))
+    x = rng.uniform(-2, 2, xshape)
+    a = rng.uniform(-2, 2, ashape)
+    b = rng.uniform(-2, 2, ashape)
+    yb = rng.uniform(-1, 1, xshape)
+    args = [torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()]
+    y = F.fused_map(fused_module, "affsig", args)
+    _, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", args, torch.from_numpy(yb).cuda())
+    torch.cuda.synchronize()
+    p, parts = OS.vec_eval(fused_module, "affsig", [a, x, b])
+    assert max_rel(y, p) <= 1e-13
+    assert max_rel(dx, yb * parts[1]) <= 1e-13
+    assert max_rel(da, OS.reduce_to(yb * parts[0], ashape)) <= 1e-12
+    assert max_rel(db, OS.reduce_to(yb * parts[2], ashape)) <= 1e-12
