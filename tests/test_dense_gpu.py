@@ -618,3 +618,78 @@ def test_deferred_splitk_is_bit_identical(sizes):
     assert torch.equal(out, ref)
     with pytest.raises(Exception):
         gemm(A, Bm, a_mn=True, b_mn=True, out=out, split_part=part[:10])
+
+
+def _bf16(x):
+    """Round to bfloat16 (nearest even), back to float64."""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_tiny_batches_bf16_layer_path_matches_bf16_arithmetic(B):
+    """One and three rows through the bf16 layer-by-layer path (a layer too
+    wide for the one-launch step): the 1-SM GEMM kernels at M = 1 / 3 and
+    the memory-bound kernels' tail blocks, against a numpy restatement that
+    rounds exactly where the bf16 path stores (X, W, the activations, the
+    seeds dz the GEMMs read; the bias gradients sum the fp32 seeds) and
+    accumulates in fp64.  With U(-1, 1) targets the MSE seed
+    z - y of a single row cancels most of z's digits: against pure fp64 the
+    bf16 path is 9 % off on dW here -- and so is this restatement, so the
+    kernels are checked against the arithmetic they implement (1e-3)."""
+    rng = np.random.default_rng(40 + B)
+    sizes = (33, 1100, 7)
+    chain = Chain(Dense(33, 1100, "relu"), Dense(1100, 7, "identity")).init_params(rng)
+    for l in chain.layers:
+        l.b = rng.uniform(-0.1, 0.1, l.fan_out).astype(np.float32)
+    X = rng.uniform(0, 1, (B, 33)).astype(np.float32)
+    Y = rng.uniform(-1, 1, (B, 7)).astype(np.float32)
+    tr = Trainer(chain, B, loss="mse", precision="bf16")
+    assert tr.engine.small is None
+    lv, ((gW0, gb0), (gW1, gb1)) = tr.gradient(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+    (W0, b0), (W1, b1) = [(l.W.astype(np.float64), l.b.astype(np.float64)) for l in chain.layers]
+    x, w0, w1 = _bf16(X), _bf16(W0), _bf16(W1)
+    z0 = x @ w0.T + b0
+    h1 = _bf16(np.maximum(z0, 0.0))
+    z = h1 @ w1.T + b1
+    d = z - Y
+    dzf = 2.0 * d / B                      # the seed in fp32: its column sums are db (epilogue)
+    dz = _bf16(dzf)                        # stored bf16: what the dW / dX GEMMs read
+    dz0f = (dz @ w1) * (z0 > 0)
+    dz0 = _bf16(dz0f)
+    want = {"loss": float((d * d).sum() / B), "gW1": dz.T @ h1, "gb1": dzf.sum(0), "gW0": dz0.T @ x,
+            "gb0": dz0f.sum(0)}
+    assert abs(lv - want["loss"]) <= 1e-3 * max(1.0, abs(want["loss"]))
+    for name, got in (("gW1", gW1), ("gb1", gb1), ("gW0", gW0), ("gb0", gb0)):
+        assert nrel(got, want[name]) <= 1e-3, name
+
+
+@pytest.mark.parametrize("sizes,acts,loss,B", [
+    ((33, 1100, 7), ("relu", "identity"), "mse", 1),
+    ((33, 1100, 7), ("relu", "identity"), "mse", 3),
+    ((40, 24, 24, 24, 24, 24, 3), ("tanh",) * 5 + ("identity",), "softmax_xent", 3),
+])
+def test_tiny_batches_tf32_layer_path_vs_oracle(sizes, acts, loss, B):
+    """The same tiny batches in TF32 (fp32 activations) against the fp64
+    oracle, at the north star's 1e-2: with one to three rows nothing
+    averages the operands' 2^-11 roundings over six layers."""
+    rng = np.random.default_rng(B + len(sizes))
+    chain = Chain(*[Dense(sizes[i], sizes[i + 1], acts[i]) for i in range(len(acts))]).init_params(rng)
+    for l in chain.layers:
+        l.b = rng.uniform(-0.1, 0.1, l.fan_out).astype(np.float32)
+    X = rng.uniform(0, 1, (B, sizes[0])).astype(np.float32)
+    if loss == "softmax_xent":
+        Y = np.zeros((B, sizes[-1]), np.float32)
+        Y[np.arange(B), rng.integers(0, sizes[-1], B)] = 1
+    else:
+        Y = rng.uniform(-1, 1, (B, sizes[-1])).astype(np.float32)
+    tr = Trainer(chain, B, loss=loss, precision="tf32")
+    assert tr.engine.small is None  # the layer-by-layer path
+    lv, grads = tr.gradient(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+    params = [(l.W.astype(np.float64), l.b.astype(np.float64)) for l in chain.layers]
+    lo, go, _ = OD.mlp_step(params, X.astype(np.float64), Y.astype(np.float64), acts, loss, mode="blas")
+    assert abs(lv - lo) <= 1e-2 * max(1.0, abs(lo))
+    for (gW, gb), (oW, ob) in zip(grads, go):
+        assert nrel(gW, oW) <= 1e-2
+        assert nrel(gb, ob) <= 1e-2
