@@ -693,3 +693,33 @@ def test_tiny_batches_tf32_layer_path_vs_oracle(sizes, acts, loss, B):
     for (gW, gb), (oW, ob) in zip(grads, go):
         assert nrel(gW, oW) <= 1e-2
         assert nrel(gb, ob) <= 1e-2
+
+
+def test_trainer_accepts_batch_dtypes_and_layouts():
+    """Trainer.step on the same batch given as fp32, fp64 and bf16-exact
+    values, with Y contiguous, row-padded (a strided slice) or fp64: the
+    minibatch load casts with sg_cast_2d and the loss reads unit-stride rows
+    in place, so every form trains to the same bits; host tensors are refused
+    with a ValueError (no silent copy inside a captured step)."""
+    rng = np.random.default_rng(21)
+    sizes, acts, B = (64, 96, 48), ("tanh", "identity"), 640
+    Xb = torch.from_numpy(rng.uniform(0, 1, (B, 64)).astype(np.float32)).to(torch.bfloat16).float().cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, 48)).astype(np.float32)).cuda()
+    Ypad = torch.zeros((B, 56), device="cuda")
+    Ypad[:, :48] = Y
+    variants = {"f32": (Xb, Y), "f64": (Xb.double(), Y.double()), "bf16 X": (Xb.to(torch.bfloat16), Y),
+                "padded Y": (Xb, Ypad[:, :48])}
+    out = {}
+    for name, (X, Yv) in variants.items():
+        chain = Chain(Dense(64, 96, "tanh"), Dense(96, 48, "identity")).init_params(np.random.default_rng(2))
+        tr = Trainer(chain, B, loss="mse", lr=1e-2, precision="bf16", small=False)
+        losses = [float(tr.step(X, Yv).item()) for _ in range(3)]
+        out[name] = (losses, tr.engine.P.clone())
+    ref = out["f32"]
+    for name, (losses, P) in out.items():
+        assert losses == ref[0], name
+        assert torch.equal(P, ref[1]), name
+    chain = Chain(Dense(64, 96, "tanh"), Dense(96, 48, "identity")).init_params(np.random.default_rng(2))
+    tr = Trainer(chain, B, loss="mse", precision="bf16", small=False)
+    with pytest.raises(ValueError, match="device tensor"):
+        tr.step(Xb.cpu(), Y)
