@@ -429,3 +429,41 @@ def test_single_element_extents(fused_module, xshape, ashape):
     assert max_rel(dx, yb * parts[1]) <= 1e-13
     assert max_rel(da, OS.reduce_to(yb * parts[0], ashape)) <= 1e-12
     assert max_rel(db, OS.reduce_to(yb * parts[2], ashape)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("xshape,ashape", [((1 << 20,), None), ((1 << 20,), (1 << 20,)), ((1, 1 << 18), (1 << 18,)),
+                                           ((1 << 18, 1), (1 << 18, 1)), ((1000003,), (1,))])
+def test_long_one_dimensional_extents(fused_module, dtype, xshape, ashape):
+    """1-D and single-row / single-column problems of up to 2^20 elements (the
+    runtime folds a long row into rows of a power-of-two width, or walks a
+    column operand per row): values and the broadcast cotangents (full
+    reductions for scalars, reduce_to otherwise) against the oracle."""
+    rng = np.random.default_rng(sum(xshape))
+    x = rng.uniform(-2, 2, xshape)
+    yb = rng.uniform(-1, 1, xshape)
+    if ashape is None:
+        a, b = 0.7, -0.3
+        args = [a, torch.from_numpy(x).to(dtype).cuda(), b]
+        host = [a, x, b]
+    else:
+        a = rng.uniform(-2, 2, ashape)
+        b = rng.uniform(-2, 2, ashape)
+        args = [torch.from_numpy(a).to(dtype).cuda(), torch.from_numpy(x).to(dtype).cuda(),
+                torch.from_numpy(b).to(dtype).cuda()]
+        host = [a, x, b]
+    if dtype == torch.float32:  # the oracle sees the fp32 inputs the device sees
+        host = [h if isinstance(h, float) else h.astype(np.float32).astype(np.float64) for h in host]
+        yb = yb.astype(np.float32).astype(np.float64)
+    y = F.fused_map(fused_module, "affsig", args)
+    _, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", args, torch.from_numpy(yb).to(dtype).cuda())
+    p, parts = OS.vec_eval(fused_module, "affsig", host)
+    tol = TOL[dtype]
+    assert max_rel(y, p) <= tol
+    assert max_rel(dx, yb * parts[1]) <= tol
+    for got, part, h in ((da, parts[0], host[0]), (db, parts[2], host[2])):
+        if isinstance(h, float):
+            want = float((yb * part).sum())
+            assert abs(float(got.reshape(-1)[0]) - want) <= max(tol, 1e-12) * np.abs(yb * part).sum()
+        else:
+            assert max_rel(got, OS.reduce_to(yb * part, h.shape)) <= max(tol, 1e-12) * 10
