@@ -572,7 +572,7 @@ def test_fused_mse_loss_matches_separate_loss_kernel(sizes, B):
         assert torch.equal(G0[wo:bo], G1[wo:bo])
 
 
-@pytest.mark.parametrize("sizes", [(256, 384, 256, 128), (300, 333, 130, 72)])
+@pytest.mark.parametrize("sizes", [(256, 384, 256, 128), (300, 333, 130, 72), (96, 48, 40, 24)])
 def test_deferred_splitk_is_bit_identical(sizes):
     """Deferred split-K (a dW GEMM's partials left in its own buffer, every
     layer's reduced in one sg_splitk_reduce_multi launch after the pullback)
