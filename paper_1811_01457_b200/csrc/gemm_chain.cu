@@ -358,7 +358,10 @@ gemm_chain_kernel(const __grid_constant__ Params P) {
       if (ew == 0 && lane == 0) SG_TRACE(i - u0, 1);  // accumulator complete
       auto publish_pending = [&]() {
         if (pend_mb >= 0) {
-          signal_rows_deferred(P, P.probs[pend_prob], pend_mb, lane, chunk_groups(p));
+          // the groups chunk 0 committed: none when this warp's 32-row group
+          // lies past M (epi_chunk returns before its stores) -- then every
+          // pending group is the published unit's and must complete
+          signal_rows_deferred(P, P.probs[pend_prob], pend_mb, lane, row0 < p.M ? chunk_groups(p) : 0);
           pend_mb = -1;
         }
       };
