@@ -494,7 +494,7 @@ np.save(sys.argv[1], np.concatenate([e.G.double().cpu().numpy(), e.loss.cpu().nu
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520), (777, 522)])
+@pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520), (777, 522), (100, 72), (200, 40)])
 def test_value_and_pullback_fuses_the_seed(M, D):
     """DenseLayer.value_and_pullback (the forward GEMM's epilogue also forms
     dZ = ybar .* act'(H) and its column sums) against the same layer's
