@@ -741,6 +741,10 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         finally:
             del os.environ["SGB200_CHAIN"]
     flops = tr.engine.flops_per_step() * world
+    # bytes the step touches: parameters (fp32 + bf16 shadow + gradients) and
+    # the per-layer activations / cotangents (bf16) of this rank's batch
+    n_par = sum(sizes[i] * sizes[i + 1] + sizes[i + 1] for i in range(len(acts)))
+    ws_mb = (n_par * 10 + lb * sum(sizes) * 2 * 3 + lb * (sizes[0] + sizes[-1]) * 4) / 1e6
     tr.close()
     tflops = flops / (ms * 1e-3) / 1e12
     if small:  # latency-bound: the roofline is the launch, not a pipe
@@ -760,6 +764,9 @@ def mlp_bench(args, world, rank, dist, peaks, name, sizes, acts, batch, loss, gr
         "flops_per_step": flops, "TFLOPs": round(tflops, 1),
         "roofline": roof,
         "compute_precision": tr.compute_precision, "clocks": clk.summary(),
+        "l2": (f"working set ~{ws_mb:.0f} MB per step > 126 MB L2 (no flush needed)" if ws_mb > 126 else
+               f"working set ~{ws_mb:.1f} MB per step stays L2-resident between steps (no flush: the step is "
+               "latency-bound, one launch; a flush would dominate it)"),
         "cuda_graph": bool(tr.use_graph) and not small, "loss_last": loss_v, "n_gpus": world,
         "gpu_launches_per_step": launches,
         "ms_per_step_without_graph": None if no_graph_ms is None else round(no_graph_ms, 4),
