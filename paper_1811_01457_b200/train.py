@@ -194,6 +194,7 @@ class Trainer:
         # library's communicator is stream-ordered and can live in a graph
         self.use_graph = graph and (self.dp is None or isinstance(self.dp, NcclDataParallel))
         self._graphs = collections.OrderedDict()  # (X, Y) buffers -> captured step (LRU)
+        self._seen = collections.OrderedDict()    # pairs stepped once, not captured yet (LRU)
         self._last_key = None
         self._small_key = self._small_graph = None  # one-launch step: replayed graph per (X, Y, lr)
 
@@ -242,12 +243,19 @@ class Trainer:
         # and later ones replay.  A few pairs are kept (double-buffered loaders).
         key = (X.data_ptr(), Y.data_ptr(), tuple(X.shape), tuple(Y.shape), X.stride(0), Y.stride(0),
                X.dtype, Y.dtype)
+        # (a pair is captured on its second step, consecutive or not, so
+        # loaders that alternate a few buffers replay too)
         g = self._graphs.get(key)
-        if g is None and self._last_key == key:
+        if g is None and key in self._seen:
             g = Tape.capture(lambda: (self.engine.load_batch(X, Y), self._device_step()), warmup=0)
             self._graphs[key] = g
+            del self._seen[key]
             while len(self._graphs) > self.MAX_GRAPHS:
                 self._graphs.popitem(last=False)
+        elif g is None:
+            self._seen[key] = True
+            while len(self._seen) > 4 * self.MAX_GRAPHS:
+                self._seen.popitem(last=False)
         self._last_key = key
         if g is not None:
             self._graphs.move_to_end(key)

@@ -723,3 +723,22 @@ def test_trainer_accepts_batch_dtypes_and_layouts():
     tr = Trainer(chain, B, loss="mse", precision="bf16", small=False)
     with pytest.raises(ValueError, match="device tensor"):
         tr.step(Xb.cpu(), Y)
+
+
+def test_graph_replay_with_alternating_batches():
+    """A loader that alternates two minibatch buffers: each (X, Y) pair is
+    captured on its second step (not only on back-to-back repeats) and
+    replayed after; the losses and parameters equal the eager run's bit for bit."""
+    rng = np.random.default_rng(17)
+    sizes, acts, B = (128, 256, 64), ("tanh", "identity"), 512
+    pairs = [(torch.from_numpy(rng.uniform(0, 1, (B, 128)).astype(np.float32)).cuda(),
+              torch.from_numpy(rng.uniform(-1, 1, (B, 64)).astype(np.float32)).cuda()) for _ in range(2)]
+    runs = {}
+    for graph in (False, True):
+        chain = Chain(Dense(128, 256, "tanh"), Dense(256, 64, "identity")).init_params(np.random.default_rng(3))
+        tr = Trainer(chain, B, loss="mse", lr=1e-2, precision="bf16", graph=graph, small=False)
+        losses = [float(tr.step(*pairs[i % 2]).item()) for i in range(8)]
+        runs[graph] = (losses, tr.engine.P.clone(), len(tr._graphs))
+    assert runs[True][2] == 2  # both pairs captured
+    assert runs[False][0] == runs[True][0]
+    assert torch.equal(runs[False][1], runs[True][1])
