@@ -196,7 +196,7 @@ class Trainer:
         self._graphs = collections.OrderedDict()  # (X, Y) buffers -> captured step (LRU)
         self._seen = collections.OrderedDict()    # pairs stepped once, not captured yet (LRU)
         self._last_key = None
-        self._small_key = self._small_graph = None  # one-launch step: replayed graph per (X, Y, lr)
+        self._small_graph = None  # the one-launch step last replayed (graphs keyed per (X, Y, lr) in _graphs)
 
     def _device_step(self):
         # NVTX ranges per phase (the C-ABI calls inside carry their own)
@@ -223,15 +223,24 @@ class Trainer:
             # a CUDA-graph replay issues it in ~3 us of host time instead of
             # the ~9 us of a cooperative launch (the c1 step is a 16 us kernel):
             # first call per (X, Y, lr) eager, the next one captures, then replays
-            key = (X.data_ptr(), Y.data_ptr(), tuple(X.shape), tuple(Y.shape), X.stride(0), Y.stride(0),
+            key = ("small", X.data_ptr(), Y.data_ptr(), tuple(X.shape), tuple(Y.shape), X.stride(0), Y.stride(0),
                    X.dtype, Y.dtype, self.lr)
-            if self._small_key == key:
-                if self._small_graph is None:
-                    self._small_graph = Tape.capture(lambda: self.engine.small_step(X, Y, self.lr), warmup=0)
-                self._small_graph.replay()
-                return self.engine.loss
-            self._small_key, self._small_graph = key, None
-            return self.engine.small_step(X, Y, self.lr)
+            g = self._graphs.get(key)
+            if g is None and key in self._seen:  # second step on this pair: capture (as below)
+                g = Tape.capture(lambda: self.engine.small_step(X, Y, self.lr), warmup=0)
+                self._graphs[key] = g
+                del self._seen[key]
+                while len(self._graphs) > self.MAX_GRAPHS:
+                    self._graphs.popitem(last=False)
+            elif g is None:
+                self._seen[key] = True
+                while len(self._seen) > 4 * self.MAX_GRAPHS:
+                    self._seen.popitem(last=False)
+                return self.engine.small_step(X, Y, self.lr)
+            self._graphs.move_to_end(key)
+            self._small_graph = g
+            g.replay()
+            return self.engine.loss
         if not self.use_graph:
             self.engine.load_batch(X, Y)
             self._device_step()
