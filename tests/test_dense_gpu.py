@@ -742,3 +742,36 @@ def test_graph_replay_with_alternating_batches():
     assert runs[True][2] == 2  # both pairs captured
     assert runs[False][0] == runs[True][0]
     assert torch.equal(runs[False][1], runs[True][1])
+
+
+@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 1000, 1024])
+@pytest.mark.parametrize("precision", ["tf32", "strict_fp64"])
+def test_softmax_xent_class_counts(N, precision):
+    """The softmax cross-entropy loss kernel across its two layouts (rows of
+    <= 128 classes per warp group, wider rows per block) and their edges, up
+    to its 1024-class limit: loss and gradients against the oracle; 1025
+    classes are refused with a ValueError."""
+    rng = np.random.default_rng(N)
+    B = 300
+    chain = Chain(Dense(16, N, "identity")).init_params(rng)
+    chain.layers[0].b = rng.uniform(-0.5, 0.5, N).astype(np.float32)
+    X = rng.uniform(-1, 1, (B, 16)).astype(np.float32)
+    Y = np.zeros((B, N), np.float32)
+    Y[np.arange(B), rng.integers(0, N, B)] = 1
+    tr = Trainer(chain, B, loss="softmax_xent", precision=precision, small=False)
+    lv, ((gW, gb),) = tr.gradient(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+    params = [(chain.layers[0].W.astype(np.float64), chain.layers[0].b.astype(np.float64))]
+    lo, ((oW, ob),), _ = OD.mlp_step(params, X.astype(np.float64), Y.astype(np.float64), ("identity",),
+                                     "softmax_xent", mode="blas")
+    tol = TOL[precision]
+    assert abs(lv - lo) <= tol * max(1.0, abs(lo))
+    assert nrel(gW, oW) <= tol and nrel(gb, ob) <= tol
+
+
+def test_softmax_xent_refuses_too_many_classes():
+    chain = Chain(Dense(16, 1025, "identity")).init_params(np.random.default_rng(0))
+    tr = Trainer(chain, 64, loss="softmax_xent", precision="tf32", small=False)
+    X = torch.zeros((64, 16), device="cuda")
+    Y = torch.zeros((64, 1025), device="cuda")
+    with pytest.raises(ValueError, match="1024 classes"):
+        tr.gradient(X, Y)
