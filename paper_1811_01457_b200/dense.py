@@ -479,7 +479,11 @@ class ChainEngine:
             gemm_chain = "full"
         if gemm_chain not in (None, False, "full", "pairwise", "forward"):
             raise ValueError(f"unknown gemm_chain mode {gemm_chain!r}")
-        self.chainable = bool(gemm_chain) and precision == "bf16" and self.L >= 2
+        # (a chain's backward holds 2 L - 1 GEMMs: deeper chains run layer by layer)
+        from .gemm import CHAIN_MAX_PROBLEMS
+
+        self.chainable = (bool(gemm_chain) and precision == "bf16" and self.L >= 2
+                          and 2 * self.L - 1 <= CHAIN_MAX_PROBLEMS)
         self.chain_mode = gemm_chain if self.chainable else None
         self.chains = None
         if self.chainable:

@@ -268,6 +268,11 @@ class ChainProblem(ctypes.Structure):  # sg_chain_problem
                 ("dep_kind", ctypes.c_int32 * 2), ("dep_on", ctypes.c_int32 * 2)]
 
 
+# problems per chain: their descriptions fill the 32 KB kernel parameter space
+# (gemm_chain.cu MAX_PROBS; sg_chain_create refuses more)
+CHAIN_MAX_PROBLEMS = 84
+
+
 class GemmChain:
     """A persistent GEMM chain (``sg_chain_*``, include/sgb200.h): a list of
     GEMMs -- each a :class:`GemmDesc` with optional dependencies on earlier

@@ -269,3 +269,14 @@ def test_broadcast_rule_rejects_empty_operands_like_the_reference():
             _broadcast([np.zeros(s) for s in shapes])
     with pytest.raises(ValueError, match="do not broadcast"):
         _broadcast([np.zeros((3,)), np.zeros((4,))])
+
+
+def test_chain_problem_limit_matches_the_library():
+    """gemm.CHAIN_MAX_PROBLEMS (ChainEngine falls back to the layer path above
+    it) is the kernel's own MAX_PROBS (gemm_chain.cu)."""
+    import re as _re
+
+    from paper_1811_01457_b200.gemm import CHAIN_MAX_PROBLEMS
+
+    src = open(os.path.join(ROOT, "paper_1811_01457_b200", "csrc", "gemm_chain.cu")).read()
+    assert int(_re.search(r"constexpr int MAX_PROBS = (\d+);", src).group(1)) == CHAIN_MAX_PROBLEMS
