@@ -281,7 +281,7 @@ def broadcast_bench(args, world, rank, local, dist):
     # Consecutive steps overlap too: a chunk's buffers are reused as soon as
     # the previous step is done with them (per-chunk events guard the
     # write-after-read hazards), so the pipeline fills once per timed run.
-    nch = next(c for c in (32, 16, 8, 1) if R % c == 0)
+    nch = next(c for c in (int(os.environ.get("SGB200_E2E_CHUNKS", "16")), 16, 8, 1) if R % c == 0)
     rc = R // nch
     s_in, s_cp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     apart = torch.empty((nch, C), device="cuda")
