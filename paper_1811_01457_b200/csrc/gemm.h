@@ -28,6 +28,7 @@ struct GemmEpilogue {
   const float* seed = nullptr; // BIAS_ACT_SEED: cotangent of the activation, fp32 [M][ld_seed]
   long long ld_seed = 0;
   __nv_bfloat16* out2_bf16 = nullptr;  // BIAS_ACT_SEED: seed .* act'(h); BIAS_MSE: dz; bf16 [M][ld_out2]
+  float* out2_f32 = nullptr;           // BIAS_ACT_SEED in TF32: seed .* act'(h), fp32 [M][ld_out2]
   long long ld_out2 = 0;
   double* loss_part = nullptr;          // BIAS_MSE: [ceil(M/32)][ceil(N/32)] partial losses
   float loss_scale = 0.0f;

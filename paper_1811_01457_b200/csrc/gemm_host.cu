@@ -25,8 +25,11 @@ extern "C" int sg_gemm(sg_ctx* ctx, const sg_gemm_desc* d, void* stream) {
        d->out_lp || d->batch > 1))
     return fail(SG_EINVAL, "gemm: BIAS_MSE needs BF16, identity, targets in aux, out2_lp and loss_part, no out_lp");
   if (d->epilogue == SG_EPI_BIAS_ACT_SEED &&
-      (d->precision != SG_PREC_BF16 || !d->aux || !d->out_lp || !d->out2_lp || d->out || d->batch > 1))
-    return fail(SG_EINVAL, "gemm: BIAS_ACT_SEED needs BF16, the seed in aux, out_lp and out2_lp, and no fp32 out");
+      (!d->aux || !d->out2_lp || d->batch > 1 ||
+       !((d->precision == SG_PREC_BF16 && d->out_lp && !d->out) ||
+         (d->precision == SG_PREC_TF32 && d->out && !d->out_lp))))
+    return fail(SG_EINVAL, "gemm: BIAS_ACT_SEED needs the seed in aux and out2_lp, with BF16 out_lp (no fp32 out) "
+                           "or TF32 out (fp32 h and out2)");
   if (d->act < SG_ACT_IDENTITY || d->act > SG_ACT_RELU) return fail(SG_EINVAL, "gemm: bad activation");
   if (d->epilogue == SG_EPI_ACT_GRAD && !d->aux) return fail(SG_EINVAL, "gemm: ACT_GRAD needs aux");
   const long long batch = d->batch < 1 ? 1 : d->batch;
@@ -94,9 +97,11 @@ void gemm_args_from_desc(sg_ctx* ctx, const sg_gemm_desc* d, GemmArgs& g) {
   }
   if (d->epilogue == SG_EPI_BIAS_ACT_SEED) {
     g.epi.aux = nullptr;  // the seed travels in aux: fp32, read per row in the epilogue
+    g.epi.aux_f32 = nullptr;
     g.epi.seed = (const float*)d->aux;
     g.epi.ld_seed = d->ld_aux;
-    g.epi.out2_bf16 = (__nv_bfloat16*)d->out2_lp;
+    if (tf32) g.epi.out2_f32 = (float*)d->out2_lp;  // TF32: h and dz in fp32
+    else g.epi.out2_bf16 = (__nv_bfloat16*)d->out2_lp;
     g.epi.ld_out2 = d->ld_out2;
   }
   g.split_part = d->split_part;

@@ -663,8 +663,9 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
 #pragma unroll
       for (int i = 0; i < 32; ++i) sd[i] = 0.0f;
     }
+    if (e.out_bf16)  // the bf16 activation as stored (TF32: the fp32 one as it is)
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+      for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
     act_grad_chunk(sd, v, e.act);  // sd *= act'(h)
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = sd[i];
@@ -673,7 +674,8 @@ __device__ __forceinline__ void epi_chunk(const KParams& p, float (&v)[32], int 
       warp_tma_store<true>(slot, map_f32, v, lane, n0, row0, bidx);  // buffer 0, after every read of it
       if (WIDE) *next_buf = 1;
     } else if (row_ok) {
-      store_row_bf16(e.out2_bf16 + (long long)m * e.ld_out2 + n0, v, nn);
+      if (e.out2_f32) store_row_f32(e.out2_f32 + (long long)m * e.ld_out2 + n0, v, nn);
+      else store_row_bf16(e.out2_bf16 + (long long)m * e.ld_out2 + n0, v, nn);
     }
   }
   SG_CPROF(3);  // stores issued

@@ -204,13 +204,16 @@ def gemm_desc(A, B, *, M=None, N=None, K=None, a_mn=False, b_mn=False, precision
     if epilogue == "bias_act_seed":
         import torch
 
-        if precision != "bf16" or seed is None or out_lp is None or out2_lp is None or out is not None:
-            raise ValueError("gemm: bias_act_seed needs bf16, seed, out_lp and out2_lp, and no fp32 out")
+        # bf16: h in out_lp, dz in out2_lp (bf16); tf32: h in out, dz in out2_lp (fp32)
+        bf = precision == "bf16"
+        if (precision not in ("bf16", "tf32") or seed is None or out2_lp is None
+                or (bf and (out_lp is None or out is not None)) or (not bf and (out is None or out_lp is not None))):
+            raise ValueError("gemm: bias_act_seed needs seed and out2_lp, with out_lp (bf16) or out (tf32)")
         for name, t in (("seed", seed), ("out2_lp", out2_lp)):
             if t.dim() != 2 or t.shape[0] < M or t.shape[1] < N:
                 raise ValueError(f"gemm: {name} of shape {tuple(t.shape)} cannot hold the {M} x {N} result")
-        if seed.dtype != torch.float32 or out2_lp.dtype != torch.bfloat16:
-            raise ValueError("gemm: seed must be float32 and out2_lp bfloat16")
+        if seed.dtype != torch.float32 or out2_lp.dtype != (torch.bfloat16 if bf else torch.float32):
+            raise ValueError("gemm: seed must be float32 and out2_lp bfloat16 (bf16) / float32 (tf32)")
         aux = seed  # the descriptor carries the seed in aux
     elif epilogue == "bias_mse":
         import torch

@@ -775,3 +775,34 @@ def test_softmax_xent_refuses_too_many_classes():
     Y = torch.zeros((64, 1025), device="cuda")
     with pytest.raises(ValueError, match="1024 classes"):
         tr.gradient(X, Y)
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 1024, 512), (1000, 520, 200), (100, 72, 64)])
+def test_tf32_seeded_forward_matches_separate_act_grad(M, N, K):
+    """TF32 BIAS_ACT_SEED (h and dz = seed .* act'(h) in fp32 from one GEMM
+    epilogue, with the bias-gradient partials) against the TF32 forward plus
+    the separate sg_act_grad kernel: h and dz bit-identical (the same fp32
+    arithmetic), the column sums equal up to their summation order."""
+    from paper_1811_01457_b200 import runtime as rt
+    from paper_1811_01457_b200.dense import ACT, _dt, _lib, _p
+    from paper_1811_01457_b200.gemm import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    X = torch.rand((M, K), generator=g, device="cuda") * 2 - 1
+    W = (torch.rand((N, K), generator=g, device="cuda") * 2 - 1) * K ** -0.5
+    b = (torch.rand(N, generator=g, device="cuda") * 2 - 1) * 0.1
+    seed = torch.rand((M, N), generator=g, device="cuda") * 2 - 1
+    G = (M + 31) // 32
+    h1, dz1, cs1 = torch.empty((M, N), device="cuda"), torch.empty((M, N), device="cuda"), torch.zeros((G, N), device="cuda")
+    gemm(X, W, precision="tf32", epilogue="bias_act_seed", act="sigmoid", bias=b, seed=seed, out=h1, out2_lp=dz1,
+         colsum=cs1)
+    h0, dz0, cs0 = torch.empty_like(h1), torch.empty_like(dz1), torch.zeros_like(cs1)
+    gemm(X, W, precision="tf32", epilogue="bias_act", act="sigmoid", bias=b, out=h0)
+    lib = _lib()
+    rt.check(lib.sg_act_grad(rt.context(), _p(seed), _dt(seed), seed.stride(0), _p(h0), _dt(h0), h0.stride(0), M, N,
+                             ACT["sigmoid"], _p(dz0), _dt(dz0), dz0.stride(0), None, 0, 0, _p(cs0), cs0.stride(0),
+                             rt.stream_ptr()), "sg_act_grad")
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h0)
+    assert torch.equal(dz1, dz0)
+    assert float((cs1.double().sum(0) - cs0.double().sum(0)).abs().max()) <= 1e-5 * float(cs0.abs().sum(0).max())
