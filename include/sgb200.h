@@ -187,7 +187,8 @@ typedef struct sg_gemm_desc {
    * take the STORE / BIAS_ACT epilogues (bias shared) without colsum/out_pre. */
   int64_t batch;
   int64_t stride_a, stride_b, stride_out, stride_lp;
-  void* out2_lp; /* BIAS_ACT_SEED: bf16 [M][ld_out2] seed .* act'(out_lp); BIAS_MSE: dz */
+  void* out2_lp; /* BIAS_ACT_SEED: [M][ld_out2] seed .* act'(h) -- bf16 (h in out_lp) for BF16,
+                  * fp32 (h in out) for TF32; BIAS_MSE: dz (bf16) */
   int64_t ld_out2;
   double* loss_part; /* BIAS_MSE: [ceil(M/32)][ceil(N/32)] partial losses */
   double loss_scale; /* BIAS_MSE: scale (1 / global batch) */
