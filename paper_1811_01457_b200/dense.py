@@ -328,15 +328,17 @@ class DenseLayer:
         """Forward and pullback with the output cotangent known up front (the
         reference's ``grad`` with seeds, reverse_ad.py:633-663): ONE forward
         GEMM whose epilogue also forms dZ = ybar .* act'(H) and its column sums
-        (``bias_act_seed``), then dX and dW -- no separate act' pass.  bf16."""
+        (``bias_act_seed``), then dX and dW -- no separate act' pass.  bf16 or TF32."""
         from .gemm import gemm
 
-        if self.precision != "bf16":
-            raise ValueError("value_and_pullback is the bf16 tensor-core path")
         if X is not None:
             cast_rows(X, self.X)
-        gemm(self.X, self.Wb, epilogue="bias_act_seed", act=self.act, bias=self.b, seed=ybar, out_lp=self.H,
-             out2_lp=self.dZ, colsum=self.colsum)
+        if self.precision == "bf16":
+            gemm(self.X, self.Wb, epilogue="bias_act_seed", act=self.act, bias=self.b, seed=ybar, out_lp=self.H,
+                 out2_lp=self.dZ, colsum=self.colsum)
+        else:  # TF32: h and dz in fp32
+            gemm(self.X, self.Wb, precision="tf32", epilogue="bias_act_seed", act=self.act, bias=self.b, seed=ybar,
+                 out=self.H, out2_lp=self.dZ, colsum=self.colsum)
         dense_backward(self.desc(), self.dZ, self.dW, self.db, dX=self.dX if need_dx else None,
                        colsum_in=self.colsum)
         return self.H, self.dX, self.dW, self.db

@@ -494,8 +494,9 @@ np.save(sys.argv[1], np.concatenate([e.G.double().cpu().numpy(), e.loss.cpu().nu
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
 @pytest.mark.parametrize("M,D", [(8192, 4096), (1000, 520), (777, 522), (100, 72), (200, 40)])
-def test_value_and_pullback_fuses_the_seed(M, D):
+def test_value_and_pullback_fuses_the_seed(M, D, precision):
     """DenseLayer.value_and_pullback (the forward GEMM's epilogue also forms
     dZ = ybar .* act'(H) and its column sums) against the same layer's
     forward + separate act' + pullback and an fp64 evaluation: c3 at full size
@@ -507,7 +508,7 @@ def test_value_and_pullback_fuses_the_seed(M, D):
     ybar = torch.rand((M, D), generator=g, device="cuda") * 2 - 1
     outs = []
     for fused in (False, True):
-        layer = DenseLayer(M, D, D, "sigmoid", precision="bf16")
+        layer = DenseLayer(M, D, D, "sigmoid", precision=precision)
         layer.set_params(W.cpu().numpy(), b.cpu().numpy())
         if fused:
             H, dX, dW, db = layer.value_and_pullback(ybar, X)
