@@ -495,3 +495,30 @@ def test_fuzz_corpus_in_fp32():
         worst = max([worst, max_rel(p32.double(), p64)] + [max_rel(u.double(), v) for u, v in zip(parts32, parts64)]
                     + [max_rel(u.double(), v) for u, v in zip(cots32, parts64)])
     assert worst <= 1e-6, worst
+
+
+def test_repeated_calls_do_not_grow_device_memory(fused_module):
+    """Operands that do not fit the 2-D broadcast pattern are expanded into
+    stream-ordered temporaries, and broadcast cotangents use partial-sum
+    buffers: every call frees them (and its error paths do too, RAII), so
+    device memory is flat over many calls -- only the first calls warm the
+    pool."""
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.uniform(-2, 2, (64, 3, 257))).cuda()
+    a = torch.from_numpy(rng.uniform(-2, 2, (64, 1, 257))).cuda()  # not a 2-D pattern: expanded
+    b = torch.from_numpy(rng.uniform(-2, 2, (3, 1))).cuda()
+    yb = torch.from_numpy(rng.uniform(-1, 1, (64, 3, 257))).cuda()
+
+    def call():
+        F.fused_map(fused_module, "affsig", [a, x, b])
+        F.fused_map_grad(fused_module, "affsig", [a, x, b], yb)
+
+    for _ in range(10):
+        call()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(200):
+        call()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 <= 8 << 20, (free0, free1)
