@@ -807,3 +807,32 @@ def test_tf32_seeded_forward_matches_separate_act_grad(M, N, K):
     assert torch.equal(h1, h0)
     assert torch.equal(dz1, dz0)
     assert float((cs1.double().sum(0) - cs0.double().sum(0)).abs().max()) <= 1e-5 * float(cs0.abs().sum(0).max())
+
+
+def test_repeated_steps_and_split_gemms_do_not_grow_device_memory():
+    """Training steps (eager and graph-replayed) and split-K GEMMs with their
+    stream-ordered partial buffers: device memory stays flat over many calls."""
+    from paper_1811_01457_b200.gemm import gemm
+
+    rng = np.random.default_rng(4)
+    B = 4096
+    X = torch.from_numpy(rng.uniform(0, 1, (B, 256)).astype(np.float32)).cuda()
+    Y = torch.from_numpy(rng.uniform(-1, 1, (B, 128)).astype(np.float32)).cuda()
+    trs = [Trainer(Chain(Dense(256, 384, "tanh"), Dense(384, 128, "identity")).init_params(np.random.default_rng(1)),
+                   B, loss="mse", lr=1e-3, precision="bf16", graph=g, small=False) for g in (False, True)]
+    A = (torch.rand((16384, 256), device="cuda") - 0.5).to(torch.bfloat16)
+    out = torch.empty((256, 256), device="cuda")
+
+    def run():
+        for tr in trs:
+            tr.step(X, Y)
+        gemm(A, A, a_mn=True, b_mn=True, out=out)  # K = 16384 over 1 tile: split-K with its own partials
+
+    for _ in range(5):
+        run()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(100):
+        run()
+    torch.cuda.synchronize()
+    assert free0 - torch.cuda.mem_get_info()[0] <= 8 << 20
