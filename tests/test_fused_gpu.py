@@ -522,3 +522,26 @@ def test_repeated_calls_do_not_grow_device_memory(fused_module):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 <= 8 << 20, (free0, free1)
+
+
+def test_broadcast_beyond_two_giga_elements(fused_module):
+    """64-bit indexing in the fused kernels: 2^31 + 2^24 fp32 elements (8.7 GB
+    per array), forward and gradient checked on the first and last rows, and
+    the broadcast cotangents (sums over all rows) against fp64 row sums."""
+    R, C = (1 << 19) + (1 << 12), 4096
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.rand((R, C), generator=g, device="cuda") * 4 - 2
+    a = torch.rand(C, generator=g, device="cuda") * 4 - 2
+    b = torch.rand(C, generator=g, device="cuda") * 4 - 2
+    yb = torch.ones((R, C), device="cuda")
+    y = F.fused_map(fused_module, "affsig", [a, x, b])
+    _, (da, dx, db) = F.fused_map_grad(fused_module, "affsig", [a, x, b], yb)
+    torch.cuda.synchronize()
+    for r in (0, 1, (1 << 19) - 1, R - 1):
+        s = torch.sigmoid(a.double() * x[r].double() + b.double())
+        assert max_rel(y[r], s) <= 1e-6
+        assert max_rel(dx[r], a.double() * s * (1 - s)) <= 1e-6
+    s_all = torch.sigmoid(a.double() * x.double() + b.double())  # 17 GB in fp64: still fits
+    want_db = (s_all * (1 - s_all)).sum(0)
+    del s_all
+    assert float((db.double() - want_db).abs().max()) <= 1e-6 * float(want_db.abs().max())

@@ -308,3 +308,21 @@ def test_outputs_never_write_outside_the_result(N, out_kind):
     if out_kind == "bf16":
         want = torch.tanh(want)
     assert float((out.double() - want).abs().max()) < 0.05 * float(want.abs().max())
+
+
+def test_output_beyond_two_giga_elements():
+    """64-bit indexing: a bf16 GEMM whose fp32 output has 2^31 + 2^20 elements
+    (8.6 GB; rows past the 32-bit element range), checked on sampled rows at
+    both ends of the output against double-precision products."""
+    M, N, K = (1 << 19) + 256, 4096, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = ((torch.rand((M, K), generator=g, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    B = ((torch.rand((N, K), generator=g, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    out = torch.empty((M, N), device="cuda")
+    gemm(A, B, out=out)
+    torch.cuda.synchronize()
+    rows = torch.tensor([0, 1, 12345, (1 << 19) - 1, 1 << 19, M - 2, M - 1], device="cuda")
+    want = A[rows].double() @ B.double().T
+    got = out[rows].double()
+    assert float((got - want).abs().max()) <= 1e-4 * float(want.abs().max())
+    del out
