@@ -199,7 +199,8 @@ def test_strict_fp64_matches_reference_bit_for_bit():
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])
 @pytest.mark.parametrize("L,M,N,K,layout", [(3, 128, 256, 64, "kk"), (5, 200, 72, 136, "k_mn"),
                                             (4, 304, 520, 96, "mn_mn"), (2, 512, 512, 256, "kk"),
-                                            (6, 64, 40, 24, "k_mn")])
+                                            (6, 64, 40, 24, "k_mn"),
+                                            (1000, 64, 48, 32, "kk"), (300, 256, 256, 64, "mn_mn")])
 def test_batched_tensor_core_gemm(precision, L, M, N, K, layout):
     """One launch over L independent GEMMs (the reference's bmm, tensor.py:364-369)."""
     from paper_1811_01457_b200.gemm import bmm
@@ -219,7 +220,7 @@ def test_batched_tensor_core_gemm(precision, L, M, N, K, layout):
     torch.cuda.synchronize()
     got = out.double().cpu().numpy()
     tol = 1e-5 if precision == "bf16" else 2.0 ** -9  # bf16 inputs exact; tf32 rounds operands
-    for l in range(L):
+    for l in (range(L) if L <= 16 else sorted({0, 1, L // 2, L - 2, L - 1})):
         check_close(got[l], aq[l], bq[l].T, tol=tol)
 
 
