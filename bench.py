@@ -919,6 +919,51 @@ def reference_broadcast(rows=32):
     }
 
 
+def _ref_c2_worker_init():
+    import_reference()
+
+
+def _ref_c2_worker(job):
+    """One worker's sample (its own rows) through the unmodified reference."""
+    seed, rows = job
+    from ssagrad import DenseTensor, parse_ir
+    from ssagrad.forward_ad import fused_map_pullback, fused_map_with_partials
+    from ssagrad.ir import tensor_type
+
+    m = parse_ir(AFFSIG)
+    rng = np.random.default_rng(seed)
+    C = C_COLS
+    x = rng.uniform(-2, 2, (rows, C)).astype(np.float32).astype(np.float64)
+    a = rng.uniform(-2, 2, C).astype(np.float32).astype(np.float64)
+    b = rng.uniform(-2, 2, C).astype(np.float32).astype(np.float64)
+    yb = rng.uniform(-1, 1, (rows, C)).astype(np.float32).astype(np.float64)
+    _, parts = fused_map_with_partials(m, "affsig", [DenseTensor(a), DenseTensor(x), DenseTensor(b)])
+    fused_map_pullback(parts, [tensor_type(C), tensor_type(rows, C), tensor_type(C)], DenseTensor(yb))
+    return rows * C
+
+
+def reference_broadcast_parallel(rows=32):
+    """The reference's c2 path on ALL host cores: the reference itself is
+    single-threaded Python, and elements are independent, so one process per
+    core runs it on its own `rows` x 4096 sample (pool warmed up first: the
+    imports are not timed); throughput = all elements / wall time."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    ctx = mp.get_context("spawn")  # no fork of a process holding a CUDA context
+    with ctx.Pool(cores, initializer=_ref_c2_worker_init) as pool:
+        pool.map(_ref_c2_worker, [(i, 1) for i in range(cores)])  # warm-up: imports, first calls
+        t0 = time.perf_counter()
+        n = sum(pool.map(_ref_c2_worker, [(100 + i, rows) for i in range(cores)]))
+        sec = time.perf_counter() - t0
+    return {"value": round(n * BYTES_PER_ELEM / sec / 1e9, 6), "unit": "GB/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{cores} processes x {rows}x{C_COLS} elements (disjoint samples) through the unmodified "
+                      "reference (baseline/_ref): fused_map_with_partials + fused_map_pullback, 20 B/elem "
+                      "algorithmic; the reference is single-threaded, elements are independent",
+            "wall_s": round(sec, 3)}
+
+
 def _reference_chain_module(sizes, acts, n, loss):
     """A Dense chain's loss IR built with the reference's own emitter, exactly
     as nn_train's trunk builds layers (nn_train.py:189-196):
@@ -1021,12 +1066,15 @@ def reference_arm(args, world, rank):
     ref = import_reference()
     vals = []
     for _ in range(max(1, min(args.steps, 3))):
-        vals.append(reference_broadcast(rows=args.ref_rows) if ref else cpu_baseline_broadcast(rows=args.ref_rows))
+        vals.append(reference_broadcast_parallel(rows=args.ref_rows) if ref
+                    else cpu_baseline_broadcast(rows=args.ref_rows))
     v = statistics.median(r["value"] for r in vals)
     cb = dict(vals[-1])
     cb["value"] = v
     secondary = []
     if ref:
+        one = reference_broadcast(rows=args.ref_rows)
+        secondary.append({"workload": "c2 (reference, one core)", **one})
         secondary += [
             reference_mlp("c1 MLP 784-32-10 train step (reference grad + SGD)", (784, 32, 10), ("sigmoid", "identity"),
                           128, "softmax_xent"),
@@ -1095,7 +1143,7 @@ def main():
     rec = broadcast_bench(args, world, rank, local, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ref = import_reference()
-        rec["cpu_baseline"] = reference_broadcast(rows=args.ref_rows) if ref else \
+        rec["cpu_baseline"] = reference_broadcast_parallel(rows=args.ref_rows) if ref else \
             cpu_baseline_broadcast(rows=args.ref_rows)
         rec["cpu_baseline"]["secondary"] = [
             reference_mlp("c1", (784, 32, 10), ("sigmoid", "identity"), 128, "softmax_xent") if ref else
